@@ -1,0 +1,147 @@
+/*
+ * kaas_b200.h -- C ABI of the B200-native KaaS executor (libkaas_b200.so).
+ *
+ * The reference (arXiv 2212.08146 artifact, pkg/src/kaas) is pure Python and
+ * has no native FFI; its "device" is host bytearrays driven by numpy.  Each
+ * entry point below replaces one device-touching step of that path; the
+ * reference call it stands in for is cited beside it.  A ctypes binding for
+ * the reference's own backend/executor classes is shown in INTEGRATION.md.
+ *
+ * Conventions
+ *   - every function returns int: 0 = ok, >0 = cudaError_t, <0 = KAAS_E_*;
+ *     kaas_last_error() returns the thread-local message of the last failure.
+ *   - device pointers, streams and events travel as uint64_t handles.
+ *   - no torch types; plain pointers and sizes only.
+ *   - thread safety: calls for different devices / streams may run
+ *     concurrently (one host worker thread per device is the intended use).
+ *   - ownership: the caller owns every allocation and frees it; the library
+ *     keeps only per-stream scratch (reductions, cGEMM operand staging),
+ *     released by kaas_stream_destroy.
+ */
+#ifndef KAAS_B200_H
+#define KAAS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------ */
+#define KAAS_OK 0
+#define KAAS_E_INVALID (-1)     /* bad argument (null pointer, bad id)       */
+#define KAAS_E_ARITY (-2)       /* literal tags / buffer count mismatch      */
+#define KAAS_E_BOUNDS (-3)      /* launch would touch bytes past a buffer    */
+#define KAAS_E_UNKNOWN_KERNEL (-4)
+#define KAAS_E_UNSUPPORTED (-5) /* e.g. device is not sm_100               */
+
+/* ---- kernel ids (reference ids in pkg/src/kaas/backend.py:236-243) ----- */
+#define KAAS_K_VECTOR_ADD 1  /* backend.py:153-160  (i32 n; X, Y, OUT)          */
+#define KAAS_K_SAXPY 2       /* backend.py:163-171  (i32 n, f32 a; X, Y, OUT)   */
+#define KAAS_K_MATMUL 3      /* backend.py:174-189  (i32 n,m,k; A, B, OUT)      */
+#define KAAS_K_REDUCE_SUM 4  /* backend.py:192-202  (i32 n; X, OUT)             */
+#define KAAS_K_FILL 5        /* backend.py:205-211  (i32 n, f32 v; OUT)         */
+#define KAAS_K_CGEMM 6       /* new: (i32 n,m,k; A, B, C) complex64, 4M x 3xTF32 */
+#define KAAS_K_JACOBI 7      /* new: (i32 n; A, b, x_in, x_out, resid)         */
+
+/* literal tags, protocol.py:27 LITERAL_TYPES order */
+#define KAAS_LIT_I32 0
+#define KAAS_LIT_I64 1
+#define KAAS_LIT_F32 2
+#define KAAS_LIT_F64 3
+
+typedef struct kaas_literal {
+  int32_t tag;
+  int32_t reserved;
+  int64_t i; /* integer payload (i32/i64)            */
+  double f;  /* float payload (f32 rounded on device) */
+} kaas_literal;
+
+#define KAAS_MAX_LITS 4
+#define KAAS_MAX_ARGS 8
+
+/* One kernel invocation (protocol.py:129-134 KernelInvocation, with the
+ * buffer names already resolved to device pointers by the executor). */
+typedef struct kaas_launch_desc {
+  int32_t kernel;
+  int32_t n_lits;
+  int32_t n_args;
+  int32_t flags;
+  uint32_t dims[6]; /* grid_x, grid_y, grid_z, block_x, block_y, block_z */
+  uint32_t reserved[2];
+  kaas_literal lits[KAAS_MAX_LITS];
+  uint64_t ptrs[KAAS_MAX_ARGS];
+  uint64_t sizes[KAAS_MAX_ARGS];
+} kaas_launch_desc;
+
+typedef struct kaas_device_info {
+  int32_t ordinal;
+  int32_t sm_count;
+  int32_t cc_major;
+  int32_t cc_minor;
+  uint64_t total_mem;
+  uint64_t l2_bytes;
+  int32_t max_smem_per_block;
+  int32_t clock_khz;
+  char name[128];
+} kaas_device_info;
+
+/* ---- errors / discovery ------------------------------------------------- */
+int kaas_last_error(char *buf, size_t len);
+int kaas_version(int *major, int *minor);
+int kaas_device_count(int *n);
+/* Set up device `dev` (memory pool that keeps freed pages, peer maps). */
+int kaas_init_device(int dev);
+int kaas_device_info_get(int dev, kaas_device_info *out);
+/* Total kernels this library has launched (all devices) -- bench evidence. */
+int kaas_launch_counter(uint64_t *out);
+
+/* ---- streams / events (executor request lifecycle, executor.py:320-387) */
+int kaas_stream_create(int dev, int priority, uint64_t *stream);
+int kaas_stream_destroy(uint64_t stream);
+int kaas_stream_sync(uint64_t stream);
+int kaas_event_create(int dev, int timing, uint64_t *event);
+int kaas_event_destroy(uint64_t event);
+int kaas_event_record(uint64_t event, uint64_t stream);
+int kaas_stream_wait_event(uint64_t stream, uint64_t event);
+int kaas_event_sync(uint64_t event);
+int kaas_event_query(uint64_t event, int *done);
+int kaas_event_elapsed_ms(uint64_t start, uint64_t end, float *ms);
+
+/* ---- device memory: DeviceBuffer.__init__ (executor.py:63-72) ---------- */
+int kaas_malloc_async(uint64_t stream, uint64_t bytes, uint64_t *dptr);
+int kaas_free_async(uint64_t stream, uint64_t dptr);
+/* zero-fill of outputs / ephemerals (executor.py:70 bytearray zeros) */
+int kaas_memset_async(uint64_t dptr, int value, uint64_t bytes, uint64_t stream);
+
+/* ---- pinned host memory (MemoryStore payloads, store.py:65-98) --------- */
+int kaas_host_alloc(uint64_t bytes, void **ptr);
+int kaas_host_free(void *ptr);
+int kaas_host_register(void *ptr, uint64_t bytes);
+int kaas_host_unregister(void *ptr);
+
+/* ---- copies: DeviceBuffer.load / snapshot (executor.py:78-82) ---------- */
+int kaas_memcpy_h2d_async(uint64_t dst, const void *src, uint64_t bytes, uint64_t stream);
+int kaas_memcpy_d2h_async(void *dst, uint64_t src, uint64_t bytes, uint64_t stream);
+int kaas_memcpy_d2d_async(uint64_t dst, uint64_t src, uint64_t bytes, uint64_t stream);
+/* NVLink peer fill of a cache entry another GPU already holds (new). */
+int kaas_enable_peer(int dev, int peer);
+int kaas_can_access_peer(int dev, int peer, int *can);
+int kaas_memcpy_p2p_async(uint64_t dst, int dst_dev, uint64_t src, int src_dev,
+                          uint64_t bytes, uint64_t stream);
+
+/* ---- kernels: SimulatedBackend.launch (backend.py:258-266) ------------- */
+/* Bounds are re-checked here (backend.py:137-150 _extent/_f32_view rules);
+ * a violation returns KAAS_E_BOUNDS and enqueues nothing. */
+int kaas_launch(int dev, uint64_t stream, const kaas_launch_desc *desc);
+/* The invocation loop of Executor.execute (executor.py:356-369) in one
+ * crossing: descs run in order on `stream`.  All descriptors are validated
+ * before the first enqueue.  Runs of KAAS_K_JACOBI sweeps that ping-pong
+ * their x buffers are fused into one persistent multi-sweep launch. */
+int kaas_launch_batch(int dev, uint64_t stream, const kaas_launch_desc *descs, int n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KAAS_B200_H */

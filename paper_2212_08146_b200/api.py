@@ -1,0 +1,477 @@
+"""The KaaS request API, unchanged from the reference.
+
+A ``KaasRequest`` is a buffer table (``BufferArg``: named, sized, keyed by
+object-store names; input / output / inout, const or ephemeral) plus an
+ordered list of ``KernelInvocation``s over that namespace.  The GPU executor
+accepts exactly these values, so clients of the reference executor switch
+without change.
+
+Reference: ``pkg/src/kaas/protocol.py`` -- types ``54-202``,
+``validate_request`` ``209-281``, wire format ``292-567``.  Field names,
+defaults, equality (NaN-equal literals, ``protocol.py:80-89``),
+``referenced_buffers`` order (``150-157``) and the violation messages are
+kept identical because they are observable in responses.
+"""
+
+from __future__ import annotations
+
+import json
+import math
+import re
+from dataclasses import dataclass, field
+from functools import cached_property
+
+from .faults import WIRE_ERROR_KINDS
+
+MAX_TOTAL_THREADS = 1 << 32
+I32_RANGE = (-(1 << 31), (1 << 31) - 1)
+I64_RANGE = (-(1 << 63), (1 << 63) - 1)
+STORE_KEY_MAX_LEN = 256
+DIRECTIONS = ("input", "output", "inout")
+LITERAL_TYPES = ("i32", "i64", "f32", "f64")
+_KEY_CHARS = re.compile(r"[A-Za-z0-9._/-]+")
+
+
+def valid_store_key(key) -> bool:
+    """``protocol.py:42-47``: 1..256 chars of ``[A-Za-z0-9._/-]``."""
+    return (isinstance(key, str) and 0 < len(key) <= STORE_KEY_MAX_LEN
+            and _KEY_CHARS.fullmatch(key) is not None)
+
+
+# ---------------------------------------------------------------------------
+# value types
+
+
+@dataclass(frozen=True)
+class LaunchDims:
+    grid_x: int = 1
+    grid_y: int = 1
+    grid_z: int = 1
+    block_x: int = 1
+    block_y: int = 1
+    block_z: int = 1
+
+    def as_tuple(self) -> tuple[int, int, int, int, int, int]:
+        return (self.grid_x, self.grid_y, self.grid_z,
+                self.block_x, self.block_y, self.block_z)
+
+    @property
+    def total_threads(self) -> int:
+        n = 1
+        for c in self.as_tuple():
+            n *= c
+        return n
+
+
+@dataclass(frozen=True, eq=False)
+class ScalarLiteral:
+    """Tagged scalar kernel argument; NaN payloads compare equal."""
+
+    type: str
+    value: int | float
+
+    def __eq__(self, other):
+        if not isinstance(other, ScalarLiteral):
+            return NotImplemented
+        if self.type != other.type or type(self.value) is not type(other.value):
+            return False
+        if isinstance(self.value, float) and math.isnan(self.value) and math.isnan(other.value):
+            return True
+        return self.value == other.value
+
+    def __hash__(self):
+        return hash(self.type)
+
+
+def i32(v) -> ScalarLiteral:
+    return ScalarLiteral("i32", int(v))
+
+
+def i64(v) -> ScalarLiteral:
+    return ScalarLiteral("i64", int(v))
+
+
+def f32(v) -> ScalarLiteral:
+    return ScalarLiteral("f32", float(v))
+
+
+def f64(v) -> ScalarLiteral:
+    return ScalarLiteral("f64", float(v))
+
+
+@dataclass(frozen=True)
+class BufferArg:
+    name: str
+    size: int
+    direction: str = "input"
+    key: str | None = None
+    is_const: bool = False
+    is_ephemeral: bool = False
+
+
+@dataclass(frozen=True)
+class KernelInvocation:
+    kernel_id: str
+    dims: LaunchDims
+    literals: tuple[ScalarLiteral, ...] = ()
+    args: tuple[str, ...] = ()
+
+
+@dataclass(frozen=True)
+class KaasRequest:
+    request_id: str
+    buffers: tuple[BufferArg, ...] = ()
+    invocations: tuple[KernelInvocation, ...] = ()
+
+    @cached_property
+    def by_name(self) -> dict[str, BufferArg]:
+        return {b.name: b for b in self.buffers}
+
+    def referenced_buffers(self) -> tuple[BufferArg, ...]:
+        """Buffers some invocation names, in buffer-table order: the
+        executor's resolution and flush order (``protocol.py:150-157``)."""
+        used = set()
+        for inv in self.invocations:
+            used.update(inv.args)
+        return tuple(b for b in self.buffers if b.name in used)
+
+
+@dataclass(frozen=True)
+class IoStats:
+    store_gets: int = 0
+    store_puts: int = 0
+    bytes_fetched: int = 0
+    bytes_flushed: int = 0
+    cache_hits: int = 0
+    cache_misses: int = 0
+
+
+@dataclass(frozen=True)
+class InvocationStats:
+    kernel_id: str
+    simulated_compute_time: int
+    launch_overhead: int
+
+
+@dataclass(frozen=True)
+class Status:
+    code: str
+    error_kind: str | None = None
+    error_message: str | None = None
+
+    @property
+    def ok(self) -> bool:
+        return self.code == "ok"
+
+    @staticmethod
+    def make_ok() -> "Status":
+        return Status("ok")
+
+    @staticmethod
+    def make_error(kind: str, message: str) -> "Status":
+        return Status("error", kind, message)
+
+
+@dataclass(frozen=True)
+class KaasResponse:
+    request_id: str
+    status: Status
+    per_invocation: tuple[InvocationStats, ...] = ()
+    io_stats: IoStats = field(default_factory=IoStats)
+    simulated_total_time: int = 0
+
+
+# ---------------------------------------------------------------------------
+# validation (protocol.py:209-281)
+
+
+def _is_int(v) -> bool:
+    return isinstance(v, int) and not isinstance(v, bool)
+
+
+def _buffer_problems(b: BufferArg, label: str):
+    if not _is_int(b.size) or b.size < 1:
+        yield f"{label}: size must be a positive integer"
+    if b.direction not in DIRECTIONS:
+        yield f'{label}: unknown direction "{b.direction}"'
+    if b.is_const and b.is_ephemeral:
+        yield f"{label}: const and ephemeral are mutually exclusive"
+    if b.is_const and b.direction != "input":
+        yield f"{label}: const buffers must have direction input"
+    if b.is_ephemeral:
+        if b.key is not None:
+            yield f"{label}: ephemeral buffers must not carry a store key"
+    elif b.key is None:
+        yield f"{label}: non-ephemeral buffers require a store key"
+    elif not valid_store_key(b.key):
+        yield f'{label}: invalid store key "{b.key}"'
+
+
+def _literal_problem(lit: ScalarLiteral, label: str):
+    if lit.type not in LITERAL_TYPES:
+        return f'{label} has unknown type "{lit.type}"'
+    if lit.type in ("f32", "f64"):
+        return None if isinstance(lit.value, float) else f"{label} ({lit.type}) must be a float"
+    if not _is_int(lit.value):
+        return f"{label} ({lit.type}) must be an integer"
+    lo, hi = I32_RANGE if lit.type == "i32" else I64_RANGE
+    if not lo <= lit.value <= hi:
+        return f"{label} out of {lit.type} range"
+    return None
+
+
+def _invocation_problems(idx: int, inv: KernelInvocation, names):
+    label = f"invocation {idx}"
+    if not isinstance(inv.kernel_id, str) or not inv.kernel_id:
+        yield f"{label}: kernel_id must be a non-empty string"
+    comps = inv.dims.as_tuple()
+    if not all(_is_int(c) and c >= 1 for c in comps):
+        yield f"{label}: launch dims must all be >= 1"
+    else:
+        total = inv.dims.total_threads
+        if total > MAX_TOTAL_THREADS:
+            yield f"{label}: total threads {total} exceeds 2^32"
+    for li, lit in enumerate(inv.literals):
+        msg = _literal_problem(lit, f"{label}: literal {li}")
+        if msg is not None:
+            yield msg
+    for name in inv.args:
+        if name not in names:
+            yield f'{label}: unknown buffer "{name}"'
+
+
+def validate_request(req: KaasRequest) -> list[str]:
+    """All invariant violations of ``req`` (empty list = acceptable)."""
+    problems: list[str] = []
+    if not isinstance(req.request_id, str) or not req.request_id:
+        problems.append("request_id must be a non-empty string")
+
+    names: set[str] = set()
+    bindings: dict[str, list[BufferArg]] = {}
+    for b in req.buffers:
+        if not isinstance(b.name, str) or not b.name:
+            problems.append("buffer name must be a non-empty string")
+            continue
+        label = f'buffer "{b.name}"'
+        if b.name in names:
+            problems.append(f"{label}: duplicate buffer name")
+            continue
+        names.add(b.name)
+        own = list(_buffer_problems(b, label))
+        problems.extend(own)
+        if (not b.is_ephemeral and b.key is not None and valid_store_key(b.key)):
+            bindings.setdefault(b.key, []).append(b)
+
+    # One key bound by several buffers is only unambiguous when all are const.
+    for key, owners in bindings.items():
+        if len(owners) > 1 and not all(o.is_const for o in owners):
+            problems.append(f'store key "{key}" bound by non-const buffers '
+                            f'({", ".join(o.name for o in owners)})')
+
+    by_name = req.by_name
+    for idx, inv in enumerate(req.invocations):
+        problems.extend(_invocation_problems(idx, inv, by_name))
+    return problems
+
+
+# ---------------------------------------------------------------------------
+# wire format (protocol.py:292-567): canonical compact JSON, NaN/Inf as words
+
+
+class ProtocolError(Exception):
+    pass
+
+
+class ParseError(ProtocolError):
+    pass
+
+
+class SchemaError(ProtocolError):
+    pass
+
+
+_WORDS = {"NaN": math.nan, "Infinity": math.inf, "-Infinity": -math.inf}
+
+
+def _word(v: float):
+    if math.isnan(v):
+        return "NaN"
+    if math.isinf(v):
+        return "Infinity" if v > 0 else "-Infinity"
+    return v
+
+
+_DIM_NAMES = ("grid_x", "grid_y", "grid_z", "block_x", "block_y", "block_z")
+
+
+def request_to_doc(req: KaasRequest) -> dict:
+    return {
+        "request_id": req.request_id,
+        "buffers": [{"name": b.name, "key": b.key, "size": b.size,
+                     "is_const": b.is_const, "is_ephemeral": b.is_ephemeral,
+                     "direction": b.direction} for b in req.buffers],
+        "invocations": [{
+            "kernel_id": inv.kernel_id,
+            "dims": dict(zip(_DIM_NAMES, inv.dims.as_tuple())),
+            "literals": [{"type": l.type,
+                          "value": _word(l.value) if l.type in ("f32", "f64")
+                          and isinstance(l.value, float) else l.value}
+                         for l in inv.literals],
+            "args": list(inv.args)} for inv in req.invocations],
+    }
+
+
+def encode_request(req: KaasRequest) -> bytes:
+    return json.dumps(request_to_doc(req), separators=(",", ":"),
+                      allow_nan=False).encode("utf-8")
+
+
+def response_to_doc(resp: KaasResponse) -> dict:
+    doc: dict = {"request_id": resp.request_id, "status": resp.status.code}
+    if not resp.status.ok:
+        doc["error"] = {"kind": resp.status.error_kind,
+                        "message": resp.status.error_message or ""}
+    doc["per_invocation"] = [{"kernel_id": s.kernel_id,
+                              "simulated_compute_time": s.simulated_compute_time,
+                              "launch_overhead": s.launch_overhead}
+                             for s in resp.per_invocation]
+    st = resp.io_stats
+    doc["io_stats"] = {n: getattr(st, n) for n in (
+        "store_gets", "store_puts", "bytes_fetched", "bytes_flushed",
+        "cache_hits", "cache_misses")}
+    doc["simulated_total_time"] = resp.simulated_total_time
+    return doc
+
+
+def encode_response(resp: KaasResponse) -> bytes:
+    return json.dumps(response_to_doc(resp), separators=(",", ":"),
+                      allow_nan=False).encode("utf-8")
+
+
+class _Reader:
+    def __init__(self, strict: bool):
+        self.strict = strict
+
+    def obj(self, v, ctx, allowed):
+        if not isinstance(v, dict):
+            raise SchemaError(f"{ctx}: expected object, got {type(v).__name__}")
+        if self.strict and set(v) - set(allowed):
+            raise SchemaError(f"{ctx}: unknown fields {sorted(set(v) - set(allowed))}")
+        return v
+
+    @staticmethod
+    def get(o, name, ctx, kind):
+        if name not in o:
+            raise SchemaError(f"{ctx}: missing field {name!r}")
+        v = o[name]
+        ok = {"str": lambda x: isinstance(x, str),
+              "int": _is_int,
+              "bool": lambda x: isinstance(x, bool),
+              "list": lambda x: isinstance(x, list),
+              "any": lambda x: True}[kind](v)
+        if not ok:
+            raise SchemaError(f"{ctx}.{name}: expected {kind}, got {type(v).__name__}")
+        return v
+
+
+def _loads(data):
+    if not isinstance(data, (bytes, bytearray)):
+        raise ParseError("input must be a byte sequence")
+    try:
+        return json.loads(bytes(data).decode("utf-8"))
+    except UnicodeDecodeError as exc:
+        raise ParseError(f"invalid UTF-8: {exc}") from None
+    except json.JSONDecodeError as exc:
+        raise ParseError(f"malformed JSON: {exc}") from None
+
+
+def request_from_doc(top, strict: bool = False) -> KaasRequest:
+    r = _Reader(strict)
+    top = r.obj(top, "request", ("request_id", "buffers", "invocations"))
+    rid = r.get(top, "request_id", "request", "str")
+    bufs = []
+    for i, raw in enumerate(r.get(top, "buffers", "request", "list")):
+        ctx = f"buffers[{i}]"
+        o = r.obj(raw, ctx, ("name", "key", "size", "is_const", "is_ephemeral", "direction"))
+        key = o.get("key")
+        if key is not None and not isinstance(key, str):
+            raise SchemaError(f"{ctx}.key: expected string")
+        direction = r.get(o, "direction", ctx, "str")
+        if direction not in DIRECTIONS:
+            raise SchemaError(f'{ctx}: unknown direction "{direction}"')
+        bufs.append(BufferArg(r.get(o, "name", ctx, "str"), r.get(o, "size", ctx, "int"),
+                              direction, key, r.get(o, "is_const", ctx, "bool"),
+                              r.get(o, "is_ephemeral", ctx, "bool")))
+    invs = []
+    for i, raw in enumerate(r.get(top, "invocations", "request", "list")):
+        ctx = f"invocations[{i}]"
+        o = r.obj(raw, ctx, ("kernel_id", "dims", "literals", "args"))
+        lits = []
+        for j, lraw in enumerate(r.get(o, "literals", ctx, "list")):
+            lctx = f"{ctx}.literals[{j}]"
+            lo = r.obj(lraw, lctx, ("type", "value"))
+            tag = r.get(lo, "type", lctx, "str")
+            if tag not in LITERAL_TYPES:
+                raise SchemaError(f'{lctx}: unknown literal type "{tag}"')
+            val = r.get(lo, "value", lctx, "any")
+            if tag in ("i32", "i64"):
+                if not _is_int(val):
+                    raise SchemaError(f"{lctx}.value: expected integer")
+            elif isinstance(val, str):
+                if val not in _WORDS:
+                    raise SchemaError(f'{lctx}: bad float word "{val}"')
+                val = _WORDS[val]
+            elif isinstance(val, bool) or not isinstance(val, (int, float)):
+                raise SchemaError(f"{lctx}.value: expected number")
+            else:
+                val = float(val)
+            lits.append(ScalarLiteral(tag, val))
+        args = r.get(o, "args", ctx, "list")
+        if not all(isinstance(a, str) for a in args):
+            raise SchemaError(f"{ctx}.args: expected strings")
+        d = r.obj(r.get(o, "dims", ctx, "any"), f"{ctx}.dims", _DIM_NAMES)
+        dims = LaunchDims(*(r.get(d, n, f"{ctx}.dims", "int") for n in _DIM_NAMES))
+        invs.append(KernelInvocation(r.get(o, "kernel_id", ctx, "str"), dims,
+                                     tuple(lits), tuple(args)))
+    return KaasRequest(rid, tuple(bufs), tuple(invs))
+
+
+def decode_request(data: bytes, strict: bool = False) -> KaasRequest:
+    return request_from_doc(_loads(data), strict)
+
+
+def response_from_doc(top, strict: bool = False) -> KaasResponse:
+    r = _Reader(strict)
+    top = r.obj(top, "response", ("request_id", "status", "error", "per_invocation",
+                                  "io_stats", "simulated_total_time"))
+    rid = r.get(top, "request_id", "response", "str")
+    code = r.get(top, "status", "response", "str")
+    if code == "ok":
+        if strict and "error" in top:
+            raise SchemaError("response: unexpected error object on ok status")
+        status = Status.make_ok()
+    elif code == "error":
+        e = r.obj(r.get(top, "error", "response", "any"), "error", ("kind", "message"))
+        kind = r.get(e, "kind", "error", "str")
+        if kind not in WIRE_ERROR_KINDS:
+            raise SchemaError(f'error: unknown kind "{kind}"')
+        status = Status.make_error(kind, r.get(e, "message", "error", "str"))
+    else:
+        raise SchemaError(f'response: unknown status "{code}"')
+    per = []
+    for i, raw in enumerate(r.get(top, "per_invocation", "response", "list")):
+        ctx = f"per_invocation[{i}]"
+        o = r.obj(raw, ctx, ("kernel_id", "simulated_compute_time", "launch_overhead"))
+        per.append(InvocationStats(r.get(o, "kernel_id", ctx, "str"),
+                                   r.get(o, "simulated_compute_time", ctx, "int"),
+                                   r.get(o, "launch_overhead", ctx, "int")))
+    names = ("store_gets", "store_puts", "bytes_fetched", "bytes_flushed",
+             "cache_hits", "cache_misses")
+    io = r.obj(r.get(top, "io_stats", "response", "any"), "io_stats", names)
+    stats = IoStats(*(r.get(io, n, "io_stats", "int") for n in names))
+    total = r.get(top, "simulated_total_time", "response", "int")
+    return KaasResponse(rid, status, tuple(per), stats, total)
+
+
+def decode_response(data: bytes, strict: bool = False) -> KaasResponse:
+    return response_from_doc(_loads(data), strict)

@@ -1,0 +1,483 @@
+// Complex64 GEMM on the 5th-gen tensor cores (tcgen05, TMEM, TMA) -- the
+// `cgemm` KaaS library kernel (new; CPU restatement: oracle/kernels.py cgemm).
+//
+//   C[n x m] = A[n x k] . B[k x m], complex64 interleaved (re, im), row-major.
+//
+// 4M decomposition as ONE real GEMM on the interleaved data:
+//   C_il[n x 2m] = A_il[n x 2k] . B_exp[2k x 2m]
+//   B_exp[2p,2j] = Br, B_exp[2p+1,2j] = -Bi, B_exp[2p,2j+1] = Bi, B_exp[2p+1,2j+1] = Br
+// so A needs no de-interleave and C is written interleaved directly.
+//
+// 3xTF32 split for FP32 accuracy: x = hi + lo, hi = rna_tf32(x), lo = x - hi
+// (exact).  C = A_hi.B_lo + A_lo.B_hi + A_hi.B_hi, small terms first, all in
+// one FP32 accumulator in TMEM.  (1xTF32 measures 2.9e-4 rel. Frobenius on
+// 1024^3 -- over the 1e-4 budget; 3xTF32 measures ~1e-7.)
+//
+// Pipeline per launch:
+//   1. prep kernels (HBM-bound): A -> [A_hi; A_lo] (K-major, K padded to 32)
+//      and B -> [Bt_hi; Bt_lo] = B_exp^T (K-major), built with an smem transpose.
+//   2. persistent warp-specialised GEMM, one CTA per SM:
+//        warp 0  TMA producer (cp.async.bulk.tensor, SWIZZLE_128B, 4-stage ring)
+//        warp 1  TMEM allocator + single-thread tcgen05.mma issuer (kind::tf32,
+//                M=128, N=BN, K=8), commits release smem stages / publish tiles
+//        warps 2-5 epilogue: tcgen05.ld 32x32b -> registers -> st.global (C is
+//                interleaved complex, row-major), coverage-masked
+//      TMEM holds two BN-column accumulators so the epilogue of tile t
+//      overlaps the main loop of tile t+1.
+#include <cuda.h>
+
+#include "kaas_internal.cuh"
+
+namespace kaas {
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 32;  // fp32 elements per k-block = 128 B rows -> SWIZZLE_128B
+constexpr int STAGES = 4;
+constexpr int GEMM_THREADS = 192;
+
+// ---------------------------------------------------------------------------
+// prep kernels
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// A_il [n x k2] (k2 = 2k) -> Ahi/Alo [n x ldk], zero padded past k2.
+__global__ void k_prep_a(int n, int k2, int ldk, const float *__restrict__ A, float *__restrict__ Ahi,
+                         float *__restrict__ Alo) {
+  const size_t total = (size_t)n * ldk;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const int r = (int)(e / ldk), q = (int)(e % ldk);
+    const float x = q < k2 ? A[(size_t)r * k2 + q] : 0.f;
+    const float hi = tf32_rna(x);
+    Ahi[e] = hi;
+    Alo[e] = x - hi;
+  }
+}
+
+// B [k x m] complex -> Bt_hi/Bt_lo [2m x ldk]:
+//   Bt[2j][2p] = Br[p][j]  Bt[2j][2p+1] = -Bi[p][j]
+//   Bt[2j+1][2p] = Bi[p][j]  Bt[2j+1][2p+1] = Br[p][j]
+// 32 (p) x 32 (j) complex tile through smem; block 32x8 threads.
+__global__ void k_prep_b(int k, int m, int ldk, const float2 *__restrict__ B, float *__restrict__ Bhi,
+                         float *__restrict__ Blo) {
+  __shared__ float2 tile[32][33];
+  const int p0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  for (int r = ty; r < 32; r += 8) {
+    const int p = p0 + r, j = j0 + tx;
+    tile[r][tx] = (p < k && j < m) ? B[(size_t)p * m + j] : make_float2(0.f, 0.f);
+  }
+  __syncthreads();
+  // write: for each j (row pair 2j, 2j+1), lanes cover p = p0 + tx
+  for (int c = ty; c < 32; c += 8) {
+    const int j = j0 + c;
+    if (j >= m) continue;
+    const int p = p0 + tx;
+    const int q = 2 * p;
+    if (q >= ldk) continue;
+    const float2 v = tile[tx][c];  // (Br, Bi) at [p][j]
+    const float e0 = v.x, e1 = -v.y, o0 = v.y, o1 = v.x;
+    const float he0 = tf32_rna(e0), he1 = tf32_rna(e1), ho0 = tf32_rna(o0), ho1 = tf32_rna(o1);
+    float2 *even_hi = reinterpret_cast<float2 *>(Bhi + (size_t)(2 * j) * ldk + q);
+    float2 *odd_hi = reinterpret_cast<float2 *>(Bhi + (size_t)(2 * j + 1) * ldk + q);
+    float2 *even_lo = reinterpret_cast<float2 *>(Blo + (size_t)(2 * j) * ldk + q);
+    float2 *odd_lo = reinterpret_cast<float2 *>(Blo + (size_t)(2 * j + 1) * ldk + q);
+    *even_hi = make_float2(he0, he1);
+    *odd_hi = make_float2(ho0, ho1);
+    *even_lo = make_float2(e0 - he0, e1 - he1);
+    *odd_lo = make_float2(o0 - ho0, o1 - ho1);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// PTX helpers
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap *map, uint64_t *bar, void *dst, int c0,
+                                            int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap *map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void tc_commit(uint64_t *bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// K-major operand tile, SWIZZLE_128B: rows of 128 B, 8-row groups 1024 B apart.
+__device__ __forceinline__ uint64_t make_sw128_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);  // start address
+  d |= (uint64_t)1 << 16;                     // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;           // SBO: 8 rows x 128 B
+  d |= (uint64_t)1 << 46;                     // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                     // SWIZZLE_128B
+  return d;
+}
+
+// kind::tf32 instruction descriptor: D=F32, A=B=TF32, both K-major.
+__host__ __device__ constexpr uint32_t make_idesc(int mdim, int ndim) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(ndim >> 3) << 17) |
+         ((uint32_t)(mdim >> 4) << 24);
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// ---------------------------------------------------------------------------
+// GEMM kernel
+
+struct GemmShape {
+  int M, N;          // output rows (n), output real columns (2m)
+  int kb_per_seg;    // k-blocks per segment (ldk / BK)
+  int a_lo_row;      // row offset of A_lo inside the A tensor map (= n)
+  int b_lo_row;      // row offset of Bt_lo inside the B tensor map (= 2m)
+  int num_m, num_n;  // tile grid
+  int m_complex;     // m (complex columns) for coverage indexing
+  unsigned long long cov;  // covered complex cells
+};
+
+template <int BN>
+struct Smem {
+  alignas(1024) float a[STAGES][BM * BK];
+  alignas(1024) float b[STAGES][BN * BK];
+  uint64_t full[STAGES];
+  uint64_t empty[STAGES];
+  uint64_t tfull[2];
+  uint64_t tempty[2];
+  uint32_t tmem_base;
+};
+
+__device__ __forceinline__ void tile_coords(const GemmShape &s, int t, int &mb, int &nb) {
+  // group 8 m-blocks together so concurrently running CTAs share B tiles in L2
+  constexpr int GM = 8;
+  const int per_group = GM * s.num_n;
+  const int g = t / per_group;
+  const int first_m = g * GM;
+  const int gsize = min(GM, s.num_m - first_m);
+  const int r = t % per_group;
+  mb = first_m + r % gsize;
+  nb = r / gsize;
+}
+
+template <int BN>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+k_cgemm_tf32x3(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+               const GemmShape s, float *__restrict__ C) {
+  extern __shared__ uint8_t smem_raw[];
+  Smem<BN> &sm = *reinterpret_cast<Smem<BN> *>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr uint32_t kTmemCols = 2 * BN;  // two accumulators
+  constexpr uint32_t kStageBytes = (BM + BN) * BK * 4;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&map_a);
+    tma_prefetch_desc(&map_b);
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&sm.full[i], 1);
+      mbar_init(&sm.empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sm.tfull[i], 1);
+      mbar_init(&sm.tempty[i], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&sm.tmem_base)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = sm.tmem_base;
+
+  const int total_tiles = s.num_m * s.num_n;
+  const int kb_total = 3 * s.kb_per_seg;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===== TMA producer =====
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        int mb, nb;
+        tile_coords(s, t, mb, nb);
+        for (int kb = 0; kb < kb_total; ++kb) {
+          const int seg = kb / s.kb_per_seg, kk = kb % s.kb_per_seg;
+          // seg 0: A_hi . B_lo, seg 1: A_lo . B_hi, seg 2: A_hi . B_hi
+          const int arow = (seg == 1 ? s.a_lo_row : 0) + mb * BM;
+          const int brow = (seg == 0 ? s.b_lo_row : 0) + nb * BN;
+          mbar_wait(&sm.empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&sm.full[stage], kStageBytes);
+          tma_load_2d(&map_a, &sm.full[stage], sm.a[stage], kk * BK, arow);
+          tma_load_2d(&map_b, &sm.full[stage], sm.b[stage], kk * BK, brow);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ===== MMA issuer =====
+      constexpr uint32_t idesc = make_idesc(BM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++local) {
+        const int acc = local & 1;
+        const uint32_t acc_phase = (local >> 1) & 1;
+        mbar_wait(&sm.tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * BN;
+        for (int kb = 0; kb < kb_total; ++kb) {
+          mbar_wait(&sm.full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sm.a[stage]);
+          const uint32_t b0 = smem_u32(sm.b[stage]);
+#pragma unroll
+          for (int k = 0; k < BK / 8; ++k) {
+            const uint64_t ad = make_sw128_desc(a0 + k * 32);
+            const uint64_t bd = make_sw128_desc(b0 + k * 32);
+            tc_mma_tf32(tmem_d, ad, bd, idesc, (kb | k) != 0);
+          }
+          tc_commit(&sm.empty[stage]);  // smem slot free once these MMAs retire
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc_commit(&sm.tfull[acc]);  // accumulator ready for the epilogue
+      }
+    }
+  } else {
+    // ===== epilogue: warps 2..5 =====
+    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    int local = 0;
+    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++local) {
+      int mb, nb;
+      tile_coords(s, t, mb, nb);
+      const int acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      mbar_wait(&sm.tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = mb * BM + quarter * 32 + lane;
+      const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld32(taddr + c0, v);
+        const int col = nb * BN + c0;
+        if (row < s.M) {
+          float *dst = C + (size_t)row * s.N + col;
+          const unsigned long long g0 = (unsigned long long)row * s.m_complex + (col >> 1);
+          const bool full = (col + 32 <= s.N) && (g0 + 16 <= s.cov) &&
+                            ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0);
+          if (full) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              reinterpret_cast<float4 *>(dst)[q] =
+                  make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                              __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+          } else {
+#pragma unroll
+            for (int q = 0; q < 32; ++q) {
+              const int c = col + q;
+              if (c < s.N && (unsigned long long)row * s.m_complex + (c >> 1) < s.cov)
+                dst[q] = __uint_as_float(v[q]);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&sm.tempty[acc]);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) {
+    __syncwarp();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(kTmemCols));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                  const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                  const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+int make_map(CUtensorMap *map, const float *base, uint64_t rows, uint64_t ld, uint32_t box_rows) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return fail(KAAS_E_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {ld, rows};
+  cuuint64_t strides[1] = {ld * sizeof(float)};
+  cuuint32_t box[2] = {BK, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)base, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(KAAS_E_INVALID, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return 0;
+}
+
+template <int BN>
+int launch_gemm(cudaStream_t s, int dev, const CUtensorMap &ma, const CUtensorMap &mb,
+                const GemmShape &shape, float *C) {
+  const size_t smem = sizeof(Smem<BN>) + 1024;
+  KAAS_CUDA(cudaFuncSetAttribute(k_cgemm_tf32x3<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+  const int tiles = shape.num_m * shape.num_n;
+  int grid = device_props(dev).sm_count;
+  if (grid > tiles) grid = tiles;
+  k_cgemm_tf32x3<BN><<<grid, GEMM_THREADS, smem, s>>>(ma, mb, shape, C);
+  count_launch();
+  KAAS_CUDA(cudaGetLastError());
+  return 0;
+}
+
+}  // namespace
+
+int launch_cgemm(cudaStream_t s, int dev, int n, int m, int k, uint64_t cov, const float *A,
+                 const float *B, float *C, StreamScratch *sc) {
+  if (n == 0 || m == 0 || cov == 0) return 0;
+  if (k == 0) {
+    // empty contraction: covered cells are 0 + 0i
+    const uint64_t nm = (uint64_t)n * m;
+    const uint64_t cells = cov < nm ? cov : nm;
+    KAAS_CUDA(cudaMemsetAsync(C, 0, cells * 8, s));
+    return 0;
+  }
+  const int k2 = 2 * k;
+  const int ldk = (k2 + BK - 1) / BK * BK;
+  const size_t a_elems = (size_t)n * ldk, b_elems = (size_t)2 * m * ldk;
+  const size_t need = (2 * a_elems + 2 * b_elems) * sizeof(float);
+  int rc = ensure_cgemm_scratch(sc, s, need);
+  if (rc) return rc;
+  float *Ahi = (float *)sc->cg_buf;
+  float *Alo = Ahi + a_elems;
+  float *Bhi = Alo + a_elems;
+  float *Blo = Bhi + b_elems;
+
+  const int sms = device_props(dev).sm_count;
+  k_prep_a<<<sms * 4, 256, 0, s>>>(n, k2, ldk, A, Ahi, Alo);
+  dim3 gb((m + 31) / 32, (k + 31) / 32);
+  k_prep_b<<<gb, dim3(32, 8), 0, s>>>(k, m, ldk, reinterpret_cast<const float2 *>(B), Bhi, Blo);
+  count_launch(2);  // k_prep_b also zero-fills the K padding columns [2k, ldk)
+  KAAS_CUDA(cudaGetLastError());
+
+  // Small problems: narrower N tiles so the grid covers the SMs.
+  const int N = 2 * m;
+  const int tiles256 = ((n + BM - 1) / BM) * ((N + 255) / 256);
+  const bool narrow = tiles256 < sms;
+  const int BNv = narrow ? 128 : 256;
+
+  CUtensorMap ma, mbm;
+  if ((rc = make_map(&ma, Ahi, (uint64_t)2 * n, ldk, BM))) return rc;
+  if ((rc = make_map(&mbm, Bhi, (uint64_t)2 * N, ldk, BNv))) return rc;
+  GemmShape shape;
+  shape.M = n;
+  shape.N = N;
+  shape.kb_per_seg = ldk / BK;
+  shape.a_lo_row = n;
+  shape.b_lo_row = N;
+  shape.num_m = (n + BM - 1) / BM;
+  shape.num_n = (N + BNv - 1) / BNv;
+  shape.m_complex = m;
+  shape.cov = cov;
+  return narrow ? launch_gemm<128>(s, dev, ma, mbm, shape, C) : launch_gemm<256>(s, dev, ma, mbm, shape, C);
+}
+
+}  // namespace kaas

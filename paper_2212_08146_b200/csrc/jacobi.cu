@@ -1,0 +1,602 @@
+// Jacobi sweep for dense systems (new kernel; no reference counterpart --
+// semantics are the CPU restatement in oracle/kernels.py:jacobi_sweep).
+//
+//   x_out[i] = (b[i] - sum_{j != i} A[i,j] * x_in[j]) / A[i,i]   for i < cov
+//   resid[0] = sum_{i < cov} |x_out[i] - x_in[i]|
+//
+// HBM-bound GEMV: 4*n*n bytes of A per sweep against 2*n*n flops.  Layout in
+// HBM is the request's row-major f32 A.  One CTA per SM, each owning a
+// contiguous band of ~n/148 rows.  Columns are cut into 128-float chunks (one
+// float4 per lane); chunk c belongs to warp c % 16, which keeps its x chunks
+// in registers for the whole sweep.  Rows are processed 8 at a time, so each
+// lane has 8 x (chunks per warp) independent 128-bit loads of A in flight
+// (16 for n = 4096).  The diagonal is masked in-register; per-row partials are
+// reduced with warp shuffles, then across warps through smem in fixed order.
+// Residual partials are reduced deterministically (rows -> CTA -> grid, fixed
+// order, grid level in double).
+//
+// A request's 500 sweeps are 500 invocations ping-ponging two ephemerals;
+// kaas_launch_batch hands such runs to launch_jacobi_chain, a cooperative
+// persistent kernel that runs every sweep with a grid barrier in between, so
+// there is one launch per request instead of 500.
+#include <cooperative_groups.h>
+
+#include "kaas_internal.cuh"
+
+namespace kaas {
+namespace {
+
+constexpr int kJacThreads = 512;
+constexpr int kJacWarps = kJacThreads / 32;
+constexpr int kGroup = 8;        // rows per group
+constexpr int kChunk = 128;      // columns per chunk (32 lanes x float4)
+
+__device__ __forceinline__ float4 ld_a(const float *p, uint64_t policy) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p), "l"(policy));
+  return v;
+}
+
+__device__ __forceinline__ uint64_t l2_policy(bool keep) {
+  uint64_t pol;
+  if (keep)  // A is re-read every sweep: ask L2 to keep it
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+// x loads: the non-coherent path only when x is read-only for the whole
+// launch (single sweep); the chain kernel rewrites x between sweeps.
+template <bool kNcX>
+__device__ __forceinline__ float4 ld_x4(const float *p) {
+  if (kNcX) return __ldg(reinterpret_cast<const float4 *>(p));
+  return __ldcg(reinterpret_cast<const float4 *>(p));
+}
+template <bool kNcX>
+__device__ __forceinline__ float ld_x(const float *p) {
+  if (kNcX) return __ldg(p);
+  return __ldcg(p);
+}
+
+__device__ __forceinline__ float dot_masked(float4 a, float4 x, int d) {
+  // d = row - first column of this float4; the diagonal term is dropped
+  float s = d == 0 ? 0.f : a.x * x.x;
+  s = fmaf(a.y, d == 1 ? 0.f : x.y, s);
+  s = fmaf(a.z, d == 2 ? 0.f : x.z, s);
+  s = fmaf(a.w, d == 3 ? 0.f : x.w, s);
+  return s;
+}
+
+struct SweepSmem {
+  float red[kJacWarps][kGroup];
+  float part[kJacWarps];
+};
+
+// One sweep over rows [r0, r1) of this CTA.  Vector path (n % 4 == 0):
+// KC = chunks per warp held in registers (n <= KC * 16 * 128).  Returns the
+// CTA's residual partial in thread 0.
+template <int KC, bool kNcX>
+__device__ __forceinline__ float sweep_band_vec(int n, int r0, int r1, const float *__restrict__ A,
+                                                const float *__restrict__ b,
+                                                const float *__restrict__ x_in,
+                                                float *__restrict__ x_out, SweepSmem &sm,
+                                                uint64_t pol) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nchunks = (n + kChunk - 1) / kChunk;
+  float4 xr[KC];
+  int col[KC];
+#pragma unroll
+  for (int k = 0; k < KC; ++k) {
+    const int c = warp + k * kJacWarps;
+    col[k] = c * kChunk + 4 * lane;
+    xr[k] = (c < nchunks && col[k] < n) ? ld_x4<kNcX>(x_in + col[k]) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  float res = 0.f;
+  for (int i0 = r0; i0 < r1; i0 += kGroup) {
+    const int g_n = min(kGroup, r1 - i0);
+    float acc[kGroup];
+#pragma unroll
+    for (int g = 0; g < kGroup; ++g) acc[g] = 0.f;
+    float4 av[kGroup][KC];
+#pragma unroll
+    for (int g = 0; g < kGroup; ++g)
+#pragma unroll
+      for (int k = 0; k < KC; ++k) {
+        const bool ok = g < g_n && col[k] < n;
+        av[g][k] = ok ? ld_a(A + (size_t)(i0 + g) * n + col[k], pol) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+    for (int g = 0; g < kGroup; ++g)
+#pragma unroll
+      for (int k = 0; k < KC; ++k) acc[g] += dot_masked(av[g][k], xr[k], i0 + g - col[k]);
+#pragma unroll
+    for (int g = 0; g < kGroup; ++g) {
+      float v = acc[g];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      acc[g] = v;
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int g = 0; g < kGroup; ++g) sm.red[warp][g] = acc[g];
+    }
+    __syncthreads();
+    if (threadIdx.x < g_n) {
+      const int g = threadIdx.x, i = i0 + g;
+      float s = 0.f;
+#pragma unroll
+      for (int w = 0; w < kJacWarps; ++w) s += sm.red[w][g];
+      const float xi = ld_x<kNcX>(x_in + i);
+      const float xn = (b[i] - s) / A[(size_t)i * n + i];  // IEEE div.rn
+      x_out[i] = xn;
+      res += fabsf(xn - xi);
+    }
+    __syncthreads();
+  }
+  // CTA partial: threads 0..kGroup-1 hold row-group residuals
+  if (threadIdx.x < kGroup) sm.part[threadIdx.x] = res;
+  __syncthreads();
+  float part = 0.f;
+  if (threadIdx.x == 0)
+    for (int g = 0; g < kGroup; ++g) part += sm.part[g];
+  __syncthreads();
+  return part;
+}
+
+// Scalar path for n % 4 != 0: one warp per row.
+template <bool kNcX>
+__device__ __forceinline__ float sweep_band_scalar(int n, int r0, int r1, const float *__restrict__ A,
+                                                   const float *__restrict__ b,
+                                                   const float *__restrict__ x_in,
+                                                   float *__restrict__ x_out, SweepSmem &sm) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float res = 0.f;
+  for (int i = r0 + warp; i < r1; i += kJacWarps) {
+    const float *row = A + (size_t)i * n;
+    float s = 0.f;
+    for (int j = lane; j < n; j += 32) s = fmaf(__ldg(row + j), j == i ? 0.f : ld_x<kNcX>(x_in + j), s);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane == 0) {
+      const float xn = (b[i] - s) / row[i];
+      x_out[i] = xn;
+      res += fabsf(xn - ld_x<kNcX>(x_in + i));
+    }
+  }
+  if (lane == 0) sm.part[warp] = res;
+  __syncthreads();
+  float part = 0.f;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < kJacWarps; ++w) part += sm.part[w];
+  __syncthreads();
+  return part;
+}
+
+template <int KC, bool kNcX>
+__device__ __forceinline__ float sweep_band(int n, int r0, int r1, const float *A, const float *b,
+                                            const float *x_in, float *x_out, SweepSmem &sm,
+                                            uint64_t pol) {
+  if (KC > 0)
+    return sweep_band_vec<(KC > 0 ? KC : 1), kNcX>(n, r0, r1, A, b, x_in, x_out, sm, pol);
+  return sweep_band_scalar<kNcX>(n, r0, r1, A, b, x_in, x_out, sm);
+}
+
+__device__ __forceinline__ void band(int cov, int &r0, int &r1) {
+  r0 = (int)(((long long)blockIdx.x * cov) / gridDim.x);
+  r1 = (int)(((long long)(blockIdx.x + 1) * cov) / gridDim.x);
+}
+
+// Final cross-CTA sum by one warp, fixed order -> deterministic.
+__device__ __forceinline__ void finish_resid(const float *partials, int nparts, float *resid) {
+  const int lane = threadIdx.x & 31;
+  double acc = 0.0;
+  for (int p = lane; p < nparts; p += 32) acc += (double)__ldcg(partials + p);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  if (lane == 0) *resid = (float)acc;
+}
+
+template <int KC>
+__global__ void __launch_bounds__(kJacThreads, 1)
+k_jacobi_sweep(int n, int cov, const float *__restrict__ A, const float *__restrict__ b,
+               const float *__restrict__ x_in, float *__restrict__ x_out, float *resid,
+               float *partials, unsigned *ticket) {
+  __shared__ SweepSmem sm;
+  __shared__ bool last;
+  int r0, r1;
+  band(cov, r0, r1);
+  const float part = sweep_band<KC, true>(n, r0, r1, A, b, x_in, x_out, sm, l2_policy(false));
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = part;
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x < 32) {
+    __threadfence();
+    finish_resid(partials, gridDim.x, resid);
+    if (threadIdx.x == 0) *ticket = 0u;  // re-arm for the next launch on this stream
+  }
+}
+
+// ---- persistent multi-sweep kernel ----------------------------------------
+
+constexpr int kChainMaxPtrs = 16;
+constexpr int kChainMaxSweeps = 2048;
+
+struct ChainParams {
+  const float *A;
+  const float *b;
+  float *ptrs[kChainMaxPtrs];
+  // per sweep: x_in, x_out, resid indices into ptrs
+  unsigned char idx[kChainMaxSweeps][3];
+  int n, cov, sweeps, keep_l2;
+};
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void grid_barrier(unsigned *count, unsigned *gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned g = ld_acquire(gen);
+    __threadfence();
+    if (atomicAdd(count, 1u) == gridDim.x - 1) {
+      *count = 0u;
+      __threadfence();
+      atomicAdd(gen, 1u);
+    } else {
+      while (ld_acquire(gen) == g) __nanosleep(20);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+template <int KC>
+__global__ void __launch_bounds__(kJacThreads, 1)
+k_jacobi_chain(const __grid_constant__ ChainParams p, float *partials, unsigned *sync) {
+  __shared__ SweepSmem sm;
+  int r0, r1;
+  band(p.cov, r0, r1);
+  const uint64_t pol = l2_policy(p.keep_l2 != 0);
+  for (int s = 0; s < p.sweeps; ++s) {
+    const float *x_in = p.ptrs[p.idx[s][0]];
+    float *x_out = p.ptrs[p.idx[s][1]];
+    const float part = sweep_band<KC, false>(p.n, r0, r1, p.A, p.b, x_in, x_out, sm, pol);
+    float *slot = partials + (s & 1) * kMaxJacobiBlocks;
+    if (threadIdx.x == 0) slot[blockIdx.x] = part;
+    grid_barrier(sync + 1, sync + 2);
+    if (blockIdx.x == 0 && threadIdx.x < 32) finish_resid(slot, gridDim.x, p.ptrs[p.idx[s][2]]);
+  }
+}
+
+
+// ---- TMA-staged sweep kernel (preferred path) -------------------------------
+//
+// Warp 0 (one lane) is a bulk-copy producer: it streams this CTA's rows of A,
+// one row per smem stage, with cp.async.bulk (TMA engine, no register
+// staging) into an S-deep ring guarded by full/empty mbarriers.  Because A is
+// the same for every sweep, the producer runs straight on into the next sweep
+// while the consumers sit in the grid barrier, so the memory pipe never
+// drains.  Warps 1..8 are consumers: x_in is staged once per sweep into smem;
+// each consumer takes every 8th row of the band, reads it from its stage with
+// conflict-free 128-bit smem loads, masks the diagonal, shuffle-reduces, and
+// releases the stage.
+
+constexpr int kTmaConsumers = 8;
+constexpr int kTmaThreads = 32 * (kTmaConsumers + 1);
+constexpr int kTmaMaxStages = 8;
+
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "JWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra JWAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ void consumers_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kTmaConsumers * 32) : "memory");
+}
+
+// consumer-only grid barrier (the producer warp never joins it)
+__device__ __forceinline__ void consumer_grid_barrier(unsigned *count, unsigned *gen, int ctid) {
+  consumers_sync();
+  if (ctid == 0) {
+    const unsigned g = ld_acquire(gen);
+    __threadfence();
+    if (atomicAdd(count, 1u) == gridDim.x - 1) {
+      *count = 0u;
+      __threadfence();
+      atomicAdd(gen, 1u);
+    } else {
+      while (ld_acquire(gen) == g) __nanosleep(20);
+    }
+    __threadfence();
+  }
+  consumers_sync();
+}
+
+template <bool kChain>
+__global__ void __launch_bounds__(kTmaThreads, 1)
+k_jacobi_tma(const __grid_constant__ ChainParams p, int stages, float *partials, unsigned *sync) {
+  extern __shared__ __align__(128) uint8_t jsm[];
+  const int n = p.n;
+  float *x_s = reinterpret_cast<float *>(jsm);
+  float *ring = x_s + ((n + 31) & ~31);
+  uint64_t *full = reinterpret_cast<uint64_t *>(ring + (size_t)stages * n);
+  uint64_t *empty = full + kTmaMaxStages;
+  float *red = reinterpret_cast<float *>(empty + kTmaMaxStages);
+  __shared__ bool last;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int r0, r1;
+  band(p.cov, r0, r1);
+  const int R = r1 - r0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < stages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint32_t row_bytes = (uint32_t)n * 4u;
+
+  if (warp == 0) {
+    // ===== producer =====
+    if (lane == 0) {
+      const uint64_t pol = l2_policy(p.keep_l2 != 0);
+      for (int s = 0; s < p.sweeps; ++s)
+        for (int t = 0; t < R; ++t) {
+          const int q = s * R + t, st = q % stages;
+          mbar_wait(&empty[st], ((q / stages) & 1) ^ 1);
+          mbar_expect_tx(&full[st], row_bytes);
+          bulk_g2s(ring + (size_t)st * n, p.A + (size_t)(r0 + t) * n, row_bytes, &full[st], pol);
+        }
+    }
+    return;
+  }
+
+  // ===== consumers =====
+  const int cw = warp - 1, ctid = threadIdx.x - 32;
+  const int n4 = n >> 2;
+  for (int s = 0; s < p.sweeps; ++s) {
+    const float *x_in = p.ptrs[p.idx[s][0]];
+    float *x_out = p.ptrs[p.idx[s][1]];
+    for (int e = ctid; e < n4; e += kTmaConsumers * 32)
+      reinterpret_cast<float4 *>(x_s)[e] = kChain ? __ldcg(reinterpret_cast<const float4 *>(x_in) + e)
+                                                  : __ldg(reinterpret_cast<const float4 *>(x_in) + e);
+    consumers_sync();
+    float res = 0.f;
+    for (int t = cw; t < R; t += kTmaConsumers) {
+      const int q = s * R + t, st = q % stages;
+      const int i = r0 + t;
+      mbar_wait(&full[st], (q / stages) & 1);
+      const float4 *row4 = reinterpret_cast<const float4 *>(ring + (size_t)st * n);
+      const float4 *x4 = reinterpret_cast<const float4 *>(x_s);
+      float a0 = 0.f, a1 = 0.f;
+      int j4 = lane;
+      for (; j4 + 32 < n4; j4 += 64) {
+        a0 += dot_masked(row4[j4], x4[j4], i - 4 * j4);
+        a1 += dot_masked(row4[j4 + 32], x4[j4 + 32], i - 4 * (j4 + 32));
+      }
+      if (j4 < n4) a0 += dot_masked(row4[j4], x4[j4], i - 4 * j4);
+      float v = a0 + a1;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      if (lane == 0) {
+        const float aii = ring[(size_t)st * n + i];
+        const float xn = (p.b[i] - v) / aii;  // IEEE div.rn
+        x_out[i] = xn;
+        res += fabsf(xn - x_s[i]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+    if (lane == 0) red[cw] = res;
+    consumers_sync();
+    float part = 0.f;
+    if (ctid == 0)
+      for (int w = 0; w < kTmaConsumers; ++w) part += red[w];
+    if (kChain) {
+      float *slot = partials + (s & 1) * kMaxJacobiBlocks;
+      if (ctid == 0) slot[blockIdx.x] = part;
+      consumer_grid_barrier(sync + 1, sync + 2, ctid);
+      if (blockIdx.x == 0 && cw == 0) finish_resid(slot, gridDim.x, p.ptrs[p.idx[s][2]]);
+    } else {
+      if (ctid == 0) {
+        partials[blockIdx.x] = part;
+        __threadfence();
+        last = atomicAdd(sync, 1u) == gridDim.x - 1;
+      }
+      consumers_sync();
+      if (last && cw == 0) {
+        __threadfence();
+        finish_resid(partials, gridDim.x, p.ptrs[p.idx[s][2]]);
+        if (lane == 0) *sync = 0u;
+      }
+    }
+  }
+}
+
+// stages that fit in smem (0 = TMA path not applicable)
+int tma_stages(int n, int max_smem) {
+  if (n % 4 != 0 || n <= 0) return 0;
+  const size_t row = (size_t)n * 4, xbytes = (size_t)((n + 31) & ~31) * 4;
+  const size_t fixed = xbytes + 2 * kTmaMaxStages * 8 + kTmaConsumers * 4 + 256;
+  if (fixed + 2 * row > (size_t)max_smem) return 0;
+  int s = (int)(((size_t)max_smem - fixed) / row);
+  return s > kTmaMaxStages ? kTmaMaxStages : s;
+}
+
+size_t tma_smem(int n, int stages) {
+  return (size_t)((n + 31) & ~31) * 4 + (size_t)stages * n * 4 + 2 * kTmaMaxStages * 8 +
+         kTmaConsumers * 4 + 128;
+}
+
+// chunks-per-warp template selector: 0 = scalar path
+int pick_kc(int n) {
+  if (n % 4 != 0) return 0;
+  const int chunks = (n + kChunk - 1) / kChunk;
+  const int per = (chunks + kJacWarps - 1) / kJacWarps;
+  if (per <= 1) return 1;
+  if (per <= 2) return 2;
+  if (per <= 4) return 4;
+  return -1;  // too wide for register-resident x: caller splits (not needed <= 8192)
+}
+
+bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
+
+}  // namespace
+
+int launch_jacobi(cudaStream_t s, int dev, int n, uint64_t cov, const float *A, const float *b,
+                  const float *x_in, float *x_out, float *resid, StreamScratch *sc) {
+  int blocks = device_props(dev).sm_count;
+  if ((uint64_t)blocks > cov) blocks = cov > 0 ? (int)cov : 1;
+  if (blocks > kMaxJacobiBlocks) blocks = kMaxJacobiBlocks;
+  const int stages = tma_stages(n, device_props(dev).max_smem_optin);
+  if (stages >= 2 && aligned16(A) && aligned16(x_in)) {
+    static thread_local ChainParams p;
+    p.A = A;
+    p.b = b;
+    p.n = n;
+    p.cov = (int)cov;
+    p.sweeps = 1;
+    p.keep_l2 = 0;
+    p.ptrs[0] = const_cast<float *>(x_in);
+    p.ptrs[1] = x_out;
+    p.ptrs[2] = resid;
+    p.idx[0][0] = 0;
+    p.idx[0][1] = 1;
+    p.idx[0][2] = 2;
+    const size_t smem = tma_smem(n, stages);
+    KAAS_CUDA(cudaFuncSetAttribute(k_jacobi_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
+    k_jacobi_tma<false><<<blocks, kTmaThreads, smem, s>>>(p, stages, sc->jac_partials, sc->jac_sync);
+    count_launch();
+    KAAS_CUDA(cudaGetLastError());
+    return 0;
+  }
+  int kc = pick_kc(n);
+  if (!aligned16(A) || !aligned16(x_in)) kc = 0;
+  if (kc < 0) kc = 0;
+#define JAC_LAUNCH(K)                                                                     \
+  k_jacobi_sweep<K><<<blocks, kJacThreads, 0, s>>>(n, (int)cov, A, b, x_in, x_out, resid, \
+                                                   sc->jac_partials, sc->jac_sync)
+  switch (kc) {
+    case 1: JAC_LAUNCH(1); break;
+    case 2: JAC_LAUNCH(2); break;
+    case 4: JAC_LAUNCH(4); break;
+    default: JAC_LAUNCH(0); break;
+  }
+#undef JAC_LAUNCH
+  count_launch();
+  KAAS_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int launch_jacobi_chain(cudaStream_t s, int dev, const JacobiChain &c, StreamScratch *sc) {
+  int kc = pick_kc(c.n);
+  if (kc < 0) kc = 0;
+  if (!aligned16(c.A)) kc = 0;
+  for (int t = 0; t < c.sweeps && kc; ++t)
+    if (!aligned16(c.x_in[t])) kc = 0;
+  const int stages = tma_stages(c.n, device_props(dev).max_smem_optin);
+  bool use_tma = stages >= 2 && aligned16(c.A);
+  for (int t = 0; t < c.sweeps && use_tma; ++t)
+    if (!aligned16(c.x_in[t])) use_tma = false;
+  const size_t tsmem = use_tma ? tma_smem(c.n, stages) : 0;
+  if (use_tma)
+    KAAS_CUDA(cudaFuncSetAttribute(k_jacobi_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)tsmem));
+  const void *fn = kc == 1 ? (const void *)k_jacobi_chain<1>
+                 : kc == 2 ? (const void *)k_jacobi_chain<2>
+                 : kc == 4 ? (const void *)k_jacobi_chain<4>
+                           : (const void *)k_jacobi_chain<0>;
+  // Keep A resident in L2 across sweeps when it fits comfortably.
+  int l2 = 0;
+  cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+  const bool keep = (double)c.n * c.n * 4.0 <= 0.75 * (double)l2;
+  int done = 0;
+  while (done < c.sweeps) {
+    static thread_local ChainParams p;  // ~6 KB: keep it off the stack
+    p.A = c.A;
+    p.b = c.b;
+    p.n = c.n;
+    p.cov = (int)c.cov;
+    p.keep_l2 = keep ? 1 : 0;
+    int np = 0, cnt = 0;
+    auto slot = [&](const float *q) -> int {
+      for (int t = 0; t < np; ++t)
+        if (p.ptrs[t] == q) return t;
+      if (np == kChainMaxPtrs) return -1;
+      p.ptrs[np] = const_cast<float *>(q);
+      return np++;
+    };
+    for (; done + cnt < c.sweeps && cnt < kChainMaxSweeps; ++cnt) {
+      const int t = done + cnt;
+      const int a = slot(c.x_in[t]), o = slot(c.x_out[t]), r = slot(c.resid[t]);
+      if (a < 0 || o < 0 || r < 0) break;
+      p.idx[cnt][0] = (unsigned char)a;
+      p.idx[cnt][1] = (unsigned char)o;
+      p.idx[cnt][2] = (unsigned char)r;
+    }
+    if (cnt == 0) return fail(KAAS_E_INVALID, "jacobi chain: too many distinct buffers");
+    p.sweeps = cnt;
+    int blocks = device_props(dev).sm_count;
+    if ((uint64_t)blocks > c.cov) blocks = c.cov > 0 ? (int)c.cov : 1;
+    float *partials = sc->jac_partials;
+    unsigned *sync = sc->jac_sync;
+    if (use_tma) {
+      int st = stages;
+      void *targs[] = {(void *)&p, (void *)&st, (void *)&partials, (void *)&sync};
+      KAAS_CUDA(cudaLaunchCooperativeKernel((const void *)k_jacobi_tma<true>, dim3(blocks),
+                                            dim3(kTmaThreads), targs, tsmem, s));
+    } else {
+      void *args[] = {(void *)&p, (void *)&partials, (void *)&sync};
+      KAAS_CUDA(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(kJacThreads), args, 0, s));
+    }
+    count_launch();
+    done += cnt;
+  }
+  return 0;
+}
+
+}  // namespace kaas

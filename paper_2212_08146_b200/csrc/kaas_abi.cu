@@ -1,0 +1,654 @@
+// C-ABI layer of libkaas_b200.so: device/stream/event/memory/copy plumbing
+// and the kernel dispatcher that stands in for SimulatedBackend.launch
+// (pkg/src/kaas/backend.py:258-266).  See include/kaas_b200.h.
+#include <cuda.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <unordered_map>
+#include <vector>
+
+#include "kaas_internal.cuh"
+
+namespace kaas {
+
+// ---------------------------------------------------------------------------
+// errors
+
+static thread_local std::string t_last_error;
+
+void set_error(const std::string &msg) { t_last_error = msg; }
+
+int fail(int code, const std::string &msg) {
+  set_error(msg);
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char *what) {
+  char buf[512];
+  snprintf(buf, sizeof buf, "%s failed: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+  set_error(buf);
+  return (int)e;
+}
+
+// ---------------------------------------------------------------------------
+// device properties, scratch, counters
+
+static std::mutex g_mu;
+static std::unordered_map<int, DeviceProps> g_props;
+static std::unordered_map<cudaStream_t, StreamScratch *> g_scratch;
+static std::unordered_map<int, cudaEvent_t> g_coop_event;  // serialises cooperative grids per device
+static std::atomic<uint64_t> g_launch_count{0};
+
+void count_launch(uint64_t n) { g_launch_count.fetch_add(n, std::memory_order_relaxed); }
+
+const DeviceProps &device_props(int dev) {
+  std::lock_guard<std::mutex> g(g_mu);
+  auto it = g_props.find(dev);
+  if (it != g_props.end()) return it->second;
+  DeviceProps p;
+  cudaDeviceGetAttribute(&p.sm_count, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&p.max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaDeviceGetAttribute(&p.cc_major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&p.cc_minor, cudaDevAttrComputeCapabilityMinor, dev);
+  return g_props.emplace(dev, p).first->second;
+}
+
+StreamScratch *scratch_for(cudaStream_t s) {
+  std::lock_guard<std::mutex> g(g_mu);
+  auto it = g_scratch.find(s);
+  return it == g_scratch.end() ? nullptr : it->second;
+}
+
+int ensure_cgemm_scratch(StreamScratch *sc, cudaStream_t s, size_t bytes) {
+  if (sc->cg_bytes >= bytes) return 0;
+  if (sc->cg_buf) KAAS_CUDA(cudaFreeAsync(sc->cg_buf, s));
+  sc->cg_buf = nullptr;
+  sc->cg_bytes = 0;
+  KAAS_CUDA(cudaMallocAsync(&sc->cg_buf, bytes, s));
+  sc->cg_bytes = bytes;
+  return 0;
+}
+
+static int stream_device(cudaStream_t s, int *dev) {
+  StreamScratch *sc = scratch_for(s);
+  if (!sc) return fail(KAAS_E_INVALID, "stream was not created by kaas_stream_create");
+  *dev = sc->dev;
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// kernel table: literal signature, buffer count, written args
+// (mirrors backend.py:236-243 plus the two new kernels)
+
+struct KernelSig {
+  int id;
+  const char *name;
+  int n_lits;
+  int lit_tags[3];
+  int n_args;
+};
+
+static const KernelSig kSigs[] = {
+    {KAAS_K_VECTOR_ADD, "vector_add", 1, {KAAS_LIT_I32}, 3},
+    {KAAS_K_SAXPY, "saxpy", 2, {KAAS_LIT_I32, KAAS_LIT_F32}, 3},
+    {KAAS_K_MATMUL, "matmul", 3, {KAAS_LIT_I32, KAAS_LIT_I32, KAAS_LIT_I32}, 3},
+    {KAAS_K_REDUCE_SUM, "reduce_sum", 1, {KAAS_LIT_I32}, 2},
+    {KAAS_K_FILL, "fill", 2, {KAAS_LIT_I32, KAAS_LIT_F32}, 1},
+    {KAAS_K_CGEMM, "cgemm", 3, {KAAS_LIT_I32, KAAS_LIT_I32, KAAS_LIT_I32}, 3},
+    {KAAS_K_JACOBI, "jacobi_sweep", 1, {KAAS_LIT_I32}, 5},
+};
+
+static const KernelSig *find_sig(int id) {
+  for (const auto &s : kSigs)
+    if (s.id == id) return &s;
+  return nullptr;
+}
+
+// A checked launch: extents, coverage and byte requirements resolved.
+struct Plan {
+  const KernelSig *sig;
+  uint64_t ext[3];  // literal extents
+  uint64_t cov;
+  float fval;       // f32 literal (saxpy a / fill v), rounded once (backend.py:165,207)
+};
+
+static bool mul_ok(uint64_t a, uint64_t b, uint64_t *out) {
+  if (a != 0 && b > UINT64_MAX / a) return false;
+  *out = a * b;
+  return true;
+}
+
+// _extent / _f32_view rules (backend.py:137-150), checked in the order the
+// reference kernels evaluate them.
+static int plan_launch(const kaas_launch_desc *d, Plan *p) {
+  const KernelSig *sig = find_sig(d->kernel);
+  if (!sig) return fail(KAAS_E_UNKNOWN_KERNEL, "unknown kernel id " + std::to_string(d->kernel));
+  p->sig = sig;
+  if (d->n_args != sig->n_args)
+    return fail(KAAS_E_ARITY, std::string(sig->name) + ": expected " +
+                                  std::to_string(sig->n_args) + " buffer args");
+  if (d->n_lits != sig->n_lits) return fail(KAAS_E_ARITY, std::string(sig->name) + ": literal count");
+  for (int i = 0; i < sig->n_lits; ++i)
+    if (d->lits[i].tag != sig->lit_tags[i])
+      return fail(KAAS_E_ARITY, std::string(sig->name) + ": literal types");
+  uint64_t total = 1;
+  for (int i = 0; i < 6; ++i) {
+    if (d->dims[i] == 0) return fail(KAAS_E_INVALID, "launch dims must be >= 1");
+    if (!mul_ok(total, d->dims[i], &total)) total = UINT64_MAX;
+  }
+  const int n_ext = (d->kernel == KAAS_K_MATMUL || d->kernel == KAAS_K_CGEMM) ? 3 : 1;
+  for (int i = 0; i < n_ext; ++i) {
+    if (d->lits[i].i < 0)
+      return fail(KAAS_E_BOUNDS, std::string(sig->name) + ": extent must be non-negative");
+    p->ext[i] = (uint64_t)d->lits[i].i;
+  }
+  p->fval = (sig->n_lits >= 2 && d->lits[1].tag == KAAS_LIT_F32) ? (float)d->lits[1].f : 0.0f;
+
+  auto need = [&](int arg, uint64_t count, uint64_t elt) -> int {
+    uint64_t bytes;
+    if (!mul_ok(count, elt, &bytes) || bytes > d->sizes[arg])
+      return fail(KAAS_E_BOUNDS, std::string(sig->name) + ": arg " + std::to_string(arg) +
+                                     " needs more bytes than the buffer holds");
+    return 0;
+  };
+  const uint64_t n = p->ext[0];
+  int rc = 0;
+  switch (d->kernel) {
+    case KAAS_K_VECTOR_ADD:
+    case KAAS_K_SAXPY:
+      if ((rc = need(0, n, 4)) || (rc = need(1, n, 4)) || (rc = need(2, n, 4))) return rc;
+      p->cov = total < n ? total : n;
+      break;
+    case KAAS_K_FILL:
+      if ((rc = need(0, n, 4))) return rc;
+      p->cov = total < n ? total : n;
+      break;
+    case KAAS_K_REDUCE_SUM:
+      if ((rc = need(0, n, 4)) || (rc = need(1, 1, 4))) return rc;
+      p->cov = n;
+      break;
+    case KAAS_K_MATMUL:
+    case KAAS_K_CGEMM: {
+      const uint64_t m = p->ext[1], k = p->ext[2];
+      const uint64_t elt = d->kernel == KAAS_K_MATMUL ? 4 : 8;
+      uint64_t nk, km, nm;
+      if (!mul_ok(n, k, &nk) || !mul_ok(k, m, &km) || !mul_ok(n, m, &nm))
+        return fail(KAAS_E_BOUNDS, std::string(sig->name) + ": extents overflow");
+      if ((rc = need(0, nk, elt)) || (rc = need(1, km, elt)) || (rc = need(2, nm, elt))) return rc;
+      p->cov = total < nm ? total : nm;
+      break;
+    }
+    case KAAS_K_JACOBI: {
+      uint64_t nn;
+      if (!mul_ok(n, n, &nn)) return fail(KAAS_E_BOUNDS, "jacobi_sweep: extent overflow");
+      if ((rc = need(0, nn, 4)) || (rc = need(1, n, 4)) || (rc = need(2, n, 4)) ||
+          (rc = need(3, n, 4)) || (rc = need(4, 1, 4)))
+        return rc;
+      if (n > 0x7fffffff) return fail(KAAS_E_BOUNDS, "jacobi_sweep: n exceeds i32");
+      p->cov = total < n ? total : n;
+      break;
+    }
+  }
+  return 0;
+}
+
+// Kernels that read some operand after writing another need the written
+// operand redirected when the request binds one buffer to both (the
+// reference reads every input before writing, backend.py:8-9).
+static bool alias_unsafe(int kernel) {
+  return kernel == KAAS_K_MATMUL || kernel == KAAS_K_CGEMM || kernel == KAAS_K_JACOBI;
+}
+
+static int written_args(int kernel, int *w) {
+  switch (kernel) {
+    case KAAS_K_FILL: w[0] = 0; return 1;
+    case KAAS_K_REDUCE_SUM: w[0] = 1; return 1;
+    case KAAS_K_JACOBI: w[0] = 3; w[1] = 4; return 2;
+    default: w[0] = 2; return 1;
+  }
+}
+
+static int run_plan(int dev, cudaStream_t s, const kaas_launch_desc *d, const Plan &p,
+                    StreamScratch *sc) {
+  uint64_t ptr[KAAS_MAX_ARGS];
+  memcpy(ptr, d->ptrs, sizeof ptr);
+
+  // Alias redirection: a written arg that shares its buffer with a read arg
+  // goes through a temporary holding a copy of the buffer (so the uncovered
+  // tail survives), then is copied back.
+  struct Redirect { uint64_t orig, tmp, bytes; };
+  std::vector<Redirect> redirects;
+  if (alias_unsafe(d->kernel)) {
+    int w[2];
+    const int nw = written_args(d->kernel, w);
+    for (int wi = 0; wi < nw; ++wi) {
+      const uint64_t target = d->ptrs[w[wi]];
+      bool aliased = false;
+      for (int a = 0; a < d->n_args; ++a) {
+        bool is_written = false;
+        for (int wj = 0; wj < nw; ++wj) is_written |= (w[wj] == a);
+        if (!is_written && d->ptrs[a] == target) aliased = true;
+      }
+      if (!aliased) continue;
+      bool have = false;
+      for (auto &r : redirects) have |= (r.orig == target);
+      if (have) continue;
+      void *tmp = nullptr;
+      KAAS_CUDA(cudaMallocAsync(&tmp, d->sizes[w[wi]], s));
+      KAAS_CUDA(cudaMemcpyAsync(tmp, (void *)target, d->sizes[w[wi]], cudaMemcpyDeviceToDevice, s));
+      redirects.push_back({target, (uint64_t)tmp, d->sizes[w[wi]]});
+    }
+    for (int wi = 0; wi < nw; ++wi)
+      for (auto &r : redirects)
+        if (d->ptrs[w[wi]] == r.orig) ptr[w[wi]] = r.tmp;
+  }
+
+  int rc = 0;
+  const uint64_t n = p.ext[0];
+  switch (d->kernel) {
+    case KAAS_K_VECTOR_ADD:
+      rc = launch_vector_add(s, dev, p.cov, (const float *)ptr[0], (const float *)ptr[1], (float *)ptr[2]);
+      break;
+    case KAAS_K_SAXPY:
+      rc = launch_saxpy(s, dev, p.cov, p.fval, (const float *)ptr[0], (const float *)ptr[1], (float *)ptr[2]);
+      break;
+    case KAAS_K_FILL:
+      rc = launch_fill(s, dev, p.cov, p.fval, (float *)ptr[0]);
+      break;
+    case KAAS_K_REDUCE_SUM:
+      rc = launch_reduce_sum(s, dev, n, (const float *)ptr[0], (float *)ptr[1]);
+      break;
+    case KAAS_K_MATMUL:
+      rc = launch_matmul(s, dev, n, p.ext[1], p.ext[2], p.cov, (const float *)ptr[0],
+                         (const float *)ptr[1], (float *)ptr[2]);
+      break;
+    case KAAS_K_CGEMM:
+      if (n > 0x7fffffff || p.ext[1] > 0x7fffffff || p.ext[2] > 0x7fffffff)
+        return fail(KAAS_E_BOUNDS, "cgemm: extent exceeds i32");
+      rc = launch_cgemm(s, dev, (int)n, (int)p.ext[1], (int)p.ext[2], p.cov, (const float *)ptr[0],
+                        (const float *)ptr[1], (float *)ptr[2], sc);
+      break;
+    case KAAS_K_JACOBI:
+      if (n == 0 || p.cov == 0) {
+        // nothing covered: residual of an empty sum
+        rc = launch_fill(s, dev, 1, 0.0f, (float *)ptr[4]);
+        break;
+      }
+      rc = launch_jacobi(s, dev, (int)n, p.cov, (const float *)ptr[0], (const float *)ptr[1],
+                         (const float *)ptr[2], (float *)ptr[3], (float *)ptr[4], sc);
+      break;
+  }
+  if (rc) return rc;
+  for (auto &r : redirects) {
+    KAAS_CUDA(cudaMemcpyAsync((void *)r.orig, (void *)r.tmp, r.bytes, cudaMemcpyDeviceToDevice, s));
+    KAAS_CUDA(cudaFreeAsync((void *)r.tmp, s));
+  }
+  return 0;
+}
+
+// A run of Jacobi sweeps that can share one persistent launch: same system,
+// no buffer both read and written within a sweep, and residual slots that
+// nothing in the run reads.
+static int jacobi_run_length(const kaas_launch_desc *d, const Plan *plans, int i, int n) {
+  const kaas_launch_desc &h = d[i];
+  if (h.kernel != KAAS_K_JACOBI || plans[i].cov == 0) return 1;
+  int j = i;
+  for (; j < n; ++j) {
+    const kaas_launch_desc &e = d[j];
+    if (e.kernel != KAAS_K_JACOBI || plans[j].ext[0] != plans[i].ext[0] ||
+        plans[j].cov != plans[i].cov || e.ptrs[0] != h.ptrs[0] || e.ptrs[1] != h.ptrs[1])
+      break;
+    const uint64_t A = e.ptrs[0], b = e.ptrs[1], xi = e.ptrs[2], xo = e.ptrs[3], r = e.ptrs[4];
+    if (xo == xi || xo == A || xo == b || r == A || r == b || r == xi || r == xo) break;
+  }
+  int len = j - i;
+  // residual slots must not be read (as x_in) or written (as x_out) by any sweep of the run
+  for (int a = i; a < i + len; ++a)
+    for (int c = i; c < i + len; ++c)
+      if (d[a].ptrs[4] == d[c].ptrs[2] || d[a].ptrs[4] == d[c].ptrs[3]) {
+        len = (a > c ? a : c) - i;  // cut before the conflict
+        if (len < 1) len = 1;
+      }
+  return len;
+}
+
+static int coop_serialise_begin(int dev, cudaStream_t s) {
+  std::lock_guard<std::mutex> g(g_mu);
+  auto it = g_coop_event.find(dev);
+  if (it == g_coop_event.end()) return 0;
+  KAAS_CUDA(cudaStreamWaitEvent(s, it->second, 0));
+  return 0;
+}
+
+static int coop_serialise_end(int dev, cudaStream_t s) {
+  std::lock_guard<std::mutex> g(g_mu);
+  auto it = g_coop_event.find(dev);
+  if (it == g_coop_event.end()) {
+    cudaEvent_t ev;
+    KAAS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    it = g_coop_event.emplace(dev, ev).first;
+  }
+  KAAS_CUDA(cudaEventRecord(it->second, s));
+  return 0;
+}
+
+}  // namespace kaas
+
+using namespace kaas;
+
+// ===========================================================================
+// exported C ABI
+
+extern "C" {
+
+int kaas_last_error(char *buf, size_t len) {
+  if (!buf || len == 0) return KAAS_E_INVALID;
+  snprintf(buf, len, "%s", t_last_error.c_str());
+  return 0;
+}
+
+int kaas_version(int *major, int *minor) {
+  if (major) *major = 1;
+  if (minor) *minor = 0;
+  return 0;
+}
+
+int kaas_device_count(int *n) {
+  if (!n) return KAAS_E_INVALID;
+  cudaError_t e = cudaGetDeviceCount(n);
+  if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) {
+    cudaGetLastError();
+    *n = 0;
+    return 0;
+  }
+  KAAS_CUDA(e);
+  return 0;
+}
+
+int kaas_init_device(int dev) {
+  KAAS_CUDA(cudaSetDevice(dev));
+  const DeviceProps &p = device_props(dev);
+  if (p.cc_major != 10)
+    return fail(KAAS_E_UNSUPPORTED, "libkaas_b200 is built for sm_100a; device " +
+                                        std::to_string(dev) + " is sm_" + std::to_string(p.cc_major) +
+                                        std::to_string(p.cc_minor));
+  cudaMemPool_t pool;
+  KAAS_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  uint64_t keep = UINT64_MAX;  // never hand pages back to the OS between requests
+  KAAS_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  KAAS_CUDA(cudaFree(nullptr));
+  return 0;
+}
+
+int kaas_device_info_get(int dev, kaas_device_info *out) {
+  if (!out) return KAAS_E_INVALID;
+  cudaDeviceProp prop;
+  KAAS_CUDA(cudaGetDeviceProperties(&prop, dev));
+  memset(out, 0, sizeof *out);
+  out->ordinal = dev;
+  out->sm_count = prop.multiProcessorCount;
+  out->cc_major = prop.major;
+  out->cc_minor = prop.minor;
+  out->total_mem = prop.totalGlobalMem;
+  out->l2_bytes = (uint64_t)prop.l2CacheSize;
+  out->max_smem_per_block = (int)prop.sharedMemPerBlockOptin;
+  int clk = 0;
+  cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, dev);
+  out->clock_khz = clk;
+  snprintf(out->name, sizeof out->name, "%s", prop.name);
+  return 0;
+}
+
+int kaas_launch_counter(uint64_t *out) {
+  if (!out) return KAAS_E_INVALID;
+  *out = g_launch_count.load();
+  return 0;
+}
+
+// ---- streams / events ------------------------------------------------------
+
+int kaas_stream_create(int dev, int priority, uint64_t *stream) {
+  if (!stream) return KAAS_E_INVALID;
+  KAAS_CUDA(cudaSetDevice(dev));
+  cudaStream_t s;
+  KAAS_CUDA(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, priority));
+  auto *sc = new StreamScratch();
+  sc->dev = dev;
+  cudaError_t e = cudaMallocAsync((void **)&sc->jac_partials, 2 * kMaxJacobiBlocks * sizeof(float), s);
+  if (e == cudaSuccess) e = cudaMallocAsync((void **)&sc->jac_sync, 16 * sizeof(unsigned), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(sc->jac_sync, 0, 16 * sizeof(unsigned), s);
+  if (e != cudaSuccess) {
+    delete sc;
+    cudaStreamDestroy(s);
+    return cuda_fail(e, "stream scratch allocation");
+  }
+  {
+    std::lock_guard<std::mutex> g(g_mu);
+    g_scratch[s] = sc;
+  }
+  *stream = (uint64_t)s;
+  return 0;
+}
+
+int kaas_stream_destroy(uint64_t stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  StreamScratch *sc = nullptr;
+  {
+    std::lock_guard<std::mutex> g(g_mu);
+    auto it = g_scratch.find(s);
+    if (it != g_scratch.end()) {
+      sc = it->second;
+      g_scratch.erase(it);
+    }
+  }
+  if (sc) {
+    cudaSetDevice(sc->dev);
+    if (sc->jac_partials) cudaFreeAsync(sc->jac_partials, s);
+    if (sc->jac_sync) cudaFreeAsync(sc->jac_sync, s);
+    if (sc->cg_buf) cudaFreeAsync(sc->cg_buf, s);
+    cudaStreamSynchronize(s);
+    delete sc;
+  }
+  KAAS_CUDA(cudaStreamDestroy(s));
+  return 0;
+}
+
+int kaas_stream_sync(uint64_t stream) {
+  KAAS_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  return 0;
+}
+
+int kaas_event_create(int dev, int timing, uint64_t *event) {
+  if (!event) return KAAS_E_INVALID;
+  KAAS_CUDA(cudaSetDevice(dev));
+  cudaEvent_t e;
+  KAAS_CUDA(cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming));
+  *event = (uint64_t)e;
+  return 0;
+}
+
+int kaas_event_destroy(uint64_t event) {
+  KAAS_CUDA(cudaEventDestroy((cudaEvent_t)event));
+  return 0;
+}
+
+int kaas_event_record(uint64_t event, uint64_t stream) {
+  KAAS_CUDA(cudaEventRecord((cudaEvent_t)event, (cudaStream_t)stream));
+  return 0;
+}
+
+int kaas_stream_wait_event(uint64_t stream, uint64_t event) {
+  KAAS_CUDA(cudaStreamWaitEvent((cudaStream_t)stream, (cudaEvent_t)event, 0));
+  return 0;
+}
+
+int kaas_event_sync(uint64_t event) {
+  KAAS_CUDA(cudaEventSynchronize((cudaEvent_t)event));
+  return 0;
+}
+
+int kaas_event_query(uint64_t event, int *done) {
+  if (!done) return KAAS_E_INVALID;
+  cudaError_t e = cudaEventQuery((cudaEvent_t)event);
+  if (e == cudaErrorNotReady) {
+    *done = 0;
+    return 0;
+  }
+  KAAS_CUDA(e);
+  *done = 1;
+  return 0;
+}
+
+int kaas_event_elapsed_ms(uint64_t start, uint64_t end, float *ms) {
+  if (!ms) return KAAS_E_INVALID;
+  KAAS_CUDA(cudaEventElapsedTime(ms, (cudaEvent_t)start, (cudaEvent_t)end));
+  return 0;
+}
+
+// ---- memory ----------------------------------------------------------------
+
+int kaas_malloc_async(uint64_t stream, uint64_t bytes, uint64_t *dptr) {
+  if (!dptr) return KAAS_E_INVALID;
+  int dev, rc;
+  if ((rc = stream_device((cudaStream_t)stream, &dev))) return rc;
+  KAAS_CUDA(cudaSetDevice(dev));
+  void *p = nullptr;
+  KAAS_CUDA(cudaMallocAsync(&p, bytes ? bytes : 1, (cudaStream_t)stream));
+  *dptr = (uint64_t)p;
+  return 0;
+}
+
+int kaas_free_async(uint64_t stream, uint64_t dptr) {
+  int dev, rc;
+  if ((rc = stream_device((cudaStream_t)stream, &dev))) return rc;
+  KAAS_CUDA(cudaSetDevice(dev));
+  KAAS_CUDA(cudaFreeAsync((void *)dptr, (cudaStream_t)stream));
+  return 0;
+}
+
+int kaas_memset_async(uint64_t dptr, int value, uint64_t bytes, uint64_t stream) {
+  if (bytes == 0) return 0;
+  KAAS_CUDA(cudaMemsetAsync((void *)dptr, value, bytes, (cudaStream_t)stream));
+  return 0;
+}
+
+int kaas_host_alloc(uint64_t bytes, void **ptr) {
+  if (!ptr) return KAAS_E_INVALID;
+  KAAS_CUDA(cudaHostAlloc(ptr, bytes ? bytes : 1, cudaHostAllocPortable));
+  return 0;
+}
+
+int kaas_host_free(void *ptr) {
+  KAAS_CUDA(cudaFreeHost(ptr));
+  return 0;
+}
+
+int kaas_host_register(void *ptr, uint64_t bytes) {
+  KAAS_CUDA(cudaHostRegister(ptr, bytes, cudaHostRegisterPortable));
+  return 0;
+}
+
+int kaas_host_unregister(void *ptr) {
+  KAAS_CUDA(cudaHostUnregister(ptr));
+  return 0;
+}
+
+// ---- copies ----------------------------------------------------------------
+
+int kaas_memcpy_h2d_async(uint64_t dst, const void *src, uint64_t bytes, uint64_t stream) {
+  if (bytes == 0) return 0;
+  KAAS_CUDA(cudaMemcpyAsync((void *)dst, src, bytes, cudaMemcpyHostToDevice, (cudaStream_t)stream));
+  return 0;
+}
+
+int kaas_memcpy_d2h_async(void *dst, uint64_t src, uint64_t bytes, uint64_t stream) {
+  if (bytes == 0) return 0;
+  KAAS_CUDA(cudaMemcpyAsync(dst, (const void *)src, bytes, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  return 0;
+}
+
+int kaas_memcpy_d2d_async(uint64_t dst, uint64_t src, uint64_t bytes, uint64_t stream) {
+  if (bytes == 0) return 0;
+  KAAS_CUDA(cudaMemcpyAsync((void *)dst, (const void *)src, bytes, cudaMemcpyDeviceToDevice,
+                            (cudaStream_t)stream));
+  return 0;
+}
+
+int kaas_enable_peer(int dev, int peer) {
+  KAAS_CUDA(cudaSetDevice(dev));
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return 0;
+  }
+  KAAS_CUDA(e);
+  return 0;
+}
+
+int kaas_can_access_peer(int dev, int peer, int *can) {
+  if (!can) return KAAS_E_INVALID;
+  KAAS_CUDA(cudaDeviceCanAccessPeer(can, dev, peer));
+  return 0;
+}
+
+int kaas_memcpy_p2p_async(uint64_t dst, int dst_dev, uint64_t src, int src_dev, uint64_t bytes,
+                          uint64_t stream) {
+  if (bytes == 0) return 0;
+  KAAS_CUDA(cudaMemcpyPeerAsync((void *)dst, dst_dev, (const void *)src, src_dev, bytes,
+                                (cudaStream_t)stream));
+  return 0;
+}
+
+// ---- kernels -----------------------------------------------------------------
+
+int kaas_launch(int dev, uint64_t stream, const kaas_launch_desc *desc) {
+  return kaas_launch_batch(dev, stream, desc, 1);
+}
+
+int kaas_launch_batch(int dev, uint64_t stream, const kaas_launch_desc *descs, int n) {
+  if (n < 0 || (n > 0 && !descs)) return fail(KAAS_E_INVALID, "null launch descriptors");
+  cudaStream_t s = (cudaStream_t)stream;
+  StreamScratch *sc = scratch_for(s);
+  if (!sc) return fail(KAAS_E_INVALID, "stream was not created by kaas_stream_create");
+  if (sc->dev != dev) return fail(KAAS_E_INVALID, "stream belongs to another device");
+  KAAS_CUDA(cudaSetDevice(dev));
+  std::vector<Plan> plans((size_t)n);
+  for (int i = 0; i < n; ++i) {
+    int rc = plan_launch(&descs[i], &plans[i]);
+    if (rc) {
+      set_error("invocation " + std::to_string(i) + ": " + t_last_error);
+      return rc;
+    }
+  }
+  std::vector<const float *> xin, xout, res;
+  for (int i = 0; i < n;) {
+    const int run = jacobi_run_length(descs, plans.data(), i, n);
+    if (run >= 2) {
+      xin.resize(run);
+      xout.resize(run);
+      res.resize(run);
+      for (int t = 0; t < run; ++t) {
+        xin[t] = (const float *)descs[i + t].ptrs[2];
+        xout[t] = (const float *)descs[i + t].ptrs[3];
+        res[t] = (const float *)descs[i + t].ptrs[4];
+      }
+      JacobiChain c{(int)plans[i].ext[0], plans[i].cov, (const float *)descs[i].ptrs[0],
+                    (const float *)descs[i].ptrs[1], run, xin.data(),
+                    (float *const *)xout.data(), (float *const *)res.data()};
+      int rc;
+      if ((rc = coop_serialise_begin(dev, s))) return rc;
+      if ((rc = launch_jacobi_chain(s, dev, c, sc))) return rc;
+      if ((rc = coop_serialise_end(dev, s))) return rc;
+      i += run;
+      continue;
+    }
+    int rc = run_plan(dev, s, &descs[i], plans[i], sc);
+    if (rc) return rc;
+    ++i;
+  }
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,79 @@
+// Internal declarations shared by the C-ABI layer and the kernel files.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <mutex>
+#include <string>
+
+#include "../../include/kaas_b200.h"
+
+namespace kaas {
+
+// ---- error plumbing --------------------------------------------------------
+void set_error(const std::string &msg);
+int fail(int code, const std::string &msg);
+int cuda_fail(cudaError_t e, const char *what);
+
+#define KAAS_CUDA(call)                                   \
+  do {                                                    \
+    cudaError_t _e = (call);                              \
+    if (_e != cudaSuccess) return ::kaas::cuda_fail(_e, #call); \
+  } while (0)
+
+// ---- per-stream scratch (outside the cache ledger) ------------------------
+// Each executor stream owns its own scratch so two executors sharing a GPU
+// never race on reduction partials or cGEMM operand staging.
+struct StreamScratch {
+  int dev = 0;
+  // Jacobi: per-block residual partials + arrival ticket + grid barrier words
+  float *jac_partials = nullptr;    // [kMaxJacobiBlocks]
+  unsigned *jac_sync = nullptr;     // [4]: ticket, barrier count, barrier gen, pad
+  // cGEMM operand staging (A_lo, B_exp^T hi, B_exp^T lo), grown on demand
+  void *cg_buf = nullptr;
+  size_t cg_bytes = 0;
+};
+constexpr int kMaxJacobiBlocks = 4096;
+
+StreamScratch *scratch_for(cudaStream_t s);
+int ensure_cgemm_scratch(StreamScratch *sc, cudaStream_t s, size_t bytes);
+
+struct DeviceProps {
+  int sm_count = 148;
+  int max_smem_optin = 227 * 1024;
+  int cc_major = 10, cc_minor = 0;
+};
+const DeviceProps &device_props(int dev);
+
+extern uint64_t g_launches;  // atomic-incremented launch counter
+void count_launch(uint64_t n = 1);
+
+// ---- kernel launchers (return 0 or error code; set_error on failure) -----
+int launch_vector_add(cudaStream_t s, int dev, uint64_t cov, const float *x,
+                      const float *y, float *out);
+int launch_saxpy(cudaStream_t s, int dev, uint64_t cov, float a, const float *x,
+                 const float *y, float *out);
+int launch_fill(cudaStream_t s, int dev, uint64_t cov, float v, float *out);
+int launch_reduce_sum(cudaStream_t s, int dev, uint64_t n, const float *x, float *out);
+int launch_matmul(cudaStream_t s, int dev, uint64_t n, uint64_t m, uint64_t k,
+                  uint64_t cov, const float *a, const float *b, float *out);
+int launch_jacobi(cudaStream_t s, int dev, int n, uint64_t cov, const float *A,
+                  const float *b, const float *x_in, float *x_out, float *resid,
+                  StreamScratch *sc);
+// `sweeps` consecutive sweeps ping-ponging between x buffers, see jacobi.cu
+struct JacobiChain {
+  int n;
+  uint64_t cov;
+  const float *A;
+  const float *b;
+  int sweeps;
+  const float *const *x_in;  // [sweeps]
+  float *const *x_out;       // [sweeps]
+  float *const *resid;       // [sweeps]
+};
+int launch_jacobi_chain(cudaStream_t s, int dev, const JacobiChain &c, StreamScratch *sc);
+int launch_cgemm(cudaStream_t s, int dev, int n, int m, int k, uint64_t cov,
+                 const float *A, const float *B, float *C, StreamScratch *sc);
+
+}  // namespace kaas
