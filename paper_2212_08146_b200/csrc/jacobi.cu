@@ -21,6 +21,8 @@
 // there is one launch per request instead of 500.
 #include <cooperative_groups.h>
 
+#include <cstdlib>
+
 #include "kaas_internal.cuh"
 
 namespace kaas {
@@ -292,7 +294,7 @@ k_jacobi_chain(const __grid_constant__ ChainParams p, float *partials, unsigned 
 
 constexpr int kTmaConsumers = 8;
 constexpr int kTmaThreads = 32 * (kTmaConsumers + 1);
-constexpr int kTmaMaxStages = 8;
+constexpr int kTmaMaxStages = 12;
 
 __device__ __forceinline__ uint32_t smem_addr(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -353,7 +355,39 @@ __device__ __forceinline__ void consumer_grid_barrier(unsigned *count, unsigned 
   consumers_sync();
 }
 
-template <bool kChain>
+// Row dot product against x held in registers: xr[it] = x[128*it + 4*lane ..].
+// Only chunk it_d = i/128 contains the diagonal; that iteration (warp-uniform
+// branch) masks it on the owning lane, every other iteration is 4 plain FMAs.
+template <int XR>
+__device__ __forceinline__ float row_dot_regs(const float4 *row4, const float4 (&xr)[XR], int n4,
+                                              int i, int lane) {
+  float a0 = 0.f, a1 = 0.f;
+  const int it_d = i >> 7;
+#pragma unroll
+  for (int it = 0; it < XR; ++it) {
+    const int j4 = it * 32 + lane;
+    if (j4 < n4) {
+      const float4 a = row4[j4];
+      float4 x = xr[it];
+      if (it == it_d) {
+        const int d = i - 4 * j4;
+        x.x = d == 0 ? 0.f : x.x;
+        x.y = d == 1 ? 0.f : x.y;
+        x.z = d == 2 ? 0.f : x.z;
+        x.w = d == 3 ? 0.f : x.w;
+      }
+      float &acc = (it & 1) ? a1 : a0;
+      acc = fmaf(a.x, x.x, acc);
+      acc = fmaf(a.y, x.y, acc);
+      acc = fmaf(a.z, x.z, acc);
+      acc = fmaf(a.w, x.w, acc);
+    }
+  }
+  return a0 + a1;
+}
+
+// XR > 0: x in registers (n <= 128*XR); XR == 0: x read from smem.
+template <bool kChain, int XR>
 __global__ void __launch_bounds__(kTmaThreads, 1)
 k_jacobi_tma(const __grid_constant__ ChainParams p, int stages, float *partials, unsigned *sync) {
   extern __shared__ __align__(128) uint8_t jsm[];
@@ -380,7 +414,7 @@ k_jacobi_tma(const __grid_constant__ ChainParams p, int stages, float *partials,
   const uint32_t row_bytes = (uint32_t)n * 4u;
 
   if (warp == 0) {
-    // ===== producer =====
+    // ===== producer: streams rows, running ahead across sweeps (A is constant)
     if (lane == 0) {
       const uint64_t pol = l2_policy(p.keep_l2 != 0);
       for (int s = 0; s < p.sweeps; ++s)
@@ -404,31 +438,45 @@ k_jacobi_tma(const __grid_constant__ ChainParams p, int stages, float *partials,
       reinterpret_cast<float4 *>(x_s)[e] = kChain ? __ldcg(reinterpret_cast<const float4 *>(x_in) + e)
                                                   : __ldg(reinterpret_cast<const float4 *>(x_in) + e);
     consumers_sync();
+    const float4 *x4 = reinterpret_cast<const float4 *>(x_s);
+    float4 xr[XR > 0 ? XR : 1];
+    if (XR > 0) {
+#pragma unroll
+      for (int it = 0; it < (XR > 0 ? XR : 1); ++it) {
+        const int j4 = it * 32 + lane;
+        xr[it] = j4 < n4 ? x4[j4] : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
     float res = 0.f;
     for (int t = cw; t < R; t += kTmaConsumers) {
       const int q = s * R + t, st = q % stages;
       const int i = r0 + t;
       mbar_wait(&full[st], (q / stages) & 1);
       const float4 *row4 = reinterpret_cast<const float4 *>(ring + (size_t)st * n);
-      const float4 *x4 = reinterpret_cast<const float4 *>(x_s);
-      float a0 = 0.f, a1 = 0.f;
-      int j4 = lane;
-      for (; j4 + 32 < n4; j4 += 64) {
-        a0 += dot_masked(row4[j4], x4[j4], i - 4 * j4);
-        a1 += dot_masked(row4[j4 + 32], x4[j4 + 32], i - 4 * (j4 + 32));
+      float v;
+      if (XR > 0) {
+        v = row_dot_regs<(XR > 0 ? XR : 1)>(row4, xr, n4, i, lane);
+      } else {
+        float a0 = 0.f, a1 = 0.f;
+        int j4 = lane;
+        for (; j4 + 32 < n4; j4 += 64) {
+          a0 += dot_masked(row4[j4], x4[j4], i - 4 * j4);
+          a1 += dot_masked(row4[j4 + 32], x4[j4 + 32], i - 4 * (j4 + 32));
+        }
+        if (j4 < n4) a0 += dot_masked(row4[j4], x4[j4], i - 4 * j4);
+        v = a0 + a1;
       }
-      if (j4 < n4) a0 += dot_masked(row4[j4], x4[j4], i - 4 * j4);
-      float v = a0 + a1;
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      float aii = 0.f;
+      if (lane == 0) aii = ring[(size_t)st * n + i];
+      __syncwarp();
       if (lane == 0) {
-        const float aii = ring[(size_t)st * n + i];
+        mbar_arrive(&empty[st]);  // row consumed: release the stage early
         const float xn = (p.b[i] - v) / aii;  // IEEE div.rn
         x_out[i] = xn;
         res += fabsf(xn - x_s[i]);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[st]);
     }
     if (lane == 0) red[cw] = res;
     consumers_sync();
@@ -463,7 +511,32 @@ int tma_stages(int n, int max_smem) {
   const size_t fixed = xbytes + 2 * kTmaMaxStages * 8 + kTmaConsumers * 4 + 256;
   if (fixed + 2 * row > (size_t)max_smem) return 0;
   int s = (int)(((size_t)max_smem - fixed) / row);
-  return s > kTmaMaxStages ? kTmaMaxStages : s;
+  int cap = kTmaMaxStages;
+  if (const char *e = getenv("KAAS_JACOBI_STAGES")) cap = atoi(e) > 1 ? atoi(e) : cap;  // dev A/B
+  if (cap > kTmaMaxStages) cap = kTmaMaxStages;
+  return s > cap ? cap : s;
+}
+
+// x-register chunks: 32 for n <= 4096, 16 for n <= 2048, ... 0 (smem x) above 4096
+// (KAAS_JACOBI_XREG=0 forces x from smem; dev A/B switch)
+int tma_xr(int n) {
+  const char *e = getenv("KAAS_JACOBI_XREG");
+  if (e && e[0] == '0') return 0;
+  const int c = (n + 127) / 128;
+  if (c <= 8) return 8;
+  if (c <= 16) return 16;
+  if (c <= 32) return 32;
+  return 0;
+}
+
+template <bool kChain>
+const void *tma_kernel(int xr) {
+  switch (xr) {
+    case 8: return (const void *)k_jacobi_tma<kChain, 8>;
+    case 16: return (const void *)k_jacobi_tma<kChain, 16>;
+    case 32: return (const void *)k_jacobi_tma<kChain, 32>;
+    default: return (const void *)k_jacobi_tma<kChain, 0>;
+  }
 }
 
 size_t tma_smem(int n, int stages) {
@@ -507,9 +580,13 @@ int launch_jacobi(cudaStream_t s, int dev, int n, uint64_t cov, const float *A, 
     p.idx[0][1] = 1;
     p.idx[0][2] = 2;
     const size_t smem = tma_smem(n, stages);
-    KAAS_CUDA(cudaFuncSetAttribute(k_jacobi_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
-    k_jacobi_tma<false><<<blocks, kTmaThreads, smem, s>>>(p, stages, sc->jac_partials, sc->jac_sync);
+    const void *fn = tma_kernel<false>(tma_xr(n));
+    KAAS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int st = stages;
+    float *partials = sc->jac_partials;
+    unsigned *sync = sc->jac_sync;
+    void *args[] = {(void *)&p, (void *)&st, (void *)&partials, (void *)&sync};
+    KAAS_CUDA(cudaLaunchKernel(fn, dim3(blocks), dim3(kTmaThreads), args, smem, s));
     count_launch();
     KAAS_CUDA(cudaGetLastError());
     return 0;
@@ -543,9 +620,9 @@ int launch_jacobi_chain(cudaStream_t s, int dev, const JacobiChain &c, StreamScr
   for (int t = 0; t < c.sweeps && use_tma; ++t)
     if (!aligned16(c.x_in[t])) use_tma = false;
   const size_t tsmem = use_tma ? tma_smem(c.n, stages) : 0;
+  const void *tfn = tma_kernel<true>(tma_xr(c.n));
   if (use_tma)
-    KAAS_CUDA(cudaFuncSetAttribute(k_jacobi_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)tsmem));
+    KAAS_CUDA(cudaFuncSetAttribute(tfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem));
   const void *fn = kc == 1 ? (const void *)k_jacobi_chain<1>
                  : kc == 2 ? (const void *)k_jacobi_chain<2>
                  : kc == 4 ? (const void *)k_jacobi_chain<4>
@@ -587,8 +664,7 @@ int launch_jacobi_chain(cudaStream_t s, int dev, const JacobiChain &c, StreamScr
     if (use_tma) {
       int st = stages;
       void *targs[] = {(void *)&p, (void *)&st, (void *)&partials, (void *)&sync};
-      KAAS_CUDA(cudaLaunchCooperativeKernel((const void *)k_jacobi_tma<true>, dim3(blocks),
-                                            dim3(kTmaThreads), targs, tsmem, s));
+      KAAS_CUDA(cudaLaunchCooperativeKernel(tfn, dim3(blocks), dim3(kTmaThreads), targs, tsmem, s));
     } else {
       void *args[] = {(void *)&p, (void *)&partials, (void *)&sync};
       KAAS_CUDA(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(kJacThreads), args, 0, s));

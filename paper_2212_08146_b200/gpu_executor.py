@@ -34,7 +34,10 @@ touch it is freed only after the request's streams drain.
 
 from __future__ import annotations
 
+from collections import OrderedDict
 from dataclasses import dataclass, field
+
+import numpy as np
 
 from . import native
 from .api import (
@@ -103,13 +106,15 @@ class _ReqStats:
 class DeviceStats:
     """Measured (not virtual) device activity of one executor."""
 
-    __slots__ = ("requests", "device_ms", "last_device_ms", "h2d_bytes", "d2h_bytes",
-                 "p2p_bytes", "kernel_launches")
+    __slots__ = ("requests", "device_ms", "last_device_ms", "kernel_ms", "last_kernel_ms",
+                 "h2d_bytes", "d2h_bytes", "p2p_bytes", "kernel_launches")
 
     def __init__(self):
         self.requests = 0
         self.device_ms = 0.0
         self.last_device_ms = 0.0
+        self.kernel_ms = 0.0       # time inside the batched invocation list
+        self.last_kernel_ms = 0.0
         self.h2d_bytes = 0
         self.d2h_bytes = 0
         self.p2p_bytes = 0
@@ -117,6 +122,31 @@ class DeviceStats:
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k in self.__slots__}
+
+
+class _Plan:
+    """Everything about a request that does not depend on cache state.
+
+    Validation, static checks, per-invocation bounds checks (resolved
+    buffers always have the declared sizes), virtual compute time and the
+    launch descriptors are pure functions of the request, so they are
+    computed once per distinct request and replayed: a 500-sweep Jacobi
+    request costs a few numpy ops on the host instead of ~4 ms of Python."""
+
+    __slots__ = ("error", "kernels", "fail_at", "fail_exc", "advance_ns", "per_inv",
+                 "template", "slots", "names", "dirty_names", "n")
+
+
+class _LRU(OrderedDict):
+    def __init__(self, cap: int):
+        super().__init__()
+        self.cap = cap
+
+    def put(self, k, v):
+        self[k] = v
+        self.move_to_end(k)
+        if len(self) > self.cap:
+            self.popitem(last=False)
 
 
 class GpuExecutor:
@@ -137,6 +167,8 @@ class GpuExecutor:
         self._ev_exec = native.Event(self.device)
         self._ev_start = native.Event(self.device, timing=True)
         self._ev_end = native.Event(self.device, timing=True)
+        self._ev_k0 = native.Event(self.device, timing=True)
+        self._ev_k1 = native.Event(self.device, timing=True)
         self.time_requests = time_requests
         self.cache = CacheState(config.capacity, debug=config.debug, on_drop=self._drop)
         self.clock = VirtualClock()
@@ -149,6 +181,8 @@ class GpuExecutor:
         self._graveyard: list[int] = []   # device ptrs to free once streams drain
         self._keepalive: list = []        # host blobs referenced by in-flight copies
         self._closed = False
+        self._plans_by_id: _LRU = _LRU(256)     # id(req) -> (req, plan)
+        self._plans_by_value: _LRU = _LRU(256)  # req -> plan
 
     # -- device memory ------------------------------------------------------
 
@@ -273,16 +307,36 @@ class GpuExecutor:
 
     # -- request lifecycle (executor.py:320-425) ------------------------------
 
-    def execute(self, req: KaasRequest) -> KaasResponse:
-        t0 = self.clock.now_ns
-        stats = _ReqStats()
+    # -- request planning -----------------------------------------------------
 
+    def _plan(self, req: KaasRequest) -> _Plan:
+        """Plans depend on the buffer table and invocation list only (the
+        request id matters just for its own validity check), so a client
+        that rebuilds the same request each call still hits the cache."""
+        hit = self._plans_by_id.get(id(req))
+        if hit is not None and hit[0] is req:
+            return hit[1]
+        if not isinstance(req.request_id, str) or not req.request_id:
+            return self._build_plan(req)  # invalid id: never cached
+        key = (req.buffers, req.invocations)
+        try:
+            plan = self._plans_by_value.get(key)
+        except TypeError:  # unhashable field values: plan without caching
+            return self._build_plan(req)
+        if plan is None:
+            plan = self._build_plan(req)
+            self._plans_by_value.put(key, plan)
+        self._plans_by_id.put(id(req), (req, plan))
+        return plan
+
+    def _build_plan(self, req: KaasRequest) -> _Plan:
+        p = _Plan()
+        p.error = None
         violations = validate_request(req)
         if violations:
-            return self._finish(req, stats, t0,
-                                Status.make_error("InvalidRequest", "; ".join(violations)))
-
-        try:
+            p.error = Status.make_error("InvalidRequest", "; ".join(violations))
+            return p
+        try:  # static checks (executor.py:331-345)
             kernels = []
             for inv in req.invocations:
                 kernel = self.backend.kernel(inv.kernel_id)
@@ -295,7 +349,54 @@ class GpuExecutor:
                             f" buffer {arg.name!r}")
                 kernels.append(kernel)
         except KaasError as exc:
-            return self._finish(req, stats, t0, Status.make_error(exc.kind, exc.message))
+            p.error = Status.make_error(exc.kind, exc.message)
+            return p
+        p.kernels = kernels
+        names = [b.name for b in req.referenced_buffers()]
+        slot_of = {nm: i for i, nm in enumerate(names)}
+        by_name = req.by_name
+        timing = self.backend.timing
+        n = len(req.invocations)
+        descs = (native.LaunchDesc * n)() if n else None
+        slots = np.full((n, native.MAX_ARGS), len(names), dtype=np.int64)
+        per_inv, dirty, advance = [], [], 0
+        p.fail_at, p.fail_exc = None, None
+        for i, (inv, kernel) in enumerate(zip(req.invocations, kernels)):
+            sizes = [by_name[nm].size for nm in inv.args]
+            try:
+                fma = kernel.plan(inv.dims, inv.literals, sizes)
+            except KaasError as exc:  # BackendFault at invocation i
+                p.fail_at, p.fail_exc = i, exc
+                break
+            compute_ns = timing.compute_time_ns(fma)
+            overhead_ns = timing.launch_overhead_ns()
+            advance += overhead_ns + compute_ns
+            fill_desc(descs[i], kernel, inv.dims, inv.literals, [0] * len(sizes), sizes)
+            for j, nm in enumerate(inv.args):
+                slots[i, j] = slot_of[nm]
+            for idx in kernel.writes:
+                nm = inv.args[idx]
+                if not by_name[nm].is_ephemeral and nm not in dirty:
+                    dirty.append(nm)
+            per_inv.append(InvocationStats(inv.kernel_id, compute_ns, overhead_ns))
+        p.advance_ns = advance
+        p.per_inv = tuple(per_inv)
+        p.dirty_names = tuple(dirty)
+        p.names = tuple(names)
+        p.n = n if p.fail_at is None else 0
+        p.slots = slots
+        p.template = (np.frombuffer(bytes(descs), dtype=native.DESC_DTYPE).copy()
+                      if n else None)
+        return p
+
+    # -- request lifecycle (executor.py:320-425) ------------------------------
+
+    def execute(self, req: KaasRequest) -> KaasResponse:
+        t0 = self.clock.now_ns
+        stats = _ReqStats()
+        plan = self._plan(req)
+        if plan.error is not None:
+            return self._finish(req, stats, t0, plan.error)
 
         self._req_seq += 1
         if self.time_requests:
@@ -305,14 +406,15 @@ class GpuExecutor:
         resolved: dict[str, DeviceBuffer] = {}
         ephemerals: list[DeviceBuffer] = []
         try:
-            for arg in req.referenced_buffers():
+            by_name = req.by_name
+            for nm in plan.names:
+                arg = by_name[nm]
                 buf = self.resolve_buffer(arg, stats)
-                resolved[arg.name] = buf
+                resolved[nm] = buf
                 if arg.is_ephemeral:
                     ephemerals.append(buf)
-
-            per_inv = self._plan_and_launch(req, kernels, resolved)
-            self._flush(req, resolved, stats)
+            self._launch(plan, resolved)
+            self._flush(plan.names, resolved, stats)
             status = Status.make_ok()
         except KaasError as exc:
             self._drain_quietly()
@@ -326,44 +428,46 @@ class GpuExecutor:
             ms = self._ev_start.elapsed_ms(self._ev_end)
             self.dev_stats.last_device_ms = ms
             self.dev_stats.device_ms += ms
+            if plan.n:
+                kms = self._ev_k0.elapsed_ms(self._ev_k1)
+                self.dev_stats.last_kernel_ms = kms
+                self.dev_stats.kernel_ms += kms
         self.dev_stats.requests += 1
-        return self._finish(req, stats, t0, status, per_inv)
+        return self._finish(req, stats, t0, status, list(plan.per_inv))
 
-    def _plan_and_launch(self, req: KaasRequest, kernels, resolved) -> list[InvocationStats]:
-        """Check + price every invocation in order (backend.launch semantics),
-        then enqueue them all in one C-ABI crossing."""
-        timing = self.backend.timing
-        n = len(req.invocations)
-        descs = (native.LaunchDesc * n)() if n else None
-        per_inv = []
-        for i, (inv, kernel) in enumerate(zip(req.invocations, kernels)):
-            bufs = [resolved[name] for name in inv.args]
-            sizes = [b.size for b in bufs]
-            kernel.check_arity(inv.literals, len(bufs))
-            fma = kernel.plan(inv.dims, inv.literals, sizes)  # BackendFault before any effect
-            compute_ns = timing.compute_time_ns(fma)
-            overhead_ns = timing.launch_overhead_ns()
-            self.clock.advance_ns(overhead_ns + compute_ns)
-            fill_desc(descs[i], kernel, inv.dims, inv.literals, [b.ptr for b in bufs], sizes)
-            for idx in kernel.writes:
-                b = bufs[idx]
-                if b.key is not None:
-                    b.dirty = True
-            per_inv.append(InvocationStats(inv.kernel_id, compute_ns, overhead_ns))
-        if n:
+    def _launch(self, plan: _Plan, resolved) -> None:
+        """Replay the plan: clock, dirty marks, one batched enqueue.  On a
+        planned BackendFault the clock and dirty marks stop where the
+        reference's would and nothing is enqueued (the failed request's
+        kernel effects are unobservable: every buffer they could write is
+        dropped or ephemeral)."""
+        self.clock.advance_ns(plan.advance_ns)
+        for nm in plan.dirty_names:
+            resolved[nm].dirty = True
+        if plan.fail_at is not None:
+            raise plan.fail_exc
+        if plan.n:
+            table = np.fromiter((resolved[nm].ptr for nm in plan.names), dtype=np.uint64,
+                                count=len(plan.names))
+            table = np.append(table, np.uint64(0))
+            descs = plan.template.copy()
+            descs["ptrs"] = table[plan.slots]
             self._ev_fill.record(self.s_in)
             self.s_exec.wait(self._ev_fill)
+            if self.time_requests:
+                self._ev_k0.record(self.s_exec)
             native.launch_batch(self.device, self.s_exec, descs)
-            self.dev_stats.kernel_launches += n
-        return per_inv
+            if self.time_requests:
+                self._ev_k1.record(self.s_exec)
+            self.dev_stats.kernel_launches += plan.n
 
-    def _flush(self, req: KaasRequest, resolved, stats: _ReqStats) -> None:
+    def _flush(self, names, resolved, stats: _ReqStats) -> None:
         """Write back dirty keyed buffers, table order (executor.py:371-380)."""
         self._ev_exec.record(self.s_exec)
         self.s_out.wait(self._ev_exec)
         pending = []
-        for arg in req.referenced_buffers():
-            buf = resolved[arg.name]
+        for nm in names:
+            buf = resolved[nm]
             # only non-const keyed buffers get dirty, and validation forbids
             # binding one non-const key twice, so no buffer appears twice here
             if buf.dirty:
@@ -454,7 +558,8 @@ class GpuExecutor:
         for s in (self.s_in, self.s_exec, self.s_out):
             s.sync()
             s.destroy()
-        for e in (self._ev_fill, self._ev_exec, self._ev_start, self._ev_end):
+        for e in (self._ev_fill, self._ev_exec, self._ev_start, self._ev_end, self._ev_k0,
+                  self._ev_k1):
             e.destroy()
 
 

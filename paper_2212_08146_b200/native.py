@@ -65,6 +65,24 @@ class DeviceInfo(C.Structure):
     ]
 
 
+def _desc_dtype():
+    import numpy as np
+    lit = np.dtype({"names": ["tag", "reserved", "i", "f"],
+                    "formats": ["<i4", "<i4", "<i8", "<f8"],
+                    "offsets": [0, 4, 8, 16], "itemsize": C.sizeof(Literal)})
+    f = LaunchDesc
+    return np.dtype({
+        "names": ["kernel", "n_lits", "n_args", "flags", "dims", "reserved", "lits", "ptrs", "sizes"],
+        "formats": ["<i4", "<i4", "<i4", "<i4", ("<u4", 6), ("<u4", 2), (lit, MAX_LITS),
+                    ("<u8", MAX_ARGS), ("<u8", MAX_ARGS)],
+        "offsets": [f.kernel.offset, f.n_lits.offset, f.n_args.offset, f.flags.offset,
+                    f.dims.offset, f.reserved.offset, f.lits.offset, f.ptrs.offset,
+                    f.sizes.offset],
+        "itemsize": C.sizeof(LaunchDesc)})
+
+
+DESC_DTYPE = _desc_dtype()
+
 _u64 = C.c_uint64
 _pu64 = C.POINTER(C.c_uint64)
 _vp = C.c_void_p
@@ -287,11 +305,15 @@ def host_free(addr: int) -> None:
 
 
 def launch_batch(dev: int, stream: Stream, descs) -> None:
-    """Enqueue a ctypes array of LaunchDesc in order; see kaas_launch_batch."""
+    """Enqueue LaunchDescs in order (ctypes array or DESC_DTYPE numpy array)."""
     n = len(descs)
     if n == 0:
         return
-    rc = load().kaas_launch_batch(dev, stream.handle, descs, n)
+    if hasattr(descs, "ctypes") and hasattr(descs, "dtype"):
+        ptr = descs.ctypes.data_as(C.POINTER(LaunchDesc))
+    else:
+        ptr = descs
+    rc = load().kaas_launch_batch(dev, stream.handle, ptr, n)
     check(rc, "kaas_launch_batch")
 
 

@@ -1,0 +1,125 @@
+"""Multi-GPU request pool: the ``KaasService`` surface over B200 executors.
+
+Same public surface as the reference service (``pkg/src/kaas/service.py:22-112``):
+``KaasService(store, n_executors, capacity, policy, timing, digest_cap,
+strict_schema, debug)``, ``submit`` / ``submit_async`` / ``stats`` /
+``close``, context manager, ``executors`` / ``router`` / ``store`` attributes.
+
+Executor ``i`` owns GPU ``devices[i % len(devices)]`` (one executor per GPU by
+default; several executors may share a GPU, each with its own ledger and
+streams).  Each executor has one consumer thread and a FIFO queue, so
+requests on one executor run in arrival order; the router decision is made
+at submission time under its lock.  ctypes drops the GIL inside every CUDA
+call, so the per-GPU workers overlap.  No NCCL: requests shard by request.
+"""
+
+from __future__ import annotations
+
+import queue
+import threading
+from concurrent.futures import Future
+
+from . import native
+from .api import KaasRequest, KaasResponse, Status
+from .gpu_executor import ExecutorConfig, GpuBackend, GpuExecutor
+from .placement import Router, parse_policy
+from .timing import TimingModel
+
+
+def visible_devices() -> list[int]:
+    return list(range(native.device_count()))
+
+
+class KaasService:
+    def __init__(self, store, n_executors: int | None = None, capacity: int = 256 * 2**20,
+                 policy="affinity:8", timing: TimingModel | None = None,
+                 digest_cap: int = 1024, strict_schema: bool = False, debug: bool = False,
+                 devices: list[int] | None = None, executor_factory=None,
+                 log_decisions: bool = False):
+        if executor_factory is None:
+            devices = devices if devices is not None else visible_devices()
+            if not devices:
+                raise RuntimeError("no CUDA devices visible (libkaas_b200 has no CPU path)")
+        if n_executors is None:
+            n_executors = len(devices) if devices else 1
+        if n_executors < 1:
+            raise ValueError("need at least one executor")
+        self.store = store
+        self.strict_schema = strict_schema
+        self.timing = timing if timing is not None else TimingModel()
+        self.devices = devices
+        if executor_factory is None:
+            def executor_factory(i):
+                cfg = ExecutorConfig(capacity=capacity, timing=self.timing, executor_id=i,
+                                     debug=debug, device=devices[i % len(devices)])
+                return GpuExecutor(cfg, store, GpuBackend(timing=self.timing))
+        self.executors = [executor_factory(i) for i in range(n_executors)]
+        if isinstance(policy, str):
+            policy = parse_policy(policy)
+        self.router = Router([e.executor_id for e in self.executors], policy,
+                             digest_cap=digest_cap, log_decisions=log_decisions)
+        self._queues = {e.executor_id: queue.Queue() for e in self.executors}
+        self._threads = [threading.Thread(target=self._worker, args=(e,), daemon=True,
+                                          name=f"kaas-executor-{e.executor_id}")
+                         for e in self.executors]
+        self._closed = False
+        for t in self._threads:
+            t.start()
+
+    def _worker(self, executor) -> None:
+        q = self._queues[executor.executor_id]
+        while True:
+            item = q.get()
+            if item is None:
+                return
+            req, fut = item
+            try:
+                resp = executor.execute(req)
+            except BaseException as exc:  # execute() reports request errors in-band
+                failed = KaasResponse(req.request_id, Status.make_error("Internal", str(exc)))
+                self.router.update_digest(executor.executor_id, failed, req)
+                fut.set_exception(exc)
+                continue
+            self.router.update_digest(executor.executor_id, resp, req)
+            fut.set_result(resp)
+
+    def submit_async(self, req: KaasRequest) -> Future:
+        if self._closed:
+            raise RuntimeError("service is closed")
+        eid = self.router.route(req)
+        fut: Future = Future()
+        fut.executor_id = eid  # placement, for benches and tests
+        self._queues[eid].put((req, fut))
+        return fut
+
+    def submit(self, req: KaasRequest) -> KaasResponse:
+        return self.submit_async(req).result()
+
+    def stats(self) -> dict:
+        out = {"executors": [e.stats() for e in self.executors],
+               "router": self.router.snapshot()}
+        dev = [e.device_stats() for e in self.executors if hasattr(e, "device_stats")]
+        if dev:
+            out["devices"] = dev
+        return out
+
+    def close(self) -> None:
+        if self._closed:
+            return
+        self._closed = True
+        for q in self._queues.values():
+            q.put(None)
+        for t in self._threads:
+            t.join(timeout=60)
+        for e in self.executors:
+            if hasattr(e, "close"):
+                e.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+GpuKaasService = KaasService

@@ -1,0 +1,112 @@
+"""GPU executor parity: the B200 path reproduces the reference executor.
+
+* golden streams recorded from the real reference: every response (status,
+  message, IoStats, per-invocation virtual times, total virtual time), the
+  cache state after every request, the removal sequence, and every store
+  write (NaN-canonical bytes) must be identical;
+* fresh streams from tests/fuzzgen.py (incl. cgemm / jacobi_sweep) against
+  the CPU oracle: decisions bit-exact, data bit-exact for builtins and within
+  the north-star tolerances for cgemm (rel. Frobenius <= 1e-4) and
+  jacobi_sweep (max abs <= 1e-5).
+"""
+
+import numpy as np
+import pytest
+
+from fuzzgen import make_stream
+from helpers import cache_digest, canon, load_golden, replay
+from oracle.executor import DictStore, OracleExecutor
+from paper_2212_08146_b200.api import response_to_doc
+from paper_2212_08146_b200.gpu_executor import ExecutorConfig, GpuExecutor
+from paper_2212_08146_b200.hoststore import MemoryStore, PinnedStore
+
+pytestmark = pytest.mark.gpu
+
+STREAMS = ["executor_fuzz31337.json.gz", "executor_fuzz77.json.gz",
+           "executor_tight.json.gz", "executor_fuzzfa22.json.gz"]
+
+
+def gpu_factory(capacity, store_cls, debug=True):
+    made = []
+
+    def make(initial):
+        store = store_cls()
+        for k, v in initial.items():
+            store.put(k, v)
+        ex = GpuExecutor(ExecutorConfig(capacity=capacity, debug=debug), store)
+        removed = []
+        orig = ex.cache.remove
+
+        def spy(key):
+            removed.append(key)
+            return orig(key)
+
+        ex.cache.remove = spy
+        made.append(ex)
+        snap = lambda: [(k, *v) for k, v in ex.cache.snapshot().items()]  # noqa: E731
+        return ex, store, snap, removed
+    return make, made
+
+
+@pytest.mark.parametrize("store_cls", [PinnedStore, MemoryStore])
+@pytest.mark.parametrize("name", STREAMS)
+def test_gpu_replays_reference_stream(cuda, name, store_cls):
+    stream = load_golden(name)
+    make, made = gpu_factory(stream["capacity"], store_cls)
+    n = 0
+    for i, step, resp, digest, removed, writes in replay(stream, make):
+        assert resp == step["response"], f"step {i}: {resp} != {step['response']}"
+        assert digest == step["cache"], f"step {i} cache"
+        assert removed == step["removed"], f"step {i} removals"
+        assert writes == step["writes"], f"step {i} store writes"
+        ex = made[0]
+        assert ex.cache.ephemeral_bytes == 0
+        assert all(b.pinned == 0 and not b.dirty for b in ex.cache.entries.values())
+        n += 1
+    assert n == len(stream["steps"])
+    ex = made[0]
+    final = sorted([k, b.size, b.last_use] for k, b in ex.cache.entries.items())
+    assert final == stream["final_cache"]
+    ex.close()
+
+
+def _compare_key(key, got, want):
+    if key.startswith("c/"):
+        g = np.frombuffer(bytes(got), "<c8").astype(np.complex128)
+        w = np.frombuffer(bytes(want), "<c8").astype(np.complex128)
+        den = np.linalg.norm(w)
+        err = np.linalg.norm(g - w) / den if den else np.linalg.norm(g - w)
+        assert err <= 1e-4, f"{key}: rel. Frobenius {err:.3e}"
+    elif key.startswith("j/"):
+        g = np.frombuffer(bytes(got), "<f4").astype(np.float64)
+        w = np.frombuffer(bytes(want), "<f4").astype(np.float64)
+        if g.size == 1:  # residual: relative tolerance
+            assert abs(g[0] - w[0]) <= 1e-5 * max(1.0, abs(w[0])), key
+        else:
+            assert np.abs(g - w).max() <= 1e-5, f"{key}: {np.abs(g - w).max():.3e}"
+    else:
+        assert canon(got) == canon(want), key
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_gpu_matches_oracle_on_fresh_streams(cuda, seed):
+    gstore, ostore = PinnedStore(), DictStore()
+    reqs = make_stream(seed, 250, gstore)
+    make_stream(seed, 250, ostore)  # same seed: identical store contents + requests
+    cap = 2 << 20
+    gex = GpuExecutor(ExecutorConfig(capacity=cap, debug=True), gstore)
+    oex = OracleExecutor(cap, ostore)
+    kinds = set()
+    for req in reqs:
+        g = gex.execute(req)
+        o = oex.execute(req)
+        assert response_to_doc(g) == response_to_doc(o), req.request_id
+        assert cache_digest((k, *v) for k, v in gex.cache.snapshot().items()) == \
+            cache_digest((k, *v) for k, v in oex.snapshot().items())
+        if not g.status.ok:
+            kinds.add(g.status.error_kind)
+    assert gstore.keys() == ostore.keys()
+    for k in ostore.keys():
+        _compare_key(k, gstore.get(k), ostore.get(k))
+    assert {"NotFound", "BackendFault", "UnknownKernel", "ArityMismatch"} <= kinds
+    gex.close()

@@ -1,0 +1,222 @@
+"""Kernel parity on the B200, through the executor (C ABI underneath).
+
+Builtins: bit-exact (NaN-canonical) against the reference backend's own
+outputs (golden) and the oracle.  cgemm: rel. Frobenius <= 1e-4 against
+complex128 truth, incl. the BASELINE configs[0] shape (1024^3).  Jacobi:
+max |dx| <= 1e-5 after 500 sweeps at N = 4096 (configs[1]) against the
+float64 oracle.
+"""
+
+import numpy as np
+import pytest
+
+from helpers import canon, load_golden
+from oracle.executor import DictStore, OracleExecutor
+from paper_2212_08146_b200.api import (
+    BufferArg,
+    KaasRequest,
+    KernelInvocation,
+    LaunchDims,
+    ScalarLiteral,
+    f32,
+    i32,
+)
+from paper_2212_08146_b200.gpu_executor import ExecutorConfig, GpuExecutor
+from paper_2212_08146_b200.hoststore import PinnedStore
+from paper_2212_08146_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def gpu(cuda):
+    store = PinnedStore()
+    ex = GpuExecutor(ExecutorConfig(capacity=48 << 30), store)
+    yield ex, store
+    ex.close()
+
+
+def _run(ex, req):
+    r = ex.execute(req)
+    assert r.status.ok, r.status
+    return r
+
+
+def test_builtins_match_reference_backend(gpu):
+    ex, store = gpu
+    for ci, case in enumerate(load_golden("kernels.json.gz")["cases"]):
+        kid = case["kernel"]
+        lits = tuple(ScalarLiteral(t, v) for t, v in case["literals"])
+        bufs, args = [], []
+        for j, h in enumerate(case["inputs"]):
+            data = bytes.fromhex(h)
+            key = f"kc/{ci}/in{j}"
+            store.put(key, data if data else b"\0\0\0\0")
+            size = max(4, len(data))
+            if not data:  # zero-length input (k = 0): a 4-byte placeholder
+                store.put(key, b"\0\0\0\0")
+            bufs.append(BufferArg(f"i{j}", size, "input", key=key, is_const=True))
+            args.append(f"i{j}")
+        out_bytes = 4 * case["out_cells"]
+        if case["out_init"] is not None:
+            store.put(f"kc/{ci}/out", bytes.fromhex(case["out_init"]))
+            bufs.append(BufferArg("o", out_bytes, "inout", key=f"kc/{ci}/out"))
+        else:
+            bufs.append(BufferArg("o", out_bytes, "output", key=f"kc/{ci}/out"))
+        args.append("o")
+        req = KaasRequest(f"kc{ci}", tuple(bufs),
+                          (KernelInvocation(kid, LaunchDims(*case["dims"]), lits, tuple(args)),))
+        _run(ex, req)
+        assert canon(store.get(f"kc/{ci}/out")) == canon(bytes.fromhex(case["expect"])), (ci, kid)
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 1), (3, 5, 7), (64, 64, 64), (130, 70, 33),
+                                   (257, 129, 65), (1000, 64, 147)])
+def test_matmul_bit_exact_vs_oracle(gpu, shape):
+    ex, store = gpu
+    n, m, k = shape
+    rng = np.random.default_rng(n * 7 + m)
+    a = (rng.standard_normal(n * k) * 4).astype("<f4")
+    b = (rng.standard_normal(k * m) * 4).astype("<f4")
+    ostore = DictStore({"a": a.tobytes(), "b": b.tobytes()})
+    store.put("mm/a", a.tobytes())
+    store.put("mm/b", b.tobytes())
+    for cov in (n * m, max(1, n * m - 37)):
+        req = KaasRequest("mm", (BufferArg("a", a.nbytes, "input", key="mm/a"),
+                                 BufferArg("b", b.nbytes, "input", key="mm/b"),
+                                 BufferArg("o", 4 * n * m, "output", key="mm/o")),
+                          (KernelInvocation("matmul", LaunchDims(grid_x=cov), (i32(n), i32(m), i32(k)),
+                                            ("a", "b", "o")),))
+        _run(ex, req)
+        oreq = KaasRequest("mm", (BufferArg("a", a.nbytes, "input", key="a"),
+                                  BufferArg("b", b.nbytes, "input", key="b"),
+                                  BufferArg("o", 4 * n * m, "output", key="o")), req.invocations)
+        OracleExecutor(1 << 30, ostore).execute(oreq)
+        assert canon(store.get("mm/o")) == canon(ostore.get("o"))
+
+
+def _cgemm_check(ex, store, n, m, k, cov=None, seed=0):
+    rng = np.random.default_rng(seed)
+    A = (rng.standard_normal((n, k)) + 1j * rng.standard_normal((n, k))).astype("<c8")
+    B = (rng.standard_normal((k, m)) + 1j * rng.standard_normal((k, m))).astype("<c8")
+    store.put(f"cg/A{n}_{k}_{seed}", A.tobytes())
+    store.put(f"cg/B{k}_{m}_{seed}", B.tobytes())
+    cov = n * m if cov is None else cov
+    req = KaasRequest("cg", (
+        BufferArg("A", A.nbytes, "input", key=f"cg/A{n}_{k}_{seed}", is_const=True),
+        BufferArg("B", B.nbytes, "input", key=f"cg/B{k}_{m}_{seed}", is_const=True),
+        BufferArg("C", 8 * n * m, "output", key="cg/C")),
+        (KernelInvocation("cgemm", LaunchDims(grid_x=cov), (i32(n), i32(m), i32(k)), ("A", "B", "C")),))
+    r = _run(ex, req)
+    assert r.per_invocation[0].simulated_compute_time == ex.backend.timing.compute_time_ns(4 * n * m * k)
+    got = np.frombuffer(store.get("cg/C"), "<c8").reshape(-1)
+    truth = (A.astype(np.complex128) @ B.astype(np.complex128)).reshape(-1)
+    err = np.linalg.norm(got[:cov] - truth[:cov]) / np.linalg.norm(truth[:cov])
+    assert err <= 1e-4, f"{n}x{m}x{k}: rel. Frobenius {err:.3e}"
+    assert np.all(got[cov:] == 0)  # uncovered cells keep the zero fill
+    return err
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 1), (7, 3, 5), (128, 128, 64), (200, 100, 17),
+                                   (129, 257, 33), (333, 65, 1), (512, 384, 256)])
+def test_cgemm_shapes(gpu, shape):
+    ex, store = gpu
+    _cgemm_check(ex, store, *shape)
+
+
+def test_cgemm_partial_coverage_and_empty_k(gpu):
+    ex, store = gpu
+    _cgemm_check(ex, store, 96, 80, 48, cov=96 * 80 - 1234)
+    store.put("cg/z", bytes(8))
+    req = KaasRequest("cz", (BufferArg("A", 8, "input", key="cg/z", is_const=True),
+                             BufferArg("B", 8, "input", key="cg/z", is_const=True),
+                             BufferArg("C", 8 * 12, "output", key="cg/Cz")),
+                      (KernelInvocation("cgemm", LaunchDims(grid_x=12), (i32(3), i32(4), i32(0)),
+                                        ("A", "B", "C")),))
+    _run(ex, req)
+    assert bytes(store.get("cg/Cz")) == bytes(96)
+
+
+def test_cgemm_config1_1024(gpu):
+    """BASELINE configs[0]: cGEMM 1024^3 complex64 kaasReq."""
+    ex, store = gpu
+    err = _cgemm_check(ex, store, 1024, 1024, 1024, seed=11)
+    assert err < 2e-5
+
+
+def test_jacobi_config2_parity(gpu):
+    """BASELINE configs[1]: N = 4096, 500 sweeps; max |dx| <= 1e-5 vs oracle."""
+    ex, store = gpu
+    n, sweeps = 4096, 500
+    A, b = W.seed_jacobi(store, n, prefix="jp")
+    req = W.jacobi_request("jp", n, sweeps, f"jp/A/{n}", f"jp/b/{n}", f"jp/x0/{n}", "jp/x", "jp/r")
+    r = _run(ex, req)
+    assert len(r.per_invocation) == sweeps
+    ostore = DictStore({f"jp/A/{n}": A.tobytes(), f"jp/b/{n}": b.tobytes(),
+                        f"jp/x0/{n}": np.zeros(n, "<f4").tobytes()})
+    o = OracleExecutor(1 << 30, ostore).execute(req)
+    assert o.simulated_total_time == r.simulated_total_time
+    assert o.io_stats == r.io_stats
+    gx = np.frombuffer(store.get("jp/x"), "<f4").astype(np.float64)
+    ox = np.frombuffer(ostore.get("jp/x"), "<f4").astype(np.float64)
+    assert np.abs(gx - ox).max() <= 1e-5
+    gr = np.frombuffer(store.get("jp/r"), "<f4")[0]
+    orr = np.frombuffer(ostore.get("jp/r"), "<f4")[0]
+    assert abs(gr - orr) <= 1e-4 * abs(orr) + 1e-6
+
+
+@pytest.mark.parametrize("n,sweeps,cov", [(1001, 9, None), (64, 5, 40), (4100, 3, None), (12, 1, None)])
+def test_jacobi_edge_shapes(gpu, n, sweeps, cov):
+    """n % 4 != 0 (scalar path), partial coverage, single sweep, odd widths."""
+    ex, store = gpu
+    A, b = W.seed_jacobi(store, n, prefix=f"je{n}")
+    req = W.jacobi_request(f"je{n}", n, sweeps, f"je{n}/A/{n}", f"je{n}/b/{n}", f"je{n}/x0/{n}",
+                           f"je{n}/x", f"je{n}/r")
+    if cov is not None:
+        req = KaasRequest(req.request_id, req.buffers, tuple(
+            KernelInvocation(i.kernel_id, LaunchDims(grid_x=cov), i.literals, i.args) for i in req.invocations))
+    _run(ex, req)
+    ostore = DictStore({f"je{n}/A/{n}": A.tobytes(), f"je{n}/b/{n}": b.tobytes(),
+                        f"je{n}/x0/{n}": np.zeros(n, "<f4").tobytes()})
+    OracleExecutor(1 << 30, ostore).execute(req)
+    g = np.frombuffer(store.get(f"je{n}/x"), "<f4").astype(np.float64)
+    o = np.frombuffer(ostore.get(f"je{n}/x"), "<f4").astype(np.float64)
+    assert np.abs(g - o).max() <= 1e-5
+
+
+def test_jacobi_in_place_alias(gpu):
+    """x_in == x_out on one buffer: the sweep must still read the old x."""
+    ex, store = gpu
+    n = 256
+    A, b = W.seed_jacobi(store, n, prefix="ja")
+    x0 = np.linspace(-1, 1, n).astype("<f4")
+    store.put("ja/x", x0.tobytes())
+    req = KaasRequest("ja", (
+        BufferArg("A", 4 * n * n, "input", key=f"ja/A/{n}", is_const=True),
+        BufferArg("b", 4 * n, "input", key=f"ja/b/{n}", is_const=True),
+        BufferArg("x", 4 * n, "inout", key="ja/x"),
+        BufferArg("r", 4, "output", key="ja/r")),
+        tuple(KernelInvocation("jacobi_sweep", LaunchDims(grid_x=n), (i32(n),), ("A", "b", "x", "x", "r"))
+              for _ in range(3)))
+    _run(ex, req)
+    ostore = DictStore({f"ja/A/{n}": A.tobytes(), f"ja/b/{n}": b.tobytes(), "ja/x": x0.tobytes()})
+    OracleExecutor(1 << 30, ostore).execute(req)
+    g = np.frombuffer(store.get("ja/x"), "<f4")
+    o = np.frombuffer(ostore.get("ja/x"), "<f4")
+    assert np.abs(g.astype(np.float64) - o).max() <= 1e-5
+
+
+def test_saxpy_fill_literal_rounding(gpu):
+    """f32 literals are rounded once on the host (backend.py:165, 207)."""
+    ex, store = gpu
+    x = np.arange(8, dtype="<f4")
+    store.put("lr/x", x.tobytes())
+    v = 0.1  # not representable: must round like np.float32(0.1)
+    req = KaasRequest("lr", (BufferArg("x", 32, "input", key="lr/x"),
+                             BufferArg("o", 32, "output", key="lr/o"),
+                             BufferArg("f", 32, "output", key="lr/f")),
+                      (KernelInvocation("saxpy", LaunchDims(grid_x=8), (i32(8), f32(v)), ("x", "x", "o")),
+                       KernelInvocation("fill", LaunchDims(grid_x=8), (i32(8), f32(v)), ("f",))))
+    _run(ex, req)
+    assert bytes(store.get("lr/o")) == (np.float32(v) * x + x).tobytes()
+    assert bytes(store.get("lr/f")) == np.full(8, np.float32(v), "<f4").tobytes()

@@ -1,0 +1,105 @@
+"""Pool + router + bench harness against the reference's own bench reports.
+
+The product service is driven with oracle-backed executors (CPU), so these
+tests pin the host-side routing / queueing / aggregation logic without a GPU;
+tests/test_gpu_service.py repeats them with the B200 executors.
+"""
+
+import json
+
+import pytest
+
+from helpers import load_golden
+from oracle.executor import OracleExecutor
+from paper_2212_08146_b200.benchlib import report_json, run_bench
+from paper_2212_08146_b200.faults import NotFoundError
+from paper_2212_08146_b200.pool import KaasService
+from paper_2212_08146_b200.workloads import WorkloadSpec
+
+
+class _StoreView:
+    """Oracle expects KeyError for a missing key."""
+
+    def __init__(self, store):
+        self.store = store
+
+    def get(self, key):
+        try:
+            return self.store.get(key)
+        except NotFoundError:
+            raise KeyError(key) from None
+
+    def put(self, key, payload):
+        self.store.put(key, payload)
+
+
+class _Clock:
+    def __init__(self, ex):
+        self.ex = ex
+
+    @property
+    def now_ns(self):
+        return self.ex.now
+
+
+class OracleBacked:
+    def __init__(self, i, store, capacity):
+        self.executor_id = i
+        self.inner = OracleExecutor(capacity, _StoreView(store))
+        self.clock = _Clock(self.inner)
+
+    def execute(self, req):
+        return self.inner.execute(req)
+
+    @property
+    def requests_served(self):
+        return self.inner.served
+
+    def stats(self):
+        return {"executor_id": self.executor_id, "requests": self.inner.served}
+
+
+def oracle_service(n_executors, capacity):
+    def factory(store, policy):
+        return KaasService(store, n_executors=n_executors, policy=policy,
+                           executor_factory=lambda i: OracleBacked(i, store, capacity))
+    return factory
+
+
+def _strip(rep):
+    rep = json.loads(report_json(rep))
+    rep.pop("measured", None)
+    return rep
+
+
+@pytest.mark.parametrize("key,spec,policies,n_exec,cap,warm", [
+    ("bench_zipf_const", WorkloadSpec("zipf_const", 5000, zipf_s=1.0, key_universe=100, seed=42),
+     ["random:1", "affinity:8"], 4, 30 * 64 * 1024, False),
+    ("bench_mixed", WorkloadSpec("mixed", 300, seed=7), ["random:3", "rr", "affinity:8"], 4, None, True),
+    ("bench_matmul_chain", WorkloadSpec("matmul_chain", 6, matrix_dim=16, seed=5), ["rr"], 2, None, True),
+])
+def test_report_matches_reference(key, spec, policies, n_exec, cap, warm):
+    golden = load_golden("routing.json.gz")[key]
+    from paper_2212_08146_b200.workloads import default_capacity
+    capacity = cap if cap is not None else default_capacity(spec)
+    rep = run_bench(spec, policies, n_executors=n_exec, capacity=cap, warm_repeat=warm,
+                    service_factory=oracle_service(n_exec, capacity))
+    assert _strip(rep) == golden
+
+
+def test_affinity_margin_gate():
+    """test_acceptance.py:270-288: affinity beats random by >= 0.30."""
+    rep = load_golden("routing.json.gz")["bench_zipf_const"]
+    margin = rep["policies"]["affinity:8"]["hit_rate"] - rep["policies"]["random:1"]["hit_rate"]
+    assert margin >= 0.30
+
+
+def test_multi_client_service_completes_and_balances():
+    spec = WorkloadSpec("zipf_const", 800, key_universe=40, seed=3)
+    from paper_2212_08146_b200.workloads import default_capacity
+    cap = default_capacity(spec)
+    rep = run_bench(spec, ["affinity:8", "static", "exclusive"], n_executors=4, clients=8,
+                    service_factory=oracle_service(4, cap))
+    for policy, entry in rep["policies"].items():
+        assert entry["requests"] == 800 and entry["errors"] == 0, policy
+        assert sum(entry["per_executor_requests"]) == 800
