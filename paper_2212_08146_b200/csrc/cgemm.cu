@@ -26,6 +26,8 @@
 //      overlaps the main loop of tile t+1.
 #include <cuda.h>
 
+#include <cstdlib>
+
 #include "kaas_internal.cuh"
 
 namespace kaas {
@@ -379,6 +381,187 @@ k_cgemm_tf32x3(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
 }
 
 // ---------------------------------------------------------------------------
+// v2: all four operand tiles in every stage, three products per k-step.
+//
+// Stage = {A_hi, A_lo} [BM x 16] + {B_hi, B_lo} [BN x 16] fp32, 64-byte rows,
+// SWIZZLE_64B (48 KiB at BN = 256, 4 stages).  Per k-step of 8 the single MMA
+// thread issues A_hi.B_lo, A_lo.B_hi, A_hi.B_hi into the tile's TMEM
+// accumulator, so K is walked once instead of three times: 2/3 of v1's
+// L2->SMEM operand traffic for the same tensor work.
+constexpr int BK2 = 16;
+constexpr int STAGES2 = 4;
+
+template <int BN>
+struct Smem2 {
+  alignas(1024) float a_hi[STAGES2][BM * BK2];
+  alignas(1024) float a_lo[STAGES2][BM * BK2];
+  alignas(1024) float b_hi[STAGES2][BN * BK2];
+  alignas(1024) float b_lo[STAGES2][BN * BK2];
+  uint64_t full[STAGES2];
+  uint64_t empty[STAGES2];
+  uint64_t tfull[2];
+  uint64_t tempty[2];
+  uint32_t tmem_base;
+};
+
+// K-major operand tile, SWIZZLE_64B: rows of 64 B, 8-row groups 512 B apart.
+__device__ __forceinline__ uint64_t make_sw64_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)(512 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)4 << 61;  // SWIZZLE_64B
+  return d;
+}
+
+template <int BN>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+k_cgemm_fused4(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+               const GemmShape s, float *__restrict__ C) {
+  extern __shared__ uint8_t smem_raw[];
+  Smem2<BN> &sm = *reinterpret_cast<Smem2<BN> *>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr uint32_t kTmemCols = 2 * BN;
+  constexpr uint32_t kStageBytes = (2 * BM + 2 * BN) * BK2 * 4;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&map_a);
+    tma_prefetch_desc(&map_b);
+    for (int i = 0; i < STAGES2; ++i) {
+      mbar_init(&sm.full[i], 1);
+      mbar_init(&sm.empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sm.tfull[i], 1);
+      mbar_init(&sm.tempty[i], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&sm.tmem_base)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = sm.tmem_base;
+  const int total_tiles = s.num_m * s.num_n;
+  const int kbs = s.kb_per_seg;  // k-blocks of BK2 per tile (one pass)
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+        int mb, nb;
+        tile_coords(s, t, mb, nb);
+        const int arow = mb * BM, brow = nb * BN;
+        for (int kb = 0; kb < kbs; ++kb) {
+          mbar_wait(&sm.empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&sm.full[stage], kStageBytes);
+          tma_load_2d(&map_a, &sm.full[stage], sm.a_hi[stage], kb * BK2, arow);
+          tma_load_2d(&map_a, &sm.full[stage], sm.a_lo[stage], kb * BK2, s.a_lo_row + arow);
+          tma_load_2d(&map_b, &sm.full[stage], sm.b_hi[stage], kb * BK2, brow);
+          tma_load_2d(&map_b, &sm.full[stage], sm.b_lo[stage], kb * BK2, s.b_lo_row + brow);
+          if (++stage == STAGES2) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc(BM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++local) {
+        const int acc = local & 1;
+        const uint32_t acc_phase = (local >> 1) & 1;
+        mbar_wait(&sm.tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * BN;
+        for (int kb = 0; kb < kbs; ++kb) {
+          mbar_wait(&sm.full[stage], phase);
+          tc_fence_after();
+          const uint32_t ah = smem_u32(sm.a_hi[stage]), al = smem_u32(sm.a_lo[stage]);
+          const uint32_t bh = smem_u32(sm.b_hi[stage]), bl = smem_u32(sm.b_lo[stage]);
+#pragma unroll
+          for (int k = 0; k < BK2 / 8; ++k) {
+            const uint32_t off = k * 32;
+            // small terms first, then the main product
+            tc_mma_tf32(tmem_d, make_sw64_desc(ah + off), make_sw64_desc(bl + off), idesc,
+                        (kb | k) != 0);
+            tc_mma_tf32(tmem_d, make_sw64_desc(al + off), make_sw64_desc(bh + off), idesc, 1);
+            tc_mma_tf32(tmem_d, make_sw64_desc(ah + off), make_sw64_desc(bh + off), idesc, 1);
+          }
+          tc_commit(&sm.empty[stage]);
+          if (++stage == STAGES2) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc_commit(&sm.tfull[acc]);
+      }
+    }
+  } else {
+    const int quarter = warp & 3;
+    int local = 0;
+    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++local) {
+      int mb, nb;
+      tile_coords(s, t, mb, nb);
+      const int acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      mbar_wait(&sm.tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = mb * BM + quarter * 32 + lane;
+      const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld32(taddr + c0, v);
+        const int col = nb * BN + c0;
+        if (row < s.M) {
+          float *dst = C + (size_t)row * s.N + col;
+          const unsigned long long g0 = (unsigned long long)row * s.m_complex + (col >> 1);
+          const bool full = (col + 32 <= s.N) && (g0 + 16 <= s.cov) &&
+                            ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0);
+          if (full) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              reinterpret_cast<float4 *>(dst)[q] =
+                  make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                              __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+          } else {
+#pragma unroll
+            for (int q = 0; q < 32; ++q) {
+              const int c = col + q;
+              if (c < s.N && (unsigned long long)row * s.m_complex + (c >> 1) < s.cov)
+                dst[q] = __uint_as_float(v[q]);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&sm.tempty[acc]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) {
+    __syncwarp();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(kTmemCols));
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host side
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
@@ -399,18 +582,39 @@ EncodeTiledFn get_encode() {
   return fn;
 }
 
-int make_map(CUtensorMap *map, const float *base, uint64_t rows, uint64_t ld, uint32_t box_rows) {
+int make_map(CUtensorMap *map, const float *base, uint64_t rows, uint64_t ld, uint32_t box_rows,
+             uint32_t box_k = BK, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return fail(KAAS_E_UNSUPPORTED, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {ld, rows};
   cuuint64_t strides[1] = {ld * sizeof(float)};
-  cuuint32_t box[2] = {BK, box_rows};
+  cuuint32_t box[2] = {box_k, box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)base, dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(KAAS_E_INVALID, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   return 0;
+}
+
+template <int BN>
+int launch_gemm2(cudaStream_t s, int dev, const CUtensorMap &ma, const CUtensorMap &mb,
+                 const GemmShape &shape, float *C) {
+  const size_t smem = sizeof(Smem2<BN>) + 1024;
+  KAAS_CUDA(cudaFuncSetAttribute(k_cgemm_fused4<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+  const int tiles = shape.num_m * shape.num_n;
+  int grid = device_props(dev).sm_count;
+  if (grid > tiles) grid = tiles;
+  k_cgemm_fused4<BN><<<grid, GEMM_THREADS, smem, s>>>(ma, mb, shape, C);
+  count_launch();
+  KAAS_CUDA(cudaGetLastError());
+  return 0;
+}
+
+bool cgemm_v1() {
+  const char *e = getenv("KAAS_CGEMM_V");  // dev A/B: "1" = segment-pass kernel
+  return e && e[0] == '1';
 }
 
 template <int BN>
@@ -465,8 +669,14 @@ int launch_cgemm(cudaStream_t s, int dev, int n, int m, int k, uint64_t cov, con
   const int BNv = narrow ? 128 : 256;
 
   CUtensorMap ma, mbm;
-  if ((rc = make_map(&ma, Ahi, (uint64_t)2 * n, ldk, BM))) return rc;
-  if ((rc = make_map(&mbm, Bhi, (uint64_t)2 * N, ldk, BNv))) return rc;
+  const bool v1 = cgemm_v1();
+  if (v1) {
+    if ((rc = make_map(&ma, Ahi, (uint64_t)2 * n, ldk, BM))) return rc;
+    if ((rc = make_map(&mbm, Bhi, (uint64_t)2 * N, ldk, BNv))) return rc;
+  } else {
+    if ((rc = make_map(&ma, Ahi, (uint64_t)2 * n, ldk, BM, BK2, CU_TENSOR_MAP_SWIZZLE_64B))) return rc;
+    if ((rc = make_map(&mbm, Bhi, (uint64_t)2 * N, ldk, BNv, BK2, CU_TENSOR_MAP_SWIZZLE_64B))) return rc;
+  }
   GemmShape shape;
   shape.M = n;
   shape.N = N;
@@ -477,6 +687,11 @@ int launch_cgemm(cudaStream_t s, int dev, int n, int m, int k, uint64_t cov, con
   shape.num_n = (N + BNv - 1) / BNv;
   shape.m_complex = m;
   shape.cov = cov;
+  if (!v1) {
+    shape.kb_per_seg = ldk / BK2;
+    return narrow ? launch_gemm2<128>(s, dev, ma, mbm, shape, C)
+                  : launch_gemm2<256>(s, dev, ma, mbm, shape, C);
+  }
   return narrow ? launch_gemm<128>(s, dev, ma, mbm, shape, C) : launch_gemm<256>(s, dev, ma, mbm, shape, C);
 }
 

@@ -244,6 +244,22 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
   return v;
 }
 
+// Monotonic grid barrier: the counter is zeroed before each launch; barrier
+// number e completes when the counter reaches (e+1)*gridDim.x.  One
+// release-atomic per CTA, acquire-polling, no reset, no extra fences
+// (release is cumulative over the CTA's writes ordered by bar.sync).
+__device__ __forceinline__ void grid_sync_mono(unsigned *counter, unsigned epoch) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned v;
+    asm volatile("atom.add.release.gpu.global.u32 %0, [%1], 1;" : "=r"(v) : "l"(counter) : "memory");
+    const unsigned target = (epoch + 1) * gridDim.x;
+    while (ld_acquire(counter) < target) {
+    }
+  }
+  __syncthreads();
+}
+
 __device__ __forceinline__ void grid_barrier(unsigned *count, unsigned *gen) {
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -275,7 +291,7 @@ k_jacobi_chain(const __grid_constant__ ChainParams p, float *partials, unsigned 
     float *slot = partials + (s & 1) * kMaxJacobiBlocks;
     if (threadIdx.x == 0) slot[blockIdx.x] = part;
     grid_barrier(sync + 1, sync + 2);
-    if (blockIdx.x == 0 && threadIdx.x < 32) finish_resid(slot, gridDim.x, p.ptrs[p.idx[s][2]]);
+    if (blockIdx.x == 0 && threadIdx.x < 32) finish_resid(slot, gridDim.x, p.ptrs[p.idx[s][2] & 0x7f]);
   }
 }
 
@@ -487,7 +503,7 @@ k_jacobi_tma(const __grid_constant__ ChainParams p, int stages, float *partials,
       float *slot = partials + (s & 1) * kMaxJacobiBlocks;
       if (ctid == 0) slot[blockIdx.x] = part;
       consumer_grid_barrier(sync + 1, sync + 2, ctid);
-      if (blockIdx.x == 0 && cw == 0) finish_resid(slot, gridDim.x, p.ptrs[p.idx[s][2]]);
+      if (blockIdx.x == 0 && cw == 0) finish_resid(slot, gridDim.x, p.ptrs[p.idx[s][2] & 0x7f]);
     } else {
       if (ctid == 0) {
         partials[blockIdx.x] = part;
@@ -497,10 +513,349 @@ k_jacobi_tma(const __grid_constant__ ChainParams p, int stages, float *partials,
       consumers_sync();
       if (last && cw == 0) {
         __threadfence();
-        finish_resid(partials, gridDim.x, p.ptrs[p.idx[s][2]]);
+        finish_resid(partials, gridDim.x, p.ptrs[p.idx[s][2] & 0x7f]);
         if (lane == 0) *sync = 0u;
       }
     }
+  }
+}
+
+// ---- direct-load sweep kernel (default path) ---------------------------------
+//
+// A row of the GEMV is used exactly once per sweep, so staging it through
+// shared memory only adds smem-pipe traffic (TMA write + LDS read of every
+// byte).  Measured on B200: an L2-resident 64 MiB buffer re-reads at ~19 TB/s
+// with 128-bit LDG from all SMs, while the smem-staged kernel above tops out
+// near 7 TB/s on the smem pipe.  This kernel loads A straight into registers:
+//   * 8 warps per CTA, one CTA per SM, band of ~n/148 rows per CTA;
+//   * warp w owns columns [w*CW, (w+1)*CW) (CW = KC*128): its x slice lives in
+//     KC float4 registers per lane for the whole sweep;
+//   * rows are processed G at a time with the next group's KC*G 128-bit loads
+//     issued before the current group's FMAs (software pipelined);
+//   * per-lane row partials are combined with a 31-shuffle reduce-scatter
+//     (lane l ends up owning row l of the 32-row block), then across the 8
+//     warps through smem in fixed order.
+constexpr int kLdgWarps = 8;
+constexpr int kLdgThreads = kLdgWarps * 32;
+constexpr int kRowBlock = 32;
+
+// reduce-scatter of v[0..31] across the warp: afterwards lane l holds the
+// warp-wide sum of row l (each step keeps the half selected by one lane bit).
+__device__ __forceinline__ float reduce_scatter32(float (&v)[kRowBlock], int lane) {
+#pragma unroll
+  for (int step = 0; step < 5; ++step) {
+    const int off = 16 >> step;
+    const int half = 16 >> step;  // number of live values halves each step
+    const bool upper = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const float send = upper ? v[i] : v[i + half];
+      const float keep = upper ? v[i + half] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  return v[0];
+}
+
+
+template <int KC, int G, bool kChain>
+__device__ __forceinline__ float sweep_ldg(int n, int r0, int r1, const float *__restrict__ A,
+                                           const float *__restrict__ b, const float *x_in,
+                                           float *x_out, float (*red)[kRowBlock], float *part,
+                                           uint64_t pol) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n4 = n >> 2;
+  // this lane's columns: c4[k] = warp*KC*32 + k*32 + lane (float4 index)
+  float4 xr[KC];
+  int c4[KC];
+#pragma unroll
+  for (int k = 0; k < KC; ++k) {
+    c4[k] = (warp * KC + k) * 32 + lane;
+    xr[k] = c4[k] < n4 ? (kChain ? __ldcg(reinterpret_cast<const float4 *>(x_in) + c4[k])
+                                 : __ldg(reinterpret_cast<const float4 *>(x_in) + c4[k]))
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  const int wlo = warp * KC * 128, whi = wlo + KC * 128;  // this warp's column range
+  float res = 0.f;
+  for (int rb = r0; rb < r1; rb += kRowBlock) {
+    const int R = min(kRowBlock, r1 - rb);
+    float acc[kRowBlock];
+#pragma unroll
+    for (int r = 0; r < kRowBlock; ++r) acc[r] = 0.f;
+    float4 cur[G][KC], nxt[G][KC];
+    auto load = [&](float4 (&dst)[G][KC], int g0) {
+#pragma unroll
+      for (int g = 0; g < G; ++g)
+#pragma unroll
+        for (int k = 0; k < KC; ++k) {
+          const int r = g0 + g;
+          dst[g][k] = (r < R && c4[k] < n4)
+                          ? ld_a(A + (size_t)(rb + r) * n + 4 * c4[k], pol)
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    };
+    load(cur, 0);
+#pragma unroll
+    for (int g0 = 0; g0 < kRowBlock; g0 += G) {
+      if (g0 + G < kRowBlock && g0 + G < R) load(nxt, g0 + G);
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const int i = rb + g0 + g;
+        if (i >= wlo && i < whi) {  // warp-uniform: this warp holds the diagonal of row i
+#pragma unroll
+          for (int k = 0; k < KC; ++k) acc[g0 + g] += dot_masked(cur[g][k], xr[k], i - 4 * c4[k]);
+        } else {
+#pragma unroll
+          for (int k = 0; k < KC; ++k) {
+            float a = acc[g0 + g];
+            a = fmaf(cur[g][k].x, xr[k].x, a);
+            a = fmaf(cur[g][k].y, xr[k].y, a);
+            a = fmaf(cur[g][k].z, xr[k].z, a);
+            a = fmaf(cur[g][k].w, xr[k].w, a);
+            acc[g0 + g] = a;
+          }
+        }
+      }
+      if (g0 + G < kRowBlock) {
+#pragma unroll
+        for (int g = 0; g < G; ++g)
+#pragma unroll
+          for (int k = 0; k < KC; ++k) cur[g][k] = nxt[g][k];
+      }
+    }
+    const float mine = reduce_scatter32(acc, lane);
+    red[warp][lane] = mine;
+    __syncthreads();
+    if (threadIdx.x < R) {
+      const int r = threadIdx.x, i = rb + r;
+      float s = 0.f;
+#pragma unroll
+      for (int w = 0; w < kLdgWarps; ++w) s += red[w][r];
+      const float xi = kChain ? __ldcg(x_in + i) : __ldg(x_in + i);
+      const float xn = (b[i] - s) / __ldg(A + (size_t)i * n + i);  // IEEE div.rn
+      x_out[i] = xn;
+      res += fabsf(xn - xi);
+    }
+    __syncthreads();
+  }
+  // CTA residual partial (threads 0..31 hold row residuals), fixed order
+  if (warp == 0) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) res += __shfl_xor_sync(0xffffffffu, res, off);
+    if (lane == 0) *part = res;
+  }
+  __syncthreads();
+  return *part;
+}
+
+template <int KC, int G, bool kChain>
+__global__ void __launch_bounds__(kLdgThreads, 1)
+k_jacobi_ldg(const __grid_constant__ ChainParams p, float *partials, unsigned *sync) {
+  __shared__ float red[kLdgWarps][kRowBlock];
+  __shared__ float part;
+  __shared__ bool last;
+  int r0, r1;
+  band(p.cov, r0, r1);
+  const uint64_t pol = l2_policy(p.keep_l2 != 0);
+  for (int s = 0; s < p.sweeps; ++s) {
+    const float *x_in = p.ptrs[p.idx[s][0]];
+    float *x_out = p.ptrs[p.idx[s][1]];
+    const float cta = sweep_ldg<KC, G, kChain>(p.n, r0, r1, p.A, p.b, x_in, x_out, red, &part, pol);
+    if (kChain) {
+      float *slot = partials + (s & 1) * kMaxJacobiBlocks;
+      if (threadIdx.x == 0) slot[blockIdx.x] = cta;
+      grid_barrier(sync + 1, sync + 2);
+      if (blockIdx.x == 0 && threadIdx.x < 32) finish_resid(slot, gridDim.x, p.ptrs[p.idx[s][2] & 0x7f]);
+    } else {
+      if (threadIdx.x == 0) {
+        partials[blockIdx.x] = cta;
+        __threadfence();
+        last = atomicAdd(sync, 1u) == gridDim.x - 1;
+      }
+      __syncthreads();
+      if (last && threadIdx.x < 32) {
+        __threadfence();
+        finish_resid(partials, gridDim.x, p.ptrs[p.idx[s][2] & 0x7f]);
+        if (threadIdx.x == 0) *sync = 0u;
+      }
+    }
+  }
+}
+
+// ---- row-per-warp direct kernel ----------------------------------------------
+//
+// One warp per row, all of the CTA's band in flight at once (~28 warps for
+// n = 4096), 8 x 128-bit loads of A per lane in flight, x staged once per
+// sweep in smem (16 KiB) and read with conflict-free 128-bit LDS, four
+// independent FMA chains, a 5-step shuffle reduce per row, no CTA barrier
+// inside the sweep.
+constexpr int kRowsMaxWarps = 28;  // 896 threads -> 72 registers per thread
+constexpr int kRowsUnroll = 8;
+constexpr int kRowsPre = 4;  // loads hoisted above the x staging
+
+template <bool kChain, bool kPrefetch>
+__global__ void __launch_bounds__(kRowsMaxWarps * 32, 1)
+k_jacobi_rows(const __grid_constant__ ChainParams p, float *partials, unsigned *sync) {
+  extern __shared__ __align__(16) float xs[];  // n floats
+  __shared__ float wres[kRowsMaxWarps];
+  __shared__ bool last;
+  const int n = p.n, n4 = n >> 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  int r0, r1;
+  band(p.cov, r0, r1);
+  const uint64_t pol = l2_policy(p.keep_l2 != 0);
+  const float4 *x4 = reinterpret_cast<const float4 *>(xs);
+  const int first = r0 + warp;                                  // this warp's first row
+  const bool full_first = kPrefetch && n4 >= 32 * kRowsPre;  // hoistable first loads
+  float4 pre[kPrefetch ? kRowsPre : 1];
+  for (int s = 0; s < p.sweeps; ++s) {
+    const float *x_in = p.ptrs[p.idx[s][0]];
+    float *x_out = p.ptrs[p.idx[s][1]];
+    const bool want_resid = !kChain || (p.idx[s][2] & 0x80) != 0;
+    // A does not depend on x: put the first 8 loads of this warp's first row
+    // in flight before staging x, so the two L2 round trips overlap
+    if (kPrefetch && first < r1 && full_first) {
+#pragma unroll
+      for (int u = 0; u < kRowsPre; ++u)
+        pre[kPrefetch ? u : 0] = ld_a(p.A + (size_t)first * n + 4 * (lane + 32 * u), pol);
+    }
+    for (int e = threadIdx.x; e < n4; e += blockDim.x)
+      reinterpret_cast<float4 *>(xs)[e] = kChain ? __ldcg(reinterpret_cast<const float4 *>(x_in) + e)
+                                                 : __ldg(reinterpret_cast<const float4 *>(x_in) + e);
+    __syncthreads();
+    float res = 0.f;
+    for (int i = first; i < r1; i += nwarps) {
+      const float *row = p.A + (size_t)i * n;
+      const int it_d = (i >> 2) / 32;  // the (warp-uniform) iteration holding the diagonal
+      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+      auto group = [&](const float4 *av, int cnt, int j4, int it) {
+#pragma unroll
+        for (int u = 0; u < cnt; ++u) {
+          float4 xv = x4[j4 + 32 * u];
+          if (it + u == it_d) {
+            const int d = i - 4 * (j4 + 32 * u);
+            xv.x = d == 0 ? 0.f : xv.x;
+            xv.y = d == 1 ? 0.f : xv.y;
+            xv.z = d == 2 ? 0.f : xv.z;
+            xv.w = d == 3 ? 0.f : xv.w;
+          }
+          a0 = fmaf(av[u].x, xv.x, a0);
+          a1 = fmaf(av[u].y, xv.y, a1);
+          a2 = fmaf(av[u].z, xv.z, a2);
+          a3 = fmaf(av[u].w, xv.w, a3);
+        }
+      };
+      int it = 0;
+      int j4 = lane;
+      if (kPrefetch && i == first && full_first) {  // first group: already in flight
+        group(pre, kRowsPre, j4, it);
+        j4 += 32 * kRowsPre;
+        it += kRowsPre;
+      }
+      for (; j4 + 32 * (kRowsUnroll - 1) < n4; j4 += 32 * kRowsUnroll, it += kRowsUnroll) {
+        float4 av[kRowsUnroll];
+#pragma unroll
+        for (int u = 0; u < kRowsUnroll; ++u) av[u] = ld_a(row + 4 * (j4 + 32 * u), pol);
+        group(av, kRowsUnroll, j4, it);
+      }
+      for (; j4 < n4; j4 += 32, ++it) {
+        const float4 a = ld_a(row + 4 * j4, pol);
+        float4 xv = x4[j4];
+        if (it == it_d) {
+          const int d = i - 4 * j4;
+          xv.x = d == 0 ? 0.f : xv.x;
+          xv.y = d == 1 ? 0.f : xv.y;
+          xv.z = d == 2 ? 0.f : xv.z;
+          xv.w = d == 3 ? 0.f : xv.w;
+        }
+        a0 = fmaf(a.x, xv.x, a0);
+        a1 = fmaf(a.y, xv.y, a1);
+        a2 = fmaf(a.z, xv.z, a2);
+        a3 = fmaf(a.w, xv.w, a3);
+      }
+      float v = (a0 + a1) + (a2 + a3);
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      if (lane == 0) {
+        const float xn = (p.b[i] - v) / __ldg(row + i);  // IEEE div.rn
+        x_out[i] = xn;
+        res += fabsf(xn - xs[i]);
+      }
+    }
+    if (want_resid && lane == 0) wres[warp] = res;
+    if (kChain) {
+      float *slot = partials + (s & 1) * kMaxJacobiBlocks;
+      if (want_resid) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          float cta = 0.f;
+          for (int w = 0; w < nwarps; ++w) cta += wres[w];
+          slot[blockIdx.x] = cta;
+        }
+      }
+      grid_sync_mono(sync + 3, (unsigned)s);  // also: xs reads done before the next stage-in
+      if (want_resid && blockIdx.x == 0 && threadIdx.x < 32)
+        finish_resid(slot, gridDim.x, p.ptrs[p.idx[s][2] & 0x7f]);
+    } else {
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        float cta = 0.f;
+        for (int w = 0; w < nwarps; ++w) cta += wres[w];
+        partials[blockIdx.x] = cta;
+        __threadfence();
+        last = atomicAdd(sync, 1u) == gridDim.x - 1;
+      }
+      __syncthreads();
+      if (last && threadIdx.x < 32) {
+        __threadfence();
+        finish_resid(partials, gridDim.x, p.ptrs[p.idx[s][2] & 0x7f]);
+        if (threadIdx.x == 0) *sync = 0u;
+      }
+    }
+  }
+}
+
+// threads for the row kernel: one warp per band row, 4..32 warps
+int rows_threads(int dev, uint64_t cov) {
+  const int sms = device_props(dev).sm_count;
+  int rows = (int)((cov + sms - 1) / sms);
+  if (rows < 4) rows = 4;
+  if (rows > kRowsMaxWarps) rows = kRowsMaxWarps;
+  return rows * 32;
+}
+
+bool rows_prefetch() {
+  const char *e = getenv("KAAS_JACOBI_PREFETCH");  // dev A/B (default on)
+  return !(e && e[0] == '0');
+}
+
+bool use_rows_kernel(int n) {
+  const char *e = getenv("KAAS_JACOBI_PATH");  // dev A/B: rows (default) | ldg | tma
+  if (e && (e[0] == 'l' || e[0] == 't')) return false;
+  return n % 4 == 0 && (size_t)n * 4 <= 160 * 1024;
+}
+
+// KC = float4 chunks per lane (x registers), 0 = direct path not applicable
+int ldg_kc(int n) {
+  if (const char *e = getenv("KAAS_JACOBI_PATH"))  // dev A/B: "tma" forces the staged kernel
+    if (e[0] == 't' || e[0] == 'r') return 0;
+  if (n % 4 != 0) return 0;
+  const int chunks = (n + 127) / 128;
+  const int per = (chunks + kLdgWarps - 1) / kLdgWarps;
+  if (per <= 1) return 1;
+  if (per <= 2) return 2;
+  if (per <= 4) return 4;
+  if (per <= 8) return 8;
+  return 0;
+}
+
+template <bool kChain>
+const void *ldg_kernel(int kc) {
+  switch (kc) {
+    case 1: return (const void *)k_jacobi_ldg<1, 8, kChain>;
+    case 2: return (const void *)k_jacobi_ldg<2, 8, kChain>;
+    case 4: return (const void *)k_jacobi_ldg<4, 4, kChain>;
+    default: return (const void *)k_jacobi_ldg<8, 2, kChain>;
   }
 }
 
@@ -564,6 +919,53 @@ int launch_jacobi(cudaStream_t s, int dev, int n, uint64_t cov, const float *A, 
   int blocks = device_props(dev).sm_count;
   if ((uint64_t)blocks > cov) blocks = cov > 0 ? (int)cov : 1;
   if (blocks > kMaxJacobiBlocks) blocks = kMaxJacobiBlocks;
+  if (use_rows_kernel(n) && aligned16(A) && aligned16(x_in)) {
+    static thread_local ChainParams p;
+    p.A = A;
+    p.b = b;
+    p.n = n;
+    p.cov = (int)cov;
+    p.sweeps = 1;
+    p.keep_l2 = 0;
+    p.ptrs[0] = const_cast<float *>(x_in);
+    p.ptrs[1] = x_out;
+    p.ptrs[2] = resid;
+    p.idx[0][0] = 0;
+    p.idx[0][1] = 1;
+    p.idx[0][2] = 2;
+    float *partials = sc->jac_partials;
+    unsigned *sync = sc->jac_sync;
+    void *args[] = {(void *)&p, (void *)&partials, (void *)&sync};
+    const size_t smem = (size_t)n * 4;
+    KAAS_CUDA(cudaFuncSetAttribute((const void *)k_jacobi_rows<false, false>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    KAAS_CUDA(cudaLaunchKernel((const void *)k_jacobi_rows<false, false>, dim3(blocks),
+                               dim3(rows_threads(dev, cov)), args, smem, s));
+    count_launch();
+    return 0;
+  }
+  const int kcl = ldg_kc(n);
+  if (kcl > 0 && aligned16(A) && aligned16(x_in)) {
+    static thread_local ChainParams p;
+    p.A = A;
+    p.b = b;
+    p.n = n;
+    p.cov = (int)cov;
+    p.sweeps = 1;
+    p.keep_l2 = 0;
+    p.ptrs[0] = const_cast<float *>(x_in);
+    p.ptrs[1] = x_out;
+    p.ptrs[2] = resid;
+    p.idx[0][0] = 0;
+    p.idx[0][1] = 1;
+    p.idx[0][2] = 2;
+    float *partials = sc->jac_partials;
+    unsigned *sync = sc->jac_sync;
+    void *args[] = {(void *)&p, (void *)&partials, (void *)&sync};
+    KAAS_CUDA(cudaLaunchKernel(ldg_kernel<false>(kcl), dim3(blocks), dim3(kLdgThreads), args, 0, s));
+    count_launch();
+    return 0;
+  }
   const int stages = tma_stages(n, device_props(dev).max_smem_optin);
   if (stages >= 2 && aligned16(A) && aligned16(x_in)) {
     static thread_local ChainParams p;
@@ -615,8 +1017,19 @@ int launch_jacobi_chain(cudaStream_t s, int dev, const JacobiChain &c, StreamScr
   if (!aligned16(c.A)) kc = 0;
   for (int t = 0; t < c.sweeps && kc; ++t)
     if (!aligned16(c.x_in[t])) kc = 0;
+  bool use_rows = use_rows_kernel(c.n) && aligned16(c.A);
+  for (int t = 0; t < c.sweeps && use_rows; ++t)
+    if (!aligned16(c.x_in[t])) use_rows = false;
+  const void *rfn = rows_prefetch() ? (const void *)k_jacobi_rows<true, true>
+                                    : (const void *)k_jacobi_rows<true, false>;
+  if (use_rows)
+    KAAS_CUDA(cudaFuncSetAttribute(rfn, cudaFuncAttributeMaxDynamicSharedMemorySize, c.n * 4));
+  const int kcl = use_rows ? 0 : ldg_kc(c.n);
+  bool use_ldg = kcl > 0 && aligned16(c.A);
+  for (int t = 0; t < c.sweeps && use_ldg; ++t)
+    if (!aligned16(c.x_in[t])) use_ldg = false;
   const int stages = tma_stages(c.n, device_props(dev).max_smem_optin);
-  bool use_tma = stages >= 2 && aligned16(c.A);
+  bool use_tma = !use_ldg && stages >= 2 && aligned16(c.A);
   for (int t = 0; t < c.sweeps && use_tma; ++t)
     if (!aligned16(c.x_in[t])) use_tma = false;
   const size_t tsmem = use_tma ? tma_smem(c.n, stages) : 0;
@@ -653,7 +1066,11 @@ int launch_jacobi_chain(cudaStream_t s, int dev, const JacobiChain &c, StreamScr
       if (a < 0 || o < 0 || r < 0) break;
       p.idx[cnt][0] = (unsigned char)a;
       p.idx[cnt][1] = (unsigned char)o;
-      p.idx[cnt][2] = (unsigned char)r;
+      // residual slots are never read inside a run, so only the last write to
+      // each slot is observable: flag it (0x80) and skip the others' finish
+      bool last_writer = true;
+      for (int u = t + 1; u < c.sweeps && last_writer; ++u) last_writer = c.resid[u] != c.resid[t];
+      p.idx[cnt][2] = (unsigned char)(r | (last_writer ? 0x80 : 0));
     }
     if (cnt == 0) return fail(KAAS_E_INVALID, "jacobi chain: too many distinct buffers");
     p.sweeps = cnt;
@@ -661,7 +1078,16 @@ int launch_jacobi_chain(cudaStream_t s, int dev, const JacobiChain &c, StreamScr
     if ((uint64_t)blocks > c.cov) blocks = c.cov > 0 ? (int)c.cov : 1;
     float *partials = sc->jac_partials;
     unsigned *sync = sc->jac_sync;
-    if (use_tma) {
+    if (use_rows) {
+      KAAS_CUDA(cudaMemsetAsync(sync + 3, 0, sizeof(unsigned), s));  // monotonic barrier counter
+      void *rargs[] = {(void *)&p, (void *)&partials, (void *)&sync};
+      KAAS_CUDA(cudaLaunchCooperativeKernel(rfn, dim3(blocks),
+                                            dim3(rows_threads(dev, c.cov)), rargs, (size_t)c.n * 4, s));
+    } else if (use_ldg) {
+      void *largs[] = {(void *)&p, (void *)&partials, (void *)&sync};
+      KAAS_CUDA(cudaLaunchCooperativeKernel(ldg_kernel<true>(kcl), dim3(blocks), dim3(kLdgThreads),
+                                            largs, 0, s));
+    } else if (use_tma) {
       int st = stages;
       void *targs[] = {(void *)&p, (void *)&st, (void *)&partials, (void *)&sync};
       KAAS_CUDA(cudaLaunchCooperativeKernel(tfn, dim3(blocks), dim3(kTmaThreads), targs, tsmem, s));

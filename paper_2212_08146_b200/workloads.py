@@ -16,7 +16,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .api import BufferArg, KaasRequest, KernelInvocation, LaunchDims, i32
+from .api import BufferArg, KaasRequest, KernelInvocation, LaunchDims, f32, i32
 
 WORKLOAD_KINDS = ("matmul_chain", "zipf_const", "mixed")
 ZIPF_BLOB_BYTES = 64 * 1024
@@ -229,3 +229,53 @@ def resnet50_gemms() -> list[tuple[str, int, int, int]]:
             cin = out
     layers.append(("fc", 1, 1000, 2048))
     return layers
+
+
+def resnet_chain_request(request_id: str, prefix: str = "resnet", layers=None,
+                         out_key: str | None = None) -> KaasRequest:
+    """BASELINE configs[4]: a ResNet-50-shaped chain of bit-exact ``matmul``
+    invocations (conv-as-GEMM, batch 1) over const weights, with residual
+    ``vector_add``s at block ends and ping-pong ephemeral activations sized to
+    the largest layer -- intermediate buffers are reused, never flushed."""
+    layers = resnet50_gemms() if layers is None else layers
+    cap = max(max(m * k, m * n) for _, m, n, k in layers)
+    bufs = [BufferArg("x", 4 * layers[0][1] * layers[0][3], "input", key=f"{prefix}/x")]
+    for li, (name, m, n, k) in enumerate(layers):
+        bufs.append(BufferArg(f"w{li}", 4 * k * n, "input", key=f"{prefix}/w/{name}", is_const=True))
+    bufs += [BufferArg("a0", 4 * cap, "inout", is_ephemeral=True),
+             BufferArg("a1", 4 * cap, "inout", is_ephemeral=True),
+             BufferArg("skip", 4 * cap, "inout", is_ephemeral=True),
+             BufferArg("out", 4 * layers[-1][1] * layers[-1][2], "output",
+                       key=out_key or f"{prefix}/out")]
+    invs = []
+    cur = "x"
+    nxt = {"x": "a0", "a0": "a1", "a1": "a0"}
+    for li, (name, m, n, k) in enumerate(layers):
+        dst = "out" if li == len(layers) - 1 else nxt[cur]
+        if name.endswith("_1x1a"):  # block input -> skip path
+            cells = min(m * k, cap)
+            invs.append(KernelInvocation("fill", grid_for(cells), (i32(cells), f32(0.0)), ("skip",)))
+            invs.append(KernelInvocation("vector_add", grid_for(cells), (i32(cells),),
+                                         (cur, "skip", "skip")))
+        if name.endswith("_proj"):  # projection shortcut replaces the identity skip
+            invs.append(KernelInvocation("matmul", grid_for(m * n), (i32(m), i32(n), i32(k)),
+                                         ("skip", f"w{li}", "skip")))
+            continue
+        invs.append(KernelInvocation("matmul", grid_for(m * n), (i32(m), i32(n), i32(k)),
+                                     (cur, f"w{li}", dst)))
+        if name.endswith("_1x1b"):  # block end: residual add
+            invs.append(KernelInvocation("vector_add", grid_for(m * n), (i32(m * n),),
+                                         (dst, "skip", dst)))
+        cur = dst
+    return KaasRequest(request_id, tuple(bufs), tuple(invs))
+
+
+def seed_resnet(store, prefix: str = "resnet", layers=None, seed: int = 0) -> None:
+    """Synthetic He-scaled weights and a random input image (f32)."""
+    layers = resnet50_gemms() if layers is None else layers
+    rng = np.random.default_rng(seed)
+    _, m0, _, k0 = layers[0]
+    store.put(f"{prefix}/x", rng.standard_normal(m0 * k0, dtype=np.float32).tobytes())
+    for name, m, n, k in layers:
+        w = (rng.standard_normal(k * n, dtype=np.float32) * np.float32((2.0 / k) ** 0.5))
+        store.put(f"{prefix}/w/{name}", w.astype(np.float32).tobytes())
