@@ -141,6 +141,24 @@ int kaas_launch(int dev, uint64_t stream, const kaas_launch_desc *desc);
  * their x buffers are fused into one persistent multi-sweep launch. */
 int kaas_launch_batch(int dev, uint64_t stream, const kaas_launch_desc *descs, int n);
 
+/* Progressive write-back (new; overlaps Executor.execute's flush loop,
+ * executor.py:371-380, with the kernel that produces the flushed buffer).
+ * Copies bytes [0, bytes) of descs[desc_index].ptrs[arg_index] into the
+ * pinned host_dst on out_stream, ordered after that kernel.  cGEMM outputs
+ * are streamed per finished row panel while later tiles still compute
+ * (device-side panel counters + cuStreamWaitValue32); other kernels copy
+ * once the kernel completes.  The descriptor must be the last in the batch
+ * that writes that buffer. */
+typedef struct kaas_stream_out {
+  int32_t desc_index;
+  int32_t arg_index;
+  uint64_t out_stream;
+  void *host_dst;
+  uint64_t bytes;
+} kaas_stream_out;
+int kaas_launch_batch_ex(int dev, uint64_t stream, const kaas_launch_desc *descs, int n,
+                         const kaas_stream_out *outs, int n_outs);
+
 #ifdef __cplusplus
 }
 #endif

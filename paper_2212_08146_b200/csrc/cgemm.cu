@@ -48,16 +48,30 @@ __device__ __forceinline__ float tf32_rna(float x) {
 }
 
 // A_il [n x k2] (k2 = 2k) -> Ahi/Alo [n x ldk], zero padded past k2.
+// One CTA per row band, 128-bit loads/stores when the row is 16B-aligned.
 __global__ void k_prep_a(int n, int k2, int ldk, const float *__restrict__ A, float *__restrict__ Ahi,
                          float *__restrict__ Alo) {
-  const size_t total = (size_t)n * ldk;
-  const size_t stride = (size_t)gridDim.x * blockDim.x;
-  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
-    const int r = (int)(e / ldk), q = (int)(e % ldk);
-    const float x = q < k2 ? A[(size_t)r * k2 + q] : 0.f;
-    const float hi = tf32_rna(x);
-    Ahi[e] = hi;
-    Alo[e] = x - hi;
+  const bool vec = (k2 & 3) == 0;
+  for (int r = blockIdx.x; r < n; r += gridDim.x) {
+    const float *src = A + (size_t)r * k2;
+    float *hi = Ahi + (size_t)r * ldk, *lo = Alo + (size_t)r * ldk;
+    if (vec) {
+      for (int q4 = threadIdx.x; q4 < (ldk >> 2); q4 += blockDim.x) {
+        const int q = q4 << 2;
+        const float4 x = q < k2 ? __ldg(reinterpret_cast<const float4 *>(src) + q4)
+                                : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 h = make_float4(tf32_rna(x.x), tf32_rna(x.y), tf32_rna(x.z), tf32_rna(x.w));
+        reinterpret_cast<float4 *>(hi)[q4] = h;
+        reinterpret_cast<float4 *>(lo)[q4] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+      }
+    } else {
+      for (int q = threadIdx.x; q < ldk; q += blockDim.x) {
+        const float x = q < k2 ? src[q] : 0.f;
+        const float h = tf32_rna(x);
+        hi[q] = h;
+        lo[q] = x - h;
+      }
+    }
   }
 }
 
@@ -219,9 +233,11 @@ struct Smem {
   uint32_t tmem_base;
 };
 
+constexpr int kGroupM = 8;  // m-blocks per raster group (= one write-back panel)
+
 __device__ __forceinline__ void tile_coords(const GemmShape &s, int t, int &mb, int &nb) {
   // group 8 m-blocks together so concurrently running CTAs share B tiles in L2
-  constexpr int GM = 8;
+  constexpr int GM = kGroupM;
   const int per_group = GM * s.num_n;
   const int g = t / per_group;
   const int first_m = g * GM;
@@ -418,7 +434,7 @@ __device__ __forceinline__ uint64_t make_sw64_desc(uint32_t saddr) {
 template <int BN>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
 k_cgemm_fused4(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-               const GemmShape s, float *__restrict__ C) {
+               const GemmShape s, float *__restrict__ C, unsigned *panel_done) {
   extern __shared__ uint8_t smem_raw[];
   Smem2<BN> &sm = *reinterpret_cast<Smem2<BN> *>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -549,6 +565,16 @@ k_cgemm_fused4(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
       }
       tc_fence_before();
       mbar_arrive(&sm.tempty[acc]);
+      if (panel_done != nullptr) {
+        // publish "tile done" for its row panel (group of GM m-blocks) so the
+        // copy stream can stream that panel to the host while tiles compute
+        __threadfence();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (warp == 2 && lane == 0) {
+          __threadfence_system();
+          atomicAdd(&panel_done[mb / kGroupM], 1u);
+        }
+      }
     }
   }
   tc_fence_before();
@@ -597,18 +623,73 @@ int make_map(CUtensorMap *map, const float *base, uint64_t rows, uint64_t ld, ui
   return 0;
 }
 
+typedef CUresult (*WaitValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+WaitValue32Fn get_wait_value() {
+  static WaitValue32Fn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<WaitValue32Fn>(p);
+  });
+  return fn;
+}
+
 template <int BN>
 int launch_gemm2(cudaStream_t s, int dev, const CUtensorMap &ma, const CUtensorMap &mb,
-                 const GemmShape &shape, float *C) {
+                 const GemmShape &shape, float *C, StreamScratch *sc, const ProgressiveOut *po) {
   const size_t smem = sizeof(Smem2<BN>) + 1024;
   KAAS_CUDA(cudaFuncSetAttribute(k_cgemm_fused4<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
   const int tiles = shape.num_m * shape.num_n;
   int grid = device_props(dev).sm_count;
   if (grid > tiles) grid = tiles;
-  k_cgemm_fused4<BN><<<grid, GEMM_THREADS, smem, s>>>(ma, mb, shape, C);
+  const int npanels = (shape.num_m + kGroupM - 1) / kGroupM;
+  WaitValue32Fn waitv = get_wait_value();
+  const bool progressive = po != nullptr && waitv != nullptr && npanels > 1 &&
+                           npanels <= kMaxPanels && sc->panel_done != nullptr;
+  cudaEvent_t ev_ready = nullptr, ev_done = nullptr;
+  if (po) {
+    KAAS_CUDA(cudaEventCreateWithFlags(&ev_ready, cudaEventDisableTiming));
+    KAAS_CUDA(cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming));
+  }
+  if (progressive) {
+    KAAS_CUDA(cudaMemsetAsync(sc->panel_done, 0, npanels * sizeof(unsigned), s));
+    KAAS_CUDA(cudaEventRecord(ev_ready, s));
+    KAAS_CUDA(cudaStreamWaitEvent(po->out_stream, ev_ready, 0));
+  }
+  k_cgemm_fused4<BN><<<grid, GEMM_THREADS, smem, s>>>(ma, mb, shape, C,
+                                                      progressive ? sc->panel_done : nullptr);
   count_launch();
   KAAS_CUDA(cudaGetLastError());
+  if (!po) return 0;
+  const uint64_t row_bytes = (uint64_t)shape.m_complex * 8;
+  uint64_t copied = 0;
+  if (progressive) {
+    for (int p = 0; p < npanels; ++p) {
+      const int mb0 = p * kGroupM, mbs = min(kGroupM, shape.num_m - mb0);
+      const int row0 = mb0 * BM, row1 = min(shape.M, (mb0 + mbs) * BM);
+      const unsigned want = (unsigned)(mbs * shape.num_n);
+      CUresult r = waitv((CUstream)po->out_stream, (CUdeviceptr)(sc->panel_done + p), want,
+                         0 /* CU_STREAM_WAIT_VALUE_GEQ */);
+      if (r != CUDA_SUCCESS) return fail(KAAS_E_UNSUPPORTED, "cuStreamWaitValue32 failed");
+      const uint64_t off = (uint64_t)row0 * row_bytes, len = (uint64_t)(row1 - row0) * row_bytes;
+      KAAS_CUDA(cudaMemcpyAsync((char *)po->host + off, (const char *)C + off, len,
+                                cudaMemcpyDeviceToHost, po->out_stream));
+      copied = off + len;
+    }
+  }
+  // the rest (or everything, without progressive support) once the kernel is done
+  KAAS_CUDA(cudaEventRecord(ev_done, s));
+  KAAS_CUDA(cudaStreamWaitEvent(po->out_stream, ev_done, 0));
+  if (copied < po->bytes)
+    KAAS_CUDA(cudaMemcpyAsync((char *)po->host + copied, (const char *)C + copied,
+                              po->bytes - copied, cudaMemcpyDeviceToHost, po->out_stream));
+  cudaEventDestroy(ev_ready);
+  cudaEventDestroy(ev_done);
   return 0;
 }
 
@@ -634,15 +715,25 @@ int launch_gemm(cudaStream_t s, int dev, const CUtensorMap &ma, const CUtensorMa
 
 }  // namespace
 
+static int plain_copy_after(cudaStream_t s, const ProgressiveOut *po, const float *C) {
+  cudaEvent_t ev;
+  KAAS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  KAAS_CUDA(cudaEventRecord(ev, s));
+  KAAS_CUDA(cudaStreamWaitEvent(po->out_stream, ev, 0));
+  KAAS_CUDA(cudaMemcpyAsync(po->host, C, po->bytes, cudaMemcpyDeviceToHost, po->out_stream));
+  cudaEventDestroy(ev);
+  return 0;
+}
+
 int launch_cgemm(cudaStream_t s, int dev, int n, int m, int k, uint64_t cov, const float *A,
-                 const float *B, float *C, StreamScratch *sc) {
-  if (n == 0 || m == 0 || cov == 0) return 0;
+                 const float *B, float *C, StreamScratch *sc, const ProgressiveOut *po) {
+  if (n == 0 || m == 0 || cov == 0) return po ? plain_copy_after(s, po, C) : 0;
   if (k == 0) {
     // empty contraction: covered cells are 0 + 0i
     const uint64_t nm = (uint64_t)n * m;
     const uint64_t cells = cov < nm ? cov : nm;
     KAAS_CUDA(cudaMemsetAsync(C, 0, cells * 8, s));
-    return 0;
+    return po ? plain_copy_after(s, po, C) : 0;
   }
   const int k2 = 2 * k;
   const int ldk = (k2 + BK - 1) / BK * BK;
@@ -656,7 +747,7 @@ int launch_cgemm(cudaStream_t s, int dev, int n, int m, int k, uint64_t cov, con
   float *Blo = Bhi + b_elems;
 
   const int sms = device_props(dev).sm_count;
-  k_prep_a<<<sms * 4, 256, 0, s>>>(n, k2, ldk, A, Ahi, Alo);
+  k_prep_a<<<n < sms * 16 ? n : sms * 16, 256, 0, s>>>(n, k2, ldk, A, Ahi, Alo);
   dim3 gb((m + 31) / 32, (k + 31) / 32);
   k_prep_b<<<gb, dim3(32, 8), 0, s>>>(k, m, ldk, reinterpret_cast<const float2 *>(B), Bhi, Blo);
   count_launch(2);  // k_prep_b also zero-fills the K padding columns [2k, ldk)
@@ -689,10 +780,12 @@ int launch_cgemm(cudaStream_t s, int dev, int n, int m, int k, uint64_t cov, con
   shape.cov = cov;
   if (!v1) {
     shape.kb_per_seg = ldk / BK2;
-    return narrow ? launch_gemm2<128>(s, dev, ma, mbm, shape, C)
-                  : launch_gemm2<256>(s, dev, ma, mbm, shape, C);
+    return narrow ? launch_gemm2<128>(s, dev, ma, mbm, shape, C, sc, po)
+                  : launch_gemm2<256>(s, dev, ma, mbm, shape, C, sc, po);
   }
-  return narrow ? launch_gemm<128>(s, dev, ma, mbm, shape, C) : launch_gemm<256>(s, dev, ma, mbm, shape, C);
+  rc = narrow ? launch_gemm<128>(s, dev, ma, mbm, shape, C) : launch_gemm<256>(s, dev, ma, mbm, shape, C);
+  if (rc) return rc;
+  return po ? plain_copy_after(s, po, C) : 0;
 }
 
 }  // namespace kaas

@@ -211,7 +211,7 @@ static int written_args(int kernel, int *w) {
 }
 
 static int run_plan(int dev, cudaStream_t s, const kaas_launch_desc *d, const Plan &p,
-                    StreamScratch *sc) {
+                    StreamScratch *sc, const ProgressiveOut *po = nullptr) {
   uint64_t ptr[KAAS_MAX_ARGS];
   memcpy(ptr, d->ptrs, sizeof ptr);
 
@@ -268,7 +268,8 @@ static int run_plan(int dev, cudaStream_t s, const kaas_launch_desc *d, const Pl
       if (n > 0x7fffffff || p.ext[1] > 0x7fffffff || p.ext[2] > 0x7fffffff)
         return fail(KAAS_E_BOUNDS, "cgemm: extent exceeds i32");
       rc = launch_cgemm(s, dev, (int)n, (int)p.ext[1], (int)p.ext[2], p.cov, (const float *)ptr[0],
-                        (const float *)ptr[1], (float *)ptr[2], sc);
+                        (const float *)ptr[1], (float *)ptr[2], sc,
+                        (po && redirects.empty()) ? po : nullptr);
       break;
     case KAAS_K_JACOBI:
       if (n == 0 || p.cov == 0) {
@@ -284,6 +285,15 @@ static int run_plan(int dev, cudaStream_t s, const kaas_launch_desc *d, const Pl
   for (auto &r : redirects) {
     KAAS_CUDA(cudaMemcpyAsync((void *)r.orig, (void *)r.tmp, r.bytes, cudaMemcpyDeviceToDevice, s));
     KAAS_CUDA(cudaFreeAsync((void *)r.tmp, s));
+  }
+  if (po && !redirects.empty()) {  // aliased output went through a temporary: copy it whole
+    cudaEvent_t ev;
+    KAAS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    KAAS_CUDA(cudaEventRecord(ev, s));
+    KAAS_CUDA(cudaStreamWaitEvent(po->out_stream, ev, 0));
+    KAAS_CUDA(cudaMemcpyAsync(po->host, (const void *)d->ptrs[2], po->bytes, cudaMemcpyDeviceToHost,
+                              po->out_stream));
+    cudaEventDestroy(ev);
   }
   return 0;
 }
@@ -419,6 +429,8 @@ int kaas_stream_create(int dev, int priority, uint64_t *stream) {
   cudaError_t e = cudaMallocAsync((void **)&sc->jac_partials, 2 * kMaxJacobiBlocks * sizeof(float), s);
   if (e == cudaSuccess) e = cudaMallocAsync((void **)&sc->jac_sync, 16 * sizeof(unsigned), s);
   if (e == cudaSuccess) e = cudaMemsetAsync(sc->jac_sync, 0, 16 * sizeof(unsigned), s);
+  // stream memory operations (cuStreamWaitValue32) target plain device memory
+  if (e == cudaSuccess) e = cudaMalloc((void **)&sc->panel_done, kMaxPanels * sizeof(unsigned));
   if (e != cudaSuccess) {
     delete sc;
     cudaStreamDestroy(s);
@@ -449,6 +461,7 @@ int kaas_stream_destroy(uint64_t stream) {
     if (sc->jac_sync) cudaFreeAsync(sc->jac_sync, s);
     if (sc->cg_buf) cudaFreeAsync(sc->cg_buf, s);
     cudaStreamSynchronize(s);
+    if (sc->panel_done) cudaFree(sc->panel_done);
     delete sc;
   }
   KAAS_CUDA(cudaStreamDestroy(s));
@@ -608,7 +621,13 @@ int kaas_launch(int dev, uint64_t stream, const kaas_launch_desc *desc) {
 }
 
 int kaas_launch_batch(int dev, uint64_t stream, const kaas_launch_desc *descs, int n) {
+  return kaas_launch_batch_ex(dev, stream, descs, n, nullptr, 0);
+}
+
+int kaas_launch_batch_ex(int dev, uint64_t stream, const kaas_launch_desc *descs, int n,
+                         const kaas_stream_out *outs, int n_outs) {
   if (n < 0 || (n > 0 && !descs)) return fail(KAAS_E_INVALID, "null launch descriptors");
+  if (n_outs < 0 || (n_outs > 0 && !outs)) return fail(KAAS_E_INVALID, "null stream-out specs");
   cudaStream_t s = (cudaStream_t)stream;
   StreamScratch *sc = scratch_for(s);
   if (!sc) return fail(KAAS_E_INVALID, "stream was not created by kaas_stream_create");
@@ -621,6 +640,25 @@ int kaas_launch_batch(int dev, uint64_t stream, const kaas_launch_desc *descs, i
       set_error("invocation " + std::to_string(i) + ": " + t_last_error);
       return rc;
     }
+  }
+  // stream-out specs: validate, and pick the ones a kernel can stream itself
+  std::vector<int> prog_of(n, -1);     // desc -> out spec streamed progressively
+  std::vector<char> done_out(n_outs, 0);
+  for (int o = 0; o < n_outs; ++o) {
+    const kaas_stream_out &so = outs[o];
+    if (so.desc_index < 0 || so.desc_index >= n || so.arg_index < 0 ||
+        so.arg_index >= descs[so.desc_index].n_args || !so.host_dst ||
+        so.bytes > descs[so.desc_index].sizes[so.arg_index])
+      return fail(KAAS_E_INVALID, "bad stream-out spec");
+    const uint64_t target = descs[so.desc_index].ptrs[so.arg_index];
+    for (int j = so.desc_index + 1; j < n; ++j) {  // must be the last writer of the buffer
+      int w[2];
+      const int nw = written_args(descs[j].kernel, w);
+      for (int q = 0; q < nw; ++q)
+        if (descs[j].ptrs[w[q]] == target)
+          return fail(KAAS_E_INVALID, "stream-out buffer is written again later in the batch");
+    }
+    if (descs[so.desc_index].kernel == KAAS_K_CGEMM && so.arg_index == 2) prog_of[so.desc_index] = o;
   }
   std::vector<const float *> xin, xout, res;
   for (int i = 0; i < n;) {
@@ -644,9 +682,33 @@ int kaas_launch_batch(int dev, uint64_t stream, const kaas_launch_desc *descs, i
       i += run;
       continue;
     }
-    int rc = run_plan(dev, s, &descs[i], plans[i], sc);
+    ProgressiveOut po;
+    const ProgressiveOut *pop = nullptr;
+    if (prog_of[i] >= 0) {
+      const kaas_stream_out &so = outs[prog_of[i]];
+      po = {(cudaStream_t)so.out_stream, so.host_dst, so.bytes};
+      pop = &po;
+      done_out[prog_of[i]] = 1;
+    }
+    int rc = run_plan(dev, s, &descs[i], plans[i], sc, pop);
     if (rc) return rc;
     ++i;
+  }
+  // remaining stream-outs: one copy each after the whole batch
+  if (n_outs) {
+    cudaEvent_t ev = nullptr;
+    for (int o = 0; o < n_outs; ++o) {
+      if (done_out[o]) continue;
+      if (!ev) {
+        KAAS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        KAAS_CUDA(cudaEventRecord(ev, s));
+      }
+      const kaas_stream_out &so = outs[o];
+      KAAS_CUDA(cudaStreamWaitEvent((cudaStream_t)so.out_stream, ev, 0));
+      KAAS_CUDA(cudaMemcpyAsync(so.host_dst, (const void *)descs[so.desc_index].ptrs[so.arg_index],
+                                so.bytes, cudaMemcpyDeviceToHost, (cudaStream_t)so.out_stream));
+    }
+    if (ev) cudaEventDestroy(ev);
   }
   return 0;
 }

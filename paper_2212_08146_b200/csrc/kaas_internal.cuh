@@ -33,6 +33,16 @@ struct StreamScratch {
   // cGEMM operand staging (A_lo, B_exp^T hi, B_exp^T lo), grown on demand
   void *cg_buf = nullptr;
   size_t cg_bytes = 0;
+  // per-row-panel tile completion counters for progressive write-back
+  unsigned *panel_done = nullptr;  // [kMaxPanels], plain cudaMalloc (stream mem-op target)
+};
+constexpr int kMaxPanels = 1024;
+
+// Progressive write-back of one kernel output (see kaas_launch_batch_ex).
+struct ProgressiveOut {
+  cudaStream_t out_stream;
+  void *host;
+  uint64_t bytes;  // bytes of the output buffer to copy
 };
 constexpr int kMaxJacobiBlocks = 4096;
 
@@ -74,6 +84,7 @@ struct JacobiChain {
 };
 int launch_jacobi_chain(cudaStream_t s, int dev, const JacobiChain &c, StreamScratch *sc);
 int launch_cgemm(cudaStream_t s, int dev, int n, int m, int k, uint64_t cov,
-                 const float *A, const float *B, float *C, StreamScratch *sc);
+                 const float *A, const float *B, float *C, StreamScratch *sc,
+                 const ProgressiveOut *po = nullptr);
 
 }  // namespace kaas

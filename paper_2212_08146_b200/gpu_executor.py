@@ -134,7 +134,7 @@ class _Plan:
     request costs a few numpy ops on the host instead of ~4 ms of Python."""
 
     __slots__ = ("error", "kernels", "fail_at", "fail_exc", "advance_ns", "per_inv",
-                 "template", "slots", "names", "dirty_names", "n")
+                 "template", "slots", "names", "dirty_names", "n", "stream_outs")
 
 
 class _LRU(OrderedDict):
@@ -183,6 +183,7 @@ class GpuExecutor:
         self._closed = False
         self._plans_by_id: _LRU = _LRU(256)     # id(req) -> (req, plan)
         self._plans_by_value: _LRU = _LRU(256)  # req -> plan
+        self._streamed: dict = {}                # name -> blob written back by the kernel
 
     # -- device memory ------------------------------------------------------
 
@@ -379,6 +380,21 @@ class GpuExecutor:
                 if not by_name[nm].is_ephemeral and nm not in dirty:
                     dirty.append(nm)
             per_inv.append(InvocationStats(inv.kernel_id, compute_ns, overhead_ns))
+        # outputs a kernel can write back progressively while it still runs:
+        # a cgemm's C that is keyed (flushed at the end) and not rewritten later
+        outs = []
+        if p.fail_at is None:
+            for i, (inv, kernel) in enumerate(zip(req.invocations, kernels)):
+                if kernel.kernel_id != "cgemm":
+                    continue
+                nm = inv.args[2]
+                if by_name[nm].is_ephemeral:
+                    continue
+                later = any(inv2.args[w] == nm for inv2, k2 in
+                            zip(req.invocations[i + 1:], kernels[i + 1:]) for w in k2.writes)
+                if not later and all(o[2] != nm for o in outs):
+                    outs = [o for o in outs if o[2] != nm] + [(i, 2, nm)]
+        p.stream_outs = tuple(outs)
         p.advance_ns = advance
         p.per_inv = tuple(per_inv)
         p.dirty_names = tuple(dirty)
@@ -436,6 +452,7 @@ class GpuExecutor:
         return self._finish(req, stats, t0, status, list(plan.per_inv))
 
     def _launch(self, plan: _Plan, resolved) -> None:
+        self._streamed = {}
         """Replay the plan: clock, dirty marks, one batched enqueue.  On a
         planned BackendFault the clock and dirty marks stop where the
         reference's would and nothing is enqueued (the failed request's
@@ -454,9 +471,17 @@ class GpuExecutor:
             descs["ptrs"] = table[plan.slots]
             self._ev_fill.record(self.s_in)
             self.s_exec.wait(self._ev_fill)
+            outs = []
+            self._streamed = {}
+            for di, ai, nm in plan.stream_outs:
+                buf = resolved[nm]
+                blob = PinnedBlob(buf.size)
+                self._keepalive.append(blob)
+                self._streamed[nm] = blob
+                outs.append((di, ai, self.s_out, blob.addr, buf.size))
             if self.time_requests:
                 self._ev_k0.record(self.s_exec)
-            native.launch_batch(self.device, self.s_exec, descs)
+            native.launch_batch(self.device, self.s_exec, descs, outs)
             if self.time_requests:
                 self._ev_k1.record(self.s_exec)
             self.dev_stats.kernel_launches += plan.n
@@ -471,8 +496,10 @@ class GpuExecutor:
             # only non-const keyed buffers get dirty, and validation forbids
             # binding one non-const key twice, so no buffer appears twice here
             if buf.dirty:
-                blob = PinnedBlob(buf.size)
-                native.d2h_async(blob.addr, buf.ptr, buf.size, self.s_out)
+                blob = self._streamed.get(nm)
+                if blob is None:
+                    blob = PinnedBlob(buf.size)
+                    native.d2h_async(blob.addr, buf.ptr, buf.size, self.s_out)
                 pending.append((buf, blob))
         if self.time_requests:
             self._ev_end.record(self.s_out)

@@ -56,6 +56,11 @@ class LaunchDesc(C.Structure):
     ]
 
 
+class StreamOut(C.Structure):
+    _fields_ = [("desc_index", C.c_int32), ("arg_index", C.c_int32),
+                ("out_stream", C.c_uint64), ("host_dst", C.c_void_p), ("bytes", C.c_uint64)]
+
+
 class DeviceInfo(C.Structure):
     _fields_ = [
         ("ordinal", C.c_int32), ("sm_count", C.c_int32), ("cc_major", C.c_int32),
@@ -120,6 +125,8 @@ EXPORTS = {
     "kaas_memcpy_p2p_async": [_u64, C.c_int, _u64, C.c_int, _u64, _u64],
     "kaas_launch": [C.c_int, _u64, C.POINTER(LaunchDesc)],
     "kaas_launch_batch": [C.c_int, _u64, C.POINTER(LaunchDesc), C.c_int],
+    "kaas_launch_batch_ex": [C.c_int, _u64, C.POINTER(LaunchDesc), C.c_int,
+                             C.POINTER(StreamOut), C.c_int],
 }
 
 _lib = None
@@ -304,8 +311,11 @@ def host_free(addr: int) -> None:
     call("kaas_host_free", C.c_void_p(addr))
 
 
-def launch_batch(dev: int, stream: Stream, descs) -> None:
-    """Enqueue LaunchDescs in order (ctypes array or DESC_DTYPE numpy array)."""
+def launch_batch(dev: int, stream: Stream, descs, outs=None) -> None:
+    """Enqueue LaunchDescs in order (ctypes array or DESC_DTYPE numpy array).
+
+    ``outs``: optional list of (desc_index, arg_index, out_stream, host_addr,
+    nbytes) progressive write-backs (kaas_launch_batch_ex)."""
     n = len(descs)
     if n == 0:
         return
@@ -313,8 +323,15 @@ def launch_batch(dev: int, stream: Stream, descs) -> None:
         ptr = descs.ctypes.data_as(C.POINTER(LaunchDesc))
     else:
         ptr = descs
-    rc = load().kaas_launch_batch(dev, stream.handle, ptr, n)
-    check(rc, "kaas_launch_batch")
+    if not outs:
+        check(load().kaas_launch_batch(dev, stream.handle, ptr, n), "kaas_launch_batch")
+        return
+    arr = (StreamOut * len(outs))()
+    for i, (di, ai, st, addr, nb) in enumerate(outs):
+        arr[i].desc_index, arr[i].arg_index = di, ai
+        arr[i].out_stream, arr[i].host_dst, arr[i].bytes = st.handle, addr, nb
+    check(load().kaas_launch_batch_ex(dev, stream.handle, ptr, n, arr, len(outs)),
+          "kaas_launch_batch_ex")
 
 
 def is_available() -> bool:

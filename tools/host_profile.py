@@ -11,16 +11,16 @@ from paper_2212_08146_b200.hoststore import PinnedStore  # noqa: E402
 from paper_2212_08146_b200.pool import KaasService  # noqa: E402
 
 
-def main(kind="jacobi", n_req=30):
+def main(kind="jacobi", n_req=30, n=1024):
     store = PinnedStore()
     if kind == "jacobi":
         W.seed_jacobi(store, 4096, prefix="j")
         mk = lambda i: W.jacobi_request(f"j/{i}", 4096, 500, "j/A/4096", "j/b/4096", "j/x0/4096",  # noqa: E731
                                         "j/x", "j/r")
     else:
-        W.seed_cgemm(store, 1024, prefix="c")
-        mk = lambda i: W.cgemm_request(f"c/{i}", 1024, "c/A/1024", "c/B/1024", "c/C")  # noqa: E731
-    svc = KaasService(store, n_executors=1, capacity=1 << 30, policy="rr", devices=[0])
+        W.seed_cgemm(store, n, prefix="c")
+        mk = lambda i: W.cgemm_request(f"c/{i}", n, f"c/A/{n}", f"c/B/{n}", "c/C")  # noqa: E731
+    svc = KaasService(store, n_executors=1, capacity=4 << 30, policy="rr", devices=[0])
     ex = svc.executors[0]
     for i in range(3):
         svc.submit(mk(i))
@@ -41,4 +41,5 @@ def main(kind="jacobi", n_req=30):
 
 
 if __name__ == "__main__":
-    main(*(sys.argv[1:2] or ["jacobi"]))
+    a = sys.argv[1:]
+    main(a[0] if a else "jacobi", int(a[1]) if len(a) > 1 else 30, int(a[2]) if len(a) > 2 else 1024)
