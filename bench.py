@@ -220,6 +220,67 @@ def measure_cgemm(n, steps, device, cold_too):
     return out
 
 
+def measure_mixed(device, clients=16, count=160, policy="affinity:8", capacity=512 << 20):
+    """BASELINE configs[3]: multi-tenant mixed cGEMM (2048^3) + Jacobi (N=4096,
+    100 sweeps), Zipf(1.0) over 8+8 const objects, 16 client threads, LRU
+    pressure (768 MiB universe vs 512 MiB ledger), on this rank's GPU."""
+    from paper_2212_08146_b200 import workloads as W
+    from paper_2212_08146_b200.benchlib import run_stream
+    from paper_2212_08146_b200.hoststore import PinnedStore
+    from paper_2212_08146_b200.pool import KaasService
+    store = PinnedStore()
+    uni = W.mixed_universe(store)
+    reqs = W.mixed_requests(uni, count)
+    with KaasService(store, n_executors=1, capacity=capacity, policy=policy,
+                     devices=[device]) as svc:
+        run_stream(svc, reqs[:8], 1)  # warm the pinned pools / plans
+        ex = svc.executors[0]
+        h2d0, h2dms0, dev0 = ex.dev_stats.h2d_bytes, ex.dev_stats.h2d_ms, ex.dev_stats.device_ms
+        t0 = time.perf_counter()
+        resps, lat = run_stream(svc, reqs, clients)
+        wall = time.perf_counter() - t0
+        hits = sum(r.io_stats.cache_hits for r in resps)
+        misses = sum(r.io_stats.cache_misses for r in resps)
+        h2d = ex.dev_stats.h2d_bytes - h2d0
+        h2d_ms = ex.dev_stats.h2d_ms - h2dms0
+        evictions = ex.cache.evictions
+    return {"workload": "mixed cgemm 2048^3 + jacobi N=4096x100 sweeps, zipf(1.0) over 8+8 const "
+                        f"objects, {clients} clients, {policy}, ledger {capacity >> 20} MiB/GPU",
+            "requests": len(reqs), "errors": sum(0 if r.status.ok else 1 for r in resps),
+            "req_per_s": len(reqs) / wall, "p50_ms": percentile(lat, 0.5) * 1e3,
+            "p99_ms": percentile(lat, 0.99) * 1e3, "hit_rate": hits / max(1, hits + misses),
+            "h2d_bytes": h2d, "h2d_gbs": h2d / (h2d_ms * 1e6) if h2d_ms else None,
+            "evictions": evictions, "device_busy_frac": (ex.dev_stats.device_ms - dev0) / (wall * 1e3)}
+
+
+def measure_resnet(device, steps=5):
+    """BASELINE configs[4]: ResNet-50-shaped chain (53 bit-exact conv-as-GEMM
+    matmuls + residual adds, batch 1), const weights, ephemeral activations."""
+    from paper_2212_08146_b200 import workloads as W
+    from paper_2212_08146_b200.hoststore import PinnedStore
+    from paper_2212_08146_b200.pool import KaasService
+    store = PinnedStore()
+    W.seed_resnet(store)
+    macs = sum(m * n * k for _, m, n, k in W.resnet50_gemms())
+    with KaasService(store, n_executors=1, capacity=1 << 30, policy="rr", devices=[device]) as svc:
+        def req(i):
+            return W.resnet_chain_request(f"rn/{i}")
+        r = svc.submit(req(0))
+        assert r.status.ok, r.status
+        svc.submit(req(1))
+        lat, dev, kern = run_requests(svc, req, steps, 10)
+    kms = statistics.median(kern)
+    return {"workload": "ResNet-50-shaped chain, batch 1: 53 bit-exact matmuls + 16 residual adds "
+                        "(102 invocations), const weights (97 MiB), ephemeral activations",
+            "req_per_s": len(lat) / sum(lat), "p50_ms": percentile(lat, 0.5) * 1e3,
+            "device_ms": statistics.median(dev), "kernel_ms": kms,
+            "tmacs": macs / (kms * 1e-3) / 1e12,
+            "roofline": {"bound": "fp32-simt", "unit": "TMAC/s", "achieved": macs / (kms * 1e-3) / 1e12,
+                         "peak": 148 * 128 * 1.965e9 / 2 / 1e12,
+                         "peak_note": "non-fused FMUL+FADD per MAC (bit-exact), 148 SMs x 128 lanes @ max clock",
+                         "frac": (macs / (kms * 1e-3) / 1e12) / (148 * 128 * 1.965e9 / 2 / 1e12)}}
+
+
 def ours(args, rank, world, local_rank, dist):
     from paper_2212_08146_b200 import native
     from paper_2212_08146_b200.hoststore import PinnedStore
@@ -270,6 +331,8 @@ def ours(args, rank, world, local_rank, dist):
         if not args.no_extras:
             extras["cgemm1024"] = measure_cgemm(1024, 20, local_rank, False)
             extras["cgemm8192"] = measure_cgemm(8192, 5, local_rank, True)
+            extras["mixed"] = measure_mixed(local_rank)
+            extras["resnet50_chain"] = measure_resnet(local_rank)
             for key in ("cgemm1024", "cgemm8192"):
                 e = extras[key]
                 e["roofline"] = {

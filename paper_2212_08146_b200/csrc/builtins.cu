@@ -112,73 +112,93 @@ __global__ void k_reduce_sum(uint64_t n, const float *x, float *out) {
 }
 
 // ---- matmul: per cell acc = 0; acc = fl(acc + fl(a*b)), k ascending --------
-// (backend.py:174-189, oracle pkg/tests/oracles.py:25-33).  SIMT tiles of
-// 64x64 cells, 256 threads x (4x4) cells, k staged through smem 16 at a time.
+// (backend.py:174-189, oracle pkg/tests/oracles.py:25-33).  Bit-exactness
+// forbids split-K, so all parallelism comes from output cells: 256 threads
+// (16 x 16) each own TM x TN cells of a (16*TM) x (16*TN) tile, k staged
+// through smem BK at a time.  The tile shape is picked per launch so small-M
+// / long-K layers (ResNet stage 4: M = 49, K = 4608) still fill the SMs,
+// while big layers get 4x4 register blocking (0.5 smem loads per MAC).
 // Padding products are never added (0*Inf would be NaN and +0 would flip
 // the sign of a -0.0 accumulator), so the k loop uses the true extent.
-constexpr int MM_BM = 64, MM_BN = 64, MM_BK = 16;
+constexpr int MM_BK = 16;
 
+template <int TM, int TN>
 __global__ void __launch_bounds__(256)
 k_matmul(int n, int m, int k, uint64_t cov, const float *__restrict__ a,
          const float *__restrict__ b, float *__restrict__ out) {
-  __shared__ float As[MM_BK][MM_BM];
-  __shared__ float Bs[MM_BK][MM_BN];
+  constexpr int BM = 16 * TM, BN = 16 * TN;
+  constexpr int LA = BM * MM_BK / 256, LB = MM_BK * BN / 256;  // elements per thread
+  __shared__ float As[2][MM_BK][BM];
+  __shared__ float Bs[2][MM_BK][BN];
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  const int bm = blockIdx.y * MM_BM, bn = blockIdx.x * MM_BN;
-  float acc[4][4];
+  const int bm = blockIdx.y * BM, bn = blockIdx.x * BN;
+  float acc[TM][TN];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < TM; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
+    for (int j = 0; j < TN; ++j) acc[i][j] = 0.0f;
 
-  for (int k0 = 0; k0 < k; k0 += MM_BK) {
+  // register staging: the next k-chunk's global loads are in flight while
+  // the current chunk computes out of the other smem buffer
+  float ra[LA], rb[LB];
+  auto load = [&](int k0) {
     const int kc = min(MM_BK, k - k0);
-    // A tile: 64 rows x 16 k; thread t loads (row = t/4 + 64*0.., kk = t%4*4..)
-    for (int e = threadIdx.x; e < MM_BM * MM_BK; e += 256) {
+#pragma unroll
+    for (int u = 0; u < LA; ++u) {
+      const int e = threadIdx.x + 256 * u;
       const int r = e / MM_BK, kk = e % MM_BK;
-      const int gr = bm + r, gk = k0 + kk;
-      As[kk][r] = (gr < n && kk < kc) ? a[(size_t)gr * k + gk] : 0.0f;
+      ra[u] = (bm + r < n && kk < kc) ? __ldg(a + (size_t)(bm + r) * k + k0 + kk) : 0.0f;
     }
-    for (int e = threadIdx.x; e < MM_BK * MM_BN; e += 256) {
-      const int kk = e / MM_BN, c = e % MM_BN;
-      const int gc = bn + c, gk = k0 + kk;
-      Bs[kk][c] = (gc < m && kk < kc) ? b[(size_t)gk * m + gc] : 0.0f;
+#pragma unroll
+    for (int u = 0; u < LB; ++u) {
+      const int e = threadIdx.x + 256 * u;
+      const int kk = e / BN, c = e % BN;
+      rb[u] = (bn + c < m && kk < kc) ? __ldg(b + (size_t)(k0 + kk) * m + bn + c) : 0.0f;
     }
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int u = 0; u < LA; ++u) {
+      const int e = threadIdx.x + 256 * u;
+      As[buf][e % MM_BK][e / MM_BK] = ra[u];
+    }
+#pragma unroll
+    for (int u = 0; u < LB; ++u) {
+      const int e = threadIdx.x + 256 * u;
+      Bs[buf][e / BN][e % BN] = rb[u];
+    }
+  };
+  if (k > 0) load(0);
+  int buf = 0;
+  for (int k0 = 0; k0 < k; k0 += MM_BK, buf ^= 1) {
+    const int kc = min(MM_BK, k - k0);
+    stash(buf);
     __syncthreads();
+    if (k0 + MM_BK < k) load(k0 + MM_BK);
+    auto step = [&](int kk) {
+      float av[TM], bv[TN];
+#pragma unroll
+      for (int i = 0; i < TM; ++i) av[i] = As[buf][kk][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < TN; ++j) bv[j] = Bs[buf][kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(av[i], bv[j]));
+    };
     if (kc == MM_BK) {
 #pragma unroll
-      for (int kk = 0; kk < MM_BK; ++kk) {
-        float av[4], bv[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) av[i] = As[kk][ty + 16 * i];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) bv[j] = Bs[kk][tx + 16 * j];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(av[i], bv[j]));
-      }
+      for (int kk = 0; kk < MM_BK; ++kk) step(kk);
     } else {
-      for (int kk = 0; kk < kc; ++kk) {
-        float av[4], bv[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) av[i] = As[kk][ty + 16 * i];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) bv[j] = Bs[kk][tx + 16 * j];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(av[i], bv[j]));
-      }
+      for (int kk = 0; kk < kc; ++kk) step(kk);
     }
-    __syncthreads();
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < TM; ++i) {
     const int r = bm + ty + 16 * i;
     if (r >= n) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < TN; ++j) {
       const int c = bn + tx + 16 * j;
       if (c >= m) continue;
       const uint64_t g = (uint64_t)r * m + c;
@@ -213,14 +233,36 @@ int launch_reduce_sum(cudaStream_t s, int dev, uint64_t n, const float *x, float
 
 int launch_matmul(cudaStream_t s, int dev, uint64_t n, uint64_t m, uint64_t k, uint64_t cov,
                   const float *a, const float *b, float *out) {
-  (void)dev;
   if (n == 0 || m == 0 || cov == 0) return 0;
   if (n > 0x7fffffffu || m > 0x7fffffffu || k > 0x7fffffffu)
     return fail(KAAS_E_INVALID, "matmul extent exceeds i32");
-  const uint64_t gy = (n + MM_BM - 1) / MM_BM, gx = (m + MM_BN - 1) / MM_BN;
+  // largest register tile that still gives >= 2 CTAs per SM
+  const uint64_t want = 2ull * device_props(dev).sm_count;
+  auto ctas = [&](int tm, int tn) {
+    return ((n + 16 * tm - 1) / (16 * tm)) * ((m + 16 * tn - 1) / (16 * tn));
+  };
+  int tm = 1, tn = 1;
+  const int cand[][2] = {{4, 4}, {2, 4}, {4, 2}, {2, 2}, {1, 2}, {2, 1}};
+  for (auto &c : cand) {
+    if (ctas(c[0], c[1]) >= want) {
+      tm = c[0];
+      tn = c[1];
+      break;
+    }
+  }
+  const uint64_t gy = (n + 16 * tm - 1) / (16 * tm), gx = (m + 16 * tn - 1) / (16 * tn);
   if (gy > 65535) return fail(KAAS_E_INVALID, "matmul: n too large for grid.y");
   dim3 grid((unsigned)gx, (unsigned)gy);
-  k_matmul<<<grid, 256, 0, s>>>((int)n, (int)m, (int)k, cov, a, b, out);
+#define MM_LAUNCH(TM, TN) \
+  k_matmul<TM, TN><<<grid, 256, 0, s>>>((int)n, (int)m, (int)k, cov, a, b, out)
+  if (tm == 4 && tn == 4) MM_LAUNCH(4, 4);
+  else if (tm == 2 && tn == 4) MM_LAUNCH(2, 4);
+  else if (tm == 4 && tn == 2) MM_LAUNCH(4, 2);
+  else if (tm == 2 && tn == 2) MM_LAUNCH(2, 2);
+  else if (tm == 1 && tn == 2) MM_LAUNCH(1, 2);
+  else if (tm == 2 && tn == 1) MM_LAUNCH(2, 1);
+  else MM_LAUNCH(1, 1);
+#undef MM_LAUNCH
   count_launch();
   KAAS_CUDA(cudaGetLastError());
   return 0;

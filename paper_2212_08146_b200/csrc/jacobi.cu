@@ -256,6 +256,7 @@ __device__ __forceinline__ void grid_sync_mono(unsigned *counter, unsigned epoch
     const unsigned target = (epoch + 1) * gridDim.x;
     while (ld_acquire(counter) < target) {
     }
+    __threadfence();  // gpu-scope fence: later plain (L1-cached) loads see other CTAs' x
   }
   __syncthreads();
 }
@@ -693,7 +694,7 @@ constexpr int kRowsMaxWarps = 28;  // 896 threads -> 72 registers per thread
 constexpr int kRowsUnroll = 8;
 constexpr int kRowsPre = 4;  // loads hoisted above the x staging
 
-template <bool kChain, bool kPrefetch>
+template <bool kChain, bool kPrefetch, bool kXDirect = false>
 __global__ void __launch_bounds__(kRowsMaxWarps * 32, 1)
 k_jacobi_rows(const __grid_constant__ ChainParams p, float *partials, unsigned *sync) {
   extern __shared__ __align__(16) float xs[];  // n floats
@@ -719,10 +720,15 @@ k_jacobi_rows(const __grid_constant__ ChainParams p, float *partials, unsigned *
       for (int u = 0; u < kRowsPre; ++u)
         pre[kPrefetch ? u : 0] = ld_a(p.A + (size_t)first * n + 4 * (lane + 32 * u), pol);
     }
-    for (int e = threadIdx.x; e < n4; e += blockDim.x)
-      reinterpret_cast<float4 *>(xs)[e] = kChain ? __ldcg(reinterpret_cast<const float4 *>(x_in) + e)
-                                                 : __ldg(reinterpret_cast<const float4 *>(x_in) + e);
-    __syncthreads();
+    if (!kXDirect) {
+      for (int e = threadIdx.x; e < n4; e += blockDim.x)
+        reinterpret_cast<float4 *>(xs)[e] = kChain ? __ldcg(reinterpret_cast<const float4 *>(x_in) + e)
+                                                   : __ldg(reinterpret_cast<const float4 *>(x_in) + e);
+      __syncthreads();
+    }
+    // kXDirect: x is read through L1 inside the row loop (the grid barrier's
+    // acquire invalidated L1, so the first warp per SM pulls each line from L2)
+    const float4 *xg = reinterpret_cast<const float4 *>(x_in);
     float res = 0.f;
     for (int i = first; i < r1; i += nwarps) {
       const float *row = p.A + (size_t)i * n;
@@ -731,7 +737,7 @@ k_jacobi_rows(const __grid_constant__ ChainParams p, float *partials, unsigned *
       auto group = [&](const float4 *av, int cnt, int j4, int it) {
 #pragma unroll
         for (int u = 0; u < cnt; ++u) {
-          float4 xv = x4[j4 + 32 * u];
+          float4 xv = kXDirect ? xg[j4 + 32 * u] : x4[j4 + 32 * u];
           if (it + u == it_d) {
             const int d = i - 4 * (j4 + 32 * u);
             xv.x = d == 0 ? 0.f : xv.x;
@@ -760,7 +766,7 @@ k_jacobi_rows(const __grid_constant__ ChainParams p, float *partials, unsigned *
       }
       for (; j4 < n4; j4 += 32, ++it) {
         const float4 a = ld_a(row + 4 * j4, pol);
-        float4 xv = x4[j4];
+        float4 xv = kXDirect ? xg[j4] : x4[j4];
         if (it == it_d) {
           const int d = i - 4 * j4;
           xv.x = d == 0 ? 0.f : xv.x;
@@ -779,7 +785,7 @@ k_jacobi_rows(const __grid_constant__ ChainParams p, float *partials, unsigned *
       if (lane == 0) {
         const float xn = (p.b[i] - v) / __ldg(row + i);  // IEEE div.rn
         x_out[i] = xn;
-        res += fabsf(xn - xs[i]);
+        res += fabsf(xn - (kXDirect ? x_in[i] : xs[i]));
       }
     }
     if (want_resid && lane == 0) wres[warp] = res;
@@ -937,9 +943,9 @@ int launch_jacobi(cudaStream_t s, int dev, int n, uint64_t cov, const float *A, 
     unsigned *sync = sc->jac_sync;
     void *args[] = {(void *)&p, (void *)&partials, (void *)&sync};
     const size_t smem = (size_t)n * 4;
-    KAAS_CUDA(cudaFuncSetAttribute((const void *)k_jacobi_rows<false, false>,
+    KAAS_CUDA(cudaFuncSetAttribute((const void *)k_jacobi_rows<false, false, true>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    KAAS_CUDA(cudaLaunchKernel((const void *)k_jacobi_rows<false, false>, dim3(blocks),
+    KAAS_CUDA(cudaLaunchKernel((const void *)k_jacobi_rows<false, false, true>, dim3(blocks),
                                dim3(rows_threads(dev, cov)), args, smem, s));
     count_launch();
     return 0;
@@ -1020,8 +1026,11 @@ int launch_jacobi_chain(cudaStream_t s, int dev, const JacobiChain &c, StreamScr
   bool use_rows = use_rows_kernel(c.n) && aligned16(c.A);
   for (int t = 0; t < c.sweeps && use_rows; ++t)
     if (!aligned16(c.x_in[t])) use_rows = false;
-  const void *rfn = rows_prefetch() ? (const void *)k_jacobi_rows<true, true>
-                                    : (const void *)k_jacobi_rows<true, false>;
+  const char *xd = getenv("KAAS_JACOBI_XDIRECT");  // dev A/B (default on)
+  const bool xdirect = !(xd && xd[0] == '0');
+  const void *rfn = xdirect ? (const void *)k_jacobi_rows<true, false, true>
+                    : rows_prefetch() ? (const void *)k_jacobi_rows<true, true>
+                                      : (const void *)k_jacobi_rows<true, false>;
   if (use_rows)
     KAAS_CUDA(cudaFuncSetAttribute(rfn, cudaFuncAttributeMaxDynamicSharedMemorySize, c.n * 4));
   const int kcl = use_rows ? 0 : ldg_kc(c.n);

@@ -107,7 +107,7 @@ class DeviceStats:
     """Measured (not virtual) device activity of one executor."""
 
     __slots__ = ("requests", "device_ms", "last_device_ms", "kernel_ms", "last_kernel_ms",
-                 "h2d_bytes", "d2h_bytes", "p2p_bytes", "kernel_launches")
+                 "h2d_bytes", "h2d_ms", "d2h_bytes", "p2p_bytes", "kernel_launches")
 
     def __init__(self):
         self.requests = 0
@@ -116,6 +116,7 @@ class DeviceStats:
         self.kernel_ms = 0.0       # time inside the batched invocation list
         self.last_kernel_ms = 0.0
         self.h2d_bytes = 0
+        self.h2d_ms = 0.0          # time the H2D fill stream was busy (first fill -> last fill done)
         self.d2h_bytes = 0
         self.p2p_bytes = 0
         self.kernel_launches = 0
@@ -149,8 +150,29 @@ class _LRU(OrderedDict):
             self.popitem(last=False)
 
 
+class _Req:
+    """One request between ``begin`` (decisions made, device work enqueued)
+    and ``complete`` (device done, store puts, response)."""
+
+    __slots__ = ("seq", "req", "response", "pending", "graveyard", "keepalive", "events",
+                 "has_kernels", "has_fills", "streamed")
+
+    def __init__(self, seq, req):
+        self.seq = seq
+        self.req = req
+        self.response = None
+        self.pending = []      # (key, blob, size) store puts, table order
+        self.graveyard = []    # device pointers to free once this request's work is done
+        self.keepalive = []    # host blobs referenced by this request's copies
+        self.events = None     # (start, end, k0, k1, in0, in1)
+        self.has_kernels = False
+        self.has_fills = False
+        self.streamed = {}
+
+
 class GpuExecutor:
-    """Owns one device cache on one GPU and runs requests one at a time."""
+    """Owns one device cache on one GPU; requests are decided strictly in
+    arrival order and may overlap on the device (``begin`` / ``complete``)."""
 
     def __init__(self, config: ExecutorConfig, store, backend: GpuBackend | None = None,
                  time_requests: bool = True):
@@ -165,10 +187,7 @@ class GpuExecutor:
         self.s_out = native.Stream(self.device)
         self._ev_fill = native.Event(self.device)
         self._ev_exec = native.Event(self.device)
-        self._ev_start = native.Event(self.device, timing=True)
-        self._ev_end = native.Event(self.device, timing=True)
-        self._ev_k0 = native.Event(self.device, timing=True)
-        self._ev_k1 = native.Event(self.device, timing=True)
+        self._ev_pool: list = []
         self.time_requests = time_requests
         self.cache = CacheState(config.capacity, debug=config.debug, on_drop=self._drop)
         self.clock = VirtualClock()
@@ -178,12 +197,13 @@ class GpuExecutor:
         self.dev_stats = DeviceStats()
         self._pinned_store = isinstance(store, PinnedStore)
         self._req_seq = 0
-        self._graveyard: list[int] = []   # device ptrs to free once streams drain
-        self._keepalive: list = []        # host blobs referenced by in-flight copies
+        self._cur: _Req | None = None             # request being begun
+        self._inflight: OrderedDict[int, _Req] = OrderedDict()  # seq -> begun, not completed
+        self._pending_puts: dict[str, int] = {}   # key -> seq of the request that will put it
+        self.on_complete = None                   # callback(req_record, response) (pool)
         self._closed = False
         self._plans_by_id: _LRU = _LRU(256)     # id(req) -> (req, plan)
-        self._plans_by_value: _LRU = _LRU(256)  # req -> plan
-        self._streamed: dict = {}                # name -> blob written back by the kernel
+        self._plans_by_value: _LRU = _LRU(256)  # (buffers, invocations) -> plan
 
     # -- device memory ------------------------------------------------------
 
@@ -200,24 +220,30 @@ class GpuExecutor:
         native.memset_async(buf.ptr, 0, buf.size, self.s_exec)
 
     def _drop(self, buf: DeviceBuffer) -> None:
-        """on_drop hook: an entry left the table or an ephemeral was freed."""
+        """on_drop hook: an entry left the table or an ephemeral was freed.
+        The allocation is released once the last request that used it is done."""
         if not buf.ptr:
             return
         ptr, buf.ptr = buf.ptr, 0
-        if buf._req == self._req_seq:
-            self._graveyard.append(ptr)  # may still be touched by this request
+        owner = self._inflight.get(buf._req)
+        if owner is None and self._cur is not None and buf._req == self._cur.seq:
+            owner = self._cur
+        if owner is not None:
+            owner.graveyard.append(ptr)
         else:
             native.free_async(self.s_in, ptr)
 
-    def _drain(self) -> None:
-        """Wait for every stream, then free deferred allocations."""
-        self.s_in.sync()
-        self.s_exec.sync()
-        self.s_out.sync()
-        for ptr in self._graveyard:
-            native.free_async(self.s_exec, ptr)
-        self._graveyard.clear()
-        self._keepalive.clear()
+    def _events(self):
+        if self._ev_pool:
+            return self._ev_pool.pop()
+        return tuple(native.Event(self.device, timing=True) for _ in range(6))
+
+    def _wait_for_user(self, buf: DeviceBuffer) -> None:
+        """A fill is about to overwrite ``buf`` in place: order it after every
+        in-flight request that may still read or copy it."""
+        owner = self._inflight.get(buf._req)
+        if owner is not None and owner is not self._cur:
+            self.s_in.wait(owner.events[1])
 
     # -- buffer resolution (executor.py:233-316) ------------------------------
 
@@ -288,25 +314,32 @@ class GpuExecutor:
         return buf
 
     def _fetch_into(self, buf: DeviceBuffer, arg: BufferArg, stats: _ReqStats) -> None:
+        owner = self._pending_puts.get(arg.key)
+        if owner is not None:  # read-your-writes: that put must land first
+            self.complete(through=owner)
         payload = self.store.get(arg.key)  # NotFound propagates
         if len(payload) != arg.size:
             raise SizeMismatchError(
                 f"buffer {arg.name!r}: store object {arg.key!r} is"
                 f" {len(payload)} bytes, request declares {arg.size}")
+        cur = self._cur
+        if buf.ptr:
+            self._wait_for_user(buf)
         self._mark(buf)
         if not buf.ptr:
             self._alloc(buf, self.s_in)
         src = payload if isinstance(payload, PinnedBlob) else PinnedBlob.from_bytes(payload)
+        if self.time_requests and not cur.has_fills:
+            cur.events[4].record(self.s_in)
+        cur.has_fills = True
         native.h2d_async(buf.ptr, src.addr, arg.size, self.s_in)
-        self._keepalive.append(src)
+        cur.keepalive.append(src)
         self.dev_stats.h2d_bytes += arg.size
         buf.dirty = False
         self.clock.advance_ns(self.backend.timing.fetch_time_ns(arg.size))
         stats.store_gets += 1
         stats.bytes_fetched += arg.size
         stats.cache_misses += 1
-
-    # -- request lifecycle (executor.py:320-425) ------------------------------
 
     # -- request planning -----------------------------------------------------
 
@@ -408,6 +441,21 @@ class GpuExecutor:
     # -- request lifecycle (executor.py:320-425) ------------------------------
 
     def execute(self, req: KaasRequest) -> KaasResponse:
+        """Run one request to completion (the reference's synchronous call)."""
+        rec = self.begin(req)
+        if isinstance(rec, KaasResponse):
+            return rec
+        self.complete(through=rec.seq)
+        return rec.response
+
+    def begin(self, req: KaasRequest):
+        """Make every decision for ``req`` and enqueue its device work.
+
+        Returns the finished ``KaasResponse`` when the request fails on the
+        host (nothing enqueued), else an in-flight record whose response is
+        produced by ``complete``.  Decisions, ledger, ticks, virtual time and
+        statistics are final here -- exactly as if the reference had run the
+        request -- so requests begun later see the same cache state."""
         t0 = self.clock.now_ns
         stats = _ReqStats()
         plan = self._plan(req)
@@ -415,10 +463,14 @@ class GpuExecutor:
             return self._finish(req, stats, t0, plan.error)
 
         self._req_seq += 1
+        rec = _Req(self._req_seq, req)
+        rec.events = self._events()
+        self._cur = rec
+        ev = rec.events
         if self.time_requests:
-            self._ev_start.record(self.s_in)
-            self.s_exec.wait(self._ev_start)
-            self.s_out.wait(self._ev_start)
+            ev[0].record(self.s_in)
+            self.s_exec.wait(ev[0])
+            self.s_out.wait(ev[0])
         resolved: dict[str, DeviceBuffer] = {}
         ephemerals: list[DeviceBuffer] = []
         try:
@@ -429,30 +481,75 @@ class GpuExecutor:
                 resolved[nm] = buf
                 if arg.is_ephemeral:
                     ephemerals.append(buf)
-            self._launch(plan, resolved)
-            self._flush(plan.names, resolved, stats)
-            status = Status.make_ok()
+            self._launch(rec, plan, resolved)
+            self._enqueue_flush(rec, plan.names, resolved, stats)
         except KaasError as exc:
-            self._drain_quietly()
+            # a host-detected failure enqueued no kernels; drain so the
+            # request's fills/zero-fills finish before its buffers are freed
+            self._cur = None
+            self.complete()
+            self._drain_streams_quietly()
             self._release(resolved, ephemerals, drop_dirty=True)
-            self._drain_quietly()
+            for ptr in rec.graveyard:
+                native.free_async(self.s_exec, ptr)
+            self._ev_pool.append(rec.events)
             return self._finish(req, stats, t0, Status.make_error(exc.kind, exc.message))
-
         self._release(resolved, ephemerals, drop_dirty=False)
-        self._drain()
-        if self.time_requests:
-            ms = self._ev_start.elapsed_ms(self._ev_end)
-            self.dev_stats.last_device_ms = ms
-            self.dev_stats.device_ms += ms
-            if plan.n:
-                kms = self._ev_k0.elapsed_ms(self._ev_k1)
-                self.dev_stats.last_kernel_ms = kms
-                self.dev_stats.kernel_ms += kms
-        self.dev_stats.requests += 1
-        return self._finish(req, stats, t0, status, list(plan.per_inv))
+        for key, _, _ in rec.pending:
+            self._pending_puts[key] = rec.seq
+        rec.response = self._finish(req, stats, t0, Status.make_ok(), list(plan.per_inv))
+        self._inflight[rec.seq] = rec
+        self._cur = None
+        return rec
 
-    def _launch(self, plan: _Plan, resolved) -> None:
-        self._streamed = {}
+    def complete(self, through: int | None = None, block: bool = True) -> int:
+        """Finish in-flight requests in order: wait for the device, put the
+        flushed objects, release deferred frees.  ``through`` = last seq to
+        finish (all when None).  With ``block=False`` only requests whose
+        device work is already done are finished.  Returns how many."""
+        done = 0
+        while self._inflight:
+            seq, rec = next(iter(self._inflight.items()))
+            if through is not None and seq > through:
+                break
+            ev = rec.events
+            if not block and not ev[1].done():
+                break
+            ev[1].sync()
+            for key, blob, size in rec.pending:
+                if self._pinned_store:
+                    self.store.put_owned(key, blob)
+                else:
+                    self.store.put(key, bytes(blob))
+                if self._pending_puts.get(key) == seq:
+                    del self._pending_puts[key]
+                self.dev_stats.d2h_bytes += size
+            for ptr in rec.graveyard:
+                native.free_async(self.s_exec, ptr)
+            if self.time_requests:
+                ms = ev[0].elapsed_ms(ev[1])
+                self.dev_stats.last_device_ms = ms
+                self.dev_stats.device_ms += ms
+                if rec.has_kernels:
+                    kms = ev[2].elapsed_ms(ev[3])
+                    self.dev_stats.last_kernel_ms = kms
+                    self.dev_stats.kernel_ms += kms
+                if rec.has_fills:
+                    self.dev_stats.h2d_ms += ev[4].elapsed_ms(ev[5])
+            self.dev_stats.requests += 1
+            del self._inflight[seq]
+            self._ev_pool.append(ev)
+            rec.keepalive.clear()
+            done += 1
+            if self.on_complete is not None:
+                self.on_complete(rec, rec.response)
+        return done
+
+    @property
+    def inflight(self) -> int:
+        return len(self._inflight)
+
+    def _launch(self, rec: _Req, plan: _Plan, resolved) -> None:
         """Replay the plan: clock, dirty marks, one batched enqueue.  On a
         planned BackendFault the clock and dirty marks stop where the
         reference's would and nothing is enqueued (the failed request's
@@ -463,6 +560,9 @@ class GpuExecutor:
             resolved[nm].dirty = True
         if plan.fail_at is not None:
             raise plan.fail_exc
+        ev = rec.events
+        if self.time_requests and rec.has_fills:
+            ev[5].record(self.s_in)
         if plan.n:
             table = np.fromiter((resolved[nm].ptr for nm in plan.names), dtype=np.uint64,
                                 count=len(plan.names))
@@ -472,59 +572,51 @@ class GpuExecutor:
             self._ev_fill.record(self.s_in)
             self.s_exec.wait(self._ev_fill)
             outs = []
-            self._streamed = {}
             for di, ai, nm in plan.stream_outs:
                 buf = resolved[nm]
                 blob = PinnedBlob(buf.size)
-                self._keepalive.append(blob)
-                self._streamed[nm] = blob
+                rec.keepalive.append(blob)
+                rec.streamed[nm] = blob
                 outs.append((di, ai, self.s_out, blob.addr, buf.size))
             if self.time_requests:
-                self._ev_k0.record(self.s_exec)
+                ev[2].record(self.s_exec)
             native.launch_batch(self.device, self.s_exec, descs, outs)
             if self.time_requests:
-                self._ev_k1.record(self.s_exec)
+                ev[3].record(self.s_exec)
+            rec.has_kernels = True
             self.dev_stats.kernel_launches += plan.n
 
-    def _flush(self, names, resolved, stats: _ReqStats) -> None:
-        """Write back dirty keyed buffers, table order (executor.py:371-380)."""
+    def _enqueue_flush(self, rec: _Req, names, resolved, stats: _ReqStats) -> None:
+        """Write-back of dirty keyed buffers in table order
+        (executor.py:371-380): the D2H copies are enqueued now, the puts
+        happen in ``complete``; virtual time, IoStats and the clean marks are
+        final now, as the next request's decisions depend on them."""
         self._ev_exec.record(self.s_exec)
         self.s_out.wait(self._ev_exec)
-        pending = []
         for nm in names:
             buf = resolved[nm]
             # only non-const keyed buffers get dirty, and validation forbids
             # binding one non-const key twice, so no buffer appears twice here
             if buf.dirty:
-                blob = self._streamed.get(nm)
+                blob = rec.streamed.get(nm)
                 if blob is None:
                     blob = PinnedBlob(buf.size)
                     native.d2h_async(blob.addr, buf.ptr, buf.size, self.s_out)
-                pending.append((buf, blob))
-        if self.time_requests:
-            self._ev_end.record(self.s_out)
-        if pending:
-            self.s_out.sync()
-        else:
-            self.s_exec.sync()
-        for buf, blob in pending:
-            if self._pinned_store:
-                self.store.put_owned(buf.key, blob)
-            else:
-                self.store.put(buf.key, bytes(blob))
-            self.clock.advance_ns(self.backend.timing.flush_time_ns(buf.size))
-            stats.store_puts += 1
-            stats.bytes_flushed += buf.size
-            buf.dirty = False
-            self.dev_stats.d2h_bytes += buf.size
+                rec.pending.append((buf.key, blob, buf.size))
+                self.clock.advance_ns(self.backend.timing.flush_time_ns(buf.size))
+                stats.store_puts += 1
+                stats.bytes_flushed += buf.size
+                buf.dirty = False
+        rec.events[1].record(self.s_out)
 
-    def _drain_quietly(self) -> None:
+    def _drain_streams_quietly(self) -> None:
         """Failure-path drain: a sticky device error must not escape execute."""
         try:
-            self._drain()
+            self.s_in.sync()
+            self.s_exec.sync()
+            self.s_out.sync()
         except KaasError:
-            self._graveyard.clear()
-            self._keepalive.clear()
+            pass
 
     def _release(self, resolved, ephemerals, drop_dirty: bool) -> None:
         for buf in ephemerals:
@@ -570,24 +662,29 @@ class GpuExecutor:
         return d
 
     def close(self) -> None:
-        """Release every device allocation and the streams."""
+        """Finish in-flight work, release every device allocation and the streams."""
         if self._closed:
             return
         self._closed = True
-        self._drain_quietly()
+        try:
+            self.complete()
+        except KaasError:
+            pass
+        self._drain_streams_quietly()
         for key in list(self.cache.entries):
             buf = self.cache.entries[key]
             buf._pinned = 0
             buf._dirty = False
             self.cache.remove(key)
-        self._req_seq += 1
-        self._drain()
+        self._drain_streams_quietly()
         for s in (self.s_in, self.s_exec, self.s_out):
             s.sync()
             s.destroy()
-        for e in (self._ev_fill, self._ev_exec, self._ev_start, self._ev_end, self._ev_k0,
-                  self._ev_k1):
+        for e in (self._ev_fill, self._ev_exec):
             e.destroy()
+        for evs in self._ev_pool:
+            for e in evs:
+                e.destroy()
 
 
 # reference-compatible name

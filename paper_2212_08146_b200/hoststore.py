@@ -16,6 +16,7 @@ through ``PinnedPool`` because ``cudaHostAlloc`` costs milliseconds.
 
 from __future__ import annotations
 
+import collections
 import ctypes as C
 import threading
 
@@ -127,13 +128,27 @@ class PinnedPool:
         self.keep_bytes = keep_bytes
         self._free: dict[int, list[int]] = {}
         self._cached = 0
-        self._lock = threading.Lock()
+        # blocks come back from PinnedBlob.__del__, which the garbage collector
+        # may run at any allocation -- including one made while this thread
+        # already holds the pool lock; __del__ therefore never takes the lock,
+        # it only appends to this deque (atomic), drained under the lock.
+        self._returns: collections.deque = collections.deque()
+        self._lock = threading.RLock()
         self._heap_blocks: dict[int, C.Array] = {}
         self.allocated = 0
+
+    def _drain_returns(self) -> None:
+        while True:
+            try:
+                addr, cap = self._returns.popleft()
+            except IndexError:
+                return
+            self._release_locked(addr, cap)
 
     def alloc(self, nbytes: int) -> tuple[int, int]:
         cap = _size_class(max(1, nbytes))
         with self._lock:
+            self._drain_returns()
             lst = self._free.get(cap)
             if lst:
                 self._cached -= cap
@@ -148,11 +163,14 @@ class PinnedPool:
         return addr, cap
 
     def release(self, addr: int, cap: int) -> None:
-        with self._lock:
-            if self._cached + cap <= self.keep_bytes:
-                self._free.setdefault(cap, []).append(addr)
-                self._cached += cap
-                return
+        """Lock-free hand-back (safe from __del__); recycled on the next alloc."""
+        self._returns.append((addr, cap))
+
+    def _release_locked(self, addr: int, cap: int) -> None:
+        if self._cached + cap <= self.keep_bytes:
+            self._free.setdefault(cap, []).append(addr)
+            self._cached += cap
+            return
         self.allocated -= cap
         if self.pinned:
             native.host_free(addr)

@@ -136,6 +136,9 @@ _lib_lock = threading.Lock()
 def load(path: str | None = None) -> C.CDLL:
     """Load the shared library (cached).  Raises if it is missing."""
     global _lib
+    lib = _lib
+    if lib is not None:  # lock-free fast path (called on every native call)
+        return lib
     with _lib_lock:
         if _lib is not None:
             return _lib

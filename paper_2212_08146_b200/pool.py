@@ -35,7 +35,7 @@ class KaasService:
                  policy="affinity:8", timing: TimingModel | None = None,
                  digest_cap: int = 1024, strict_schema: bool = False, debug: bool = False,
                  devices: list[int] | None = None, executor_factory=None,
-                 log_decisions: bool = False):
+                 log_decisions: bool = False, max_inflight: int = 3):
         if executor_factory is None:
             devices = devices if devices is not None else visible_devices()
             if not devices:
@@ -46,6 +46,7 @@ class KaasService:
             raise ValueError("need at least one executor")
         self.store = store
         self.strict_schema = strict_schema
+        self.max_inflight = max_inflight
         self.timing = timing if timing is not None else TimingModel()
         self.devices = devices
         if executor_factory is None:
@@ -67,6 +68,8 @@ class KaasService:
             t.start()
 
     def _worker(self, executor) -> None:
+        if hasattr(executor, "begin"):
+            return self._pipelined_worker(executor)
         q = self._queues[executor.executor_id]
         while True:
             item = q.get()
@@ -82,6 +85,55 @@ class KaasService:
                 continue
             self.router.update_digest(executor.executor_id, resp, req)
             fut.set_result(resp)
+
+    def _pipelined_worker(self, executor) -> None:
+        """Up to ``max_inflight`` requests per executor overlap on the device:
+        request i's write-back and epilogue run while request i+1's fills and
+        kernels are queued.  Decisions are still taken strictly in arrival
+        order inside ``begin`` (bit-exact), puts and responses in ``complete``."""
+        eid = executor.executor_id
+        q = self._queues[eid]
+        futs: dict[int, tuple] = {}
+
+        def on_complete(rec, resp):
+            req, fut = futs.pop(rec.seq)
+            self.router.update_digest(eid, resp, req)
+            fut.set_result(resp)
+
+        executor.on_complete = on_complete
+        while True:
+            if executor.inflight:
+                executor.complete(block=False)
+            if executor.inflight:
+                try:
+                    item = q.get_nowait()
+                except queue.Empty:
+                    executor.complete(through=next(iter(futs)))  # block on the oldest
+                    continue
+            else:
+                item = q.get()
+            if item is None:
+                executor.complete()
+                return
+            req, fut = item
+            try:
+                rec = executor.begin(req)
+            except BaseException as exc:
+                try:
+                    executor.complete()
+                except BaseException:
+                    pass
+                failed = KaasResponse(req.request_id, Status.make_error("Internal", str(exc)))
+                self.router.update_digest(eid, failed, req)
+                fut.set_exception(exc)
+                continue
+            if isinstance(rec, KaasResponse):  # failed on the host: nothing in flight
+                self.router.update_digest(eid, rec, req)
+                fut.set_result(rec)
+                continue
+            futs[rec.seq] = (req, fut)
+            while executor.inflight > self.max_inflight:
+                executor.complete(through=next(iter(futs)))
 
     def submit_async(self, req: KaasRequest) -> Future:
         if self._closed:

@@ -279,3 +279,45 @@ def seed_resnet(store, prefix: str = "resnet", layers=None, seed: int = 0) -> No
     for name, m, n, k in layers:
         w = (rng.standard_normal(k * n, dtype=np.float32) * np.float32((2.0 / k) ** 0.5))
         store.put(f"{prefix}/w/{name}", w.astype(np.float32).tobytes())
+
+
+def mixed_universe(store, n_cgemm: int = 8, cg_n: int = 2048, n_jacobi: int = 8,
+                   jac_n: int = 4096, seed: int = 0) -> dict:
+    """BASELINE configs[3] data: a universe of const cGEMM operands and Jacobi
+    systems, drawn Zipf-wise by ``mixed_requests``."""
+    rng = np.random.default_rng(seed)
+    for i in range(n_cgemm):
+        re = rng.standard_normal((cg_n, cg_n), dtype=np.float32)
+        im = rng.standard_normal((cg_n, cg_n), dtype=np.float32)
+        m = np.empty((cg_n, cg_n), np.complex64)
+        m.real, m.imag = re, im
+        store.put(f"mix/cg/{i}", m.tobytes())
+    for i in range(n_jacobi):
+        A, b = jacobi_system(jac_n, seed=seed + 1000 + i)
+        store.put(f"mix/jA/{i}", A.tobytes())
+        store.put(f"mix/jb/{i}", b.tobytes())
+    store.put("mix/x0", np.zeros(jac_n, np.float32).tobytes())
+    return {"n_cgemm": n_cgemm, "cg_n": cg_n, "n_jacobi": n_jacobi, "jac_n": jac_n}
+
+
+def mixed_requests(universe: dict, count: int, sweeps: int = 100, zipf_s: float = 1.0,
+                   seed: int = 1) -> list[KaasRequest]:
+    """Multi-tenant stream: half cGEMM (A_i . B_j, both const, Zipf-drawn),
+    half Jacobi solves (system k const, Zipf-drawn); request ids carry a
+    tenant prefix (``t<c>/``) for the exclusive policy."""
+    rng = random.Random(seed)
+    zc = ZipfSampler(zipf_s, universe["n_cgemm"], rng)
+    zj = ZipfSampler(zipf_s, universe["n_jacobi"], rng)
+    n, jn = universe["cg_n"], universe["jac_n"]
+    out = []
+    for i in range(count):
+        tenant = f"t{i % 16}"
+        if rng.random() < 0.5:
+            a, b = zc.draw(), zc.draw()
+            out.append(cgemm_request(f"{tenant}/cg{i}", n, f"mix/cg/{a}", f"mix/cg/{b}",
+                                     f"mix/out/cg{i % 32}"))
+        else:
+            k = zj.draw()
+            out.append(jacobi_request(f"{tenant}/jac{i}", jn, sweeps, f"mix/jA/{k}", f"mix/jb/{k}",
+                                      "mix/x0", f"mix/out/x{i % 32}", f"mix/out/r{i % 32}"))
+    return out

@@ -110,3 +110,57 @@ def test_gpu_matches_oracle_on_fresh_streams(cuda, seed):
         _compare_key(k, gstore.get(k), ostore.get(k))
     assert {"NotFound", "BackendFault", "UnknownKernel", "ArityMismatch"} <= kinds
     gex.close()
+
+
+@pytest.mark.parametrize("depth", [2, 4])
+def test_pipelined_begin_complete_matches_sequential(cuda, depth):
+    """Overlapping requests (begin several, complete later) must give the
+    sequential reference's responses, cache states and store bytes --
+    including a request that reads (non-const) the key its predecessor is
+    still writing back (read-your-writes), and evictions of buffers an
+    in-flight request is still flushing (tight capacity)."""
+    from paper_2212_08146_b200 import workloads as W
+    from paper_2212_08146_b200.api import BufferArg, KaasRequest, KernelInvocation, LaunchDims, f32, i32
+    gstore, ostore = PinnedStore(), DictStore()
+    reqs = make_stream(7, 120, gstore)
+    make_stream(7, 120, ostore)
+    # read-after-write chain, back to back: r_i writes key k_i; r_{i+1} reads
+    # k_i (non-const) while r_i may still be writing it back
+    chain = []
+    for i in range(12):
+        n = 256 + 64 * i
+        bufs = [BufferArg("o", 4 * 4096, "output", key=f"f/raw{i}")]
+        invs = [KernelInvocation("fill", LaunchDims(grid_x=4096), (i32(4096), f32(0.5 + i)), ("o",))]
+        if i:
+            bufs.insert(0, BufferArg("x", 4 * 4096, "input", key=f"f/raw{i - 1}"))
+            invs.append(KernelInvocation("vector_add", LaunchDims(grid_x=n), (i32(4096),), ("x", "o", "o")))
+        chain.append(KaasRequest(f"raw/{i}", tuple(bufs), tuple(invs)))
+    reqs[20:20] = chain
+    W.seed_jacobi(gstore, 512, prefix="pj")
+    W.seed_jacobi(ostore, 512, prefix="pj")
+    for i in range(6):
+        reqs.insert(15 * i + 5, W.jacobi_request(f"pj/{i}", 512, 9, "pj/A/512", "pj/b/512",
+                                                 "pj/x0/512", f"j/pj{i % 2}", "j/pjr"))
+    cap = 3 << 20
+    gex = GpuExecutor(ExecutorConfig(capacity=cap, debug=True), gstore)
+    oex = OracleExecutor(cap, ostore)
+    got = {}
+    gex.on_complete = lambda rec, resp: got.__setitem__(rec.req.request_id, resp)
+    want = {}
+    for req in reqs:
+        want[req.request_id] = oex.execute(req)
+        rec = gex.begin(req)
+        if isinstance(rec, type(want[req.request_id])):
+            got[req.request_id] = rec
+        assert cache_digest((k, *v) for k, v in gex.cache.snapshot().items()) == \
+            cache_digest((k, *v) for k, v in oex.snapshot().items()), req.request_id
+        while gex.inflight > depth:
+            gex.complete(through=next(iter(gex._inflight)))
+    gex.complete()
+    assert set(got) == set(want)
+    for rid, resp in want.items():
+        assert response_to_doc(got[rid]) == response_to_doc(resp), rid
+    assert gstore.keys() == ostore.keys()
+    for k in ostore.keys():
+        _compare_key(k, gstore.get(k), ostore.get(k))
+    gex.close()

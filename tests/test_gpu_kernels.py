@@ -220,3 +220,20 @@ def test_saxpy_fill_literal_rounding(gpu):
     _run(ex, req)
     assert bytes(store.get("lr/o")) == (np.float32(v) * x + x).tobytes()
     assert bytes(store.get("lr/f")) == np.full(8, np.float32(v), "<f4").tobytes()
+
+
+def test_resnet_chain_bit_exact(gpu):
+    """BASELINE configs[4] shape: conv-as-GEMM chain with residual adds and
+    reused ephemeral activations, bit-exact against the oracle (first two
+    ResNet-50 stages, 22 matmuls)."""
+    ex, store = gpu
+    layers = W.resnet50_gemms()[:23]
+    W.seed_resnet(store, prefix="rn", layers=layers)
+    ostore = DictStore()
+    W.seed_resnet(ostore, prefix="rn", layers=layers)
+    req = W.resnet_chain_request("rn", prefix="rn", layers=layers, out_key="rn/out")
+    r = _run(ex, req)
+    o = OracleExecutor(1 << 30, ostore).execute(req)
+    assert o.status.ok and r.per_invocation == o.per_invocation
+    assert r.simulated_total_time == o.simulated_total_time
+    assert canon(store.get("rn/out")) == canon(ostore.get("rn/out"))
