@@ -254,9 +254,10 @@ __device__ __forceinline__ void grid_sync_mono(unsigned *counter, unsigned epoch
     unsigned v;
     asm volatile("atom.add.release.gpu.global.u32 %0, [%1], 1;" : "=r"(v) : "l"(counter) : "memory");
     const unsigned target = (epoch + 1) * gridDim.x;
+    // ld.acquire.gpu lowers to LDG.STRONG.GPU + CCTL.IVALL: the SM's L1 is
+    // invalidated, so later plain loads of x see the other CTAs' writes
     while (ld_acquire(counter) < target) {
     }
-    __threadfence();  // gpu-scope fence: later plain (L1-cached) loads see other CTAs' x
   }
   __syncthreads();
 }

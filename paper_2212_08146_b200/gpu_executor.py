@@ -201,6 +201,8 @@ class GpuExecutor:
         self._inflight: OrderedDict[int, _Req] = OrderedDict()  # seq -> begun, not completed
         self._pending_puts: dict[str, int] = {}   # key -> seq of the request that will put it
         self.on_complete = None                   # callback(req_record, response) (pool)
+        self.peers = None                         # PeerDirectory shared by a pool (peers.py)
+        self._versioned = hasattr(store, "get_versioned")
         self._closed = False
         self._plans_by_id: _LRU = _LRU(256)     # id(req) -> (req, plan)
         self._plans_by_value: _LRU = _LRU(256)  # (buffers, invocations) -> plan
@@ -224,6 +226,7 @@ class GpuExecutor:
         The allocation is released once the last request that used it is done."""
         if not buf.ptr:
             return
+        self._fence_lends(buf)
         ptr, buf.ptr = buf.ptr, 0
         owner = self._inflight.get(buf._req)
         if owner is None and self._cur is not None and buf._req == self._cur.seq:
@@ -232,6 +235,16 @@ class GpuExecutor:
             owner.graveyard.append(ptr)
         else:
             native.free_async(self.s_in, ptr)
+
+    def _fence_lends(self, buf: DeviceBuffer) -> None:
+        """Withdraw ``buf`` from the peer directory and order any later free
+        or rewrite of it after every peer copy still reading it."""
+        if self.peers is None or buf.key is None:
+            return
+        self.peers.withdraw(self.executor_id, buf)
+        for ev in self.peers.take_lends(buf):
+            self.s_in.wait(ev)
+            self.s_exec.wait(ev)
 
     def _events(self):
         if self._ev_pool:
@@ -317,7 +330,10 @@ class GpuExecutor:
         owner = self._pending_puts.get(arg.key)
         if owner is not None:  # read-your-writes: that put must land first
             self.complete(through=owner)
-        payload = self.store.get(arg.key)  # NotFound propagates
+        if self._versioned:
+            payload, version = self.store.get_versioned(arg.key)  # NotFound propagates
+        else:
+            payload, version = self.store.get(arg.key), None
         if len(payload) != arg.size:
             raise SizeMismatchError(
                 f"buffer {arg.name!r}: store object {arg.key!r} is"
@@ -325,16 +341,33 @@ class GpuExecutor:
         cur = self._cur
         if buf.ptr:
             self._wait_for_user(buf)
+            self._fence_lends(buf)
         self._mark(buf)
         if not buf.ptr:
             self._alloc(buf, self.s_in)
-        src = payload if isinstance(payload, PinnedBlob) else PinnedBlob.from_bytes(payload)
         if self.time_requests and not cur.has_fills:
             cur.events[4].record(self.s_in)
         cur.has_fills = True
-        native.h2d_async(buf.ptr, src.addr, arg.size, self.s_in)
-        cur.keepalive.append(src)
-        self.dev_stats.h2d_bytes += arg.size
+        borrowed = False
+        if self.peers is not None and version is not None:
+            def copy_from_peer(src, ready):
+                if ready is not None:
+                    self.s_in.wait(ready)
+                native.p2p_async(buf.ptr, self.device, src.ptr, src.dev, arg.size, self.s_in)
+                return native.Event(self.device).record(self.s_in)
+            borrowed = self.peers.borrow(arg.key, version, self.executor_id, copy_from_peer)
+        if borrowed:
+            self.dev_stats.p2p_bytes += arg.size
+        else:
+            src = payload if isinstance(payload, PinnedBlob) else PinnedBlob.from_bytes(payload)
+            native.h2d_async(buf.ptr, src.addr, arg.size, self.s_in)
+            cur.keepalive.append(src)
+            self.dev_stats.h2d_bytes += arg.size
+        if self.peers is not None and version is not None:
+            if buf._ready is None:
+                buf._ready = native.Event(self.device)
+            buf._ready.record(self.s_in)
+            self.peers.publish(self.executor_id, buf, version, buf._ready)
         buf.dirty = False
         self.clock.advance_ns(self.backend.timing.fetch_time_ns(arg.size))
         stats.store_gets += 1
@@ -495,7 +528,7 @@ class GpuExecutor:
             self._ev_pool.append(rec.events)
             return self._finish(req, stats, t0, Status.make_error(exc.kind, exc.message))
         self._release(resolved, ephemerals, drop_dirty=False)
-        for key, _, _ in rec.pending:
+        for key, _, _, _ in rec.pending:
             self._pending_puts[key] = rec.seq
         rec.response = self._finish(req, stats, t0, Status.make_ok(), list(plan.per_inv))
         self._inflight[rec.seq] = rec
@@ -516,14 +549,18 @@ class GpuExecutor:
             if not block and not ev[1].done():
                 break
             ev[1].sync()
-            for key, blob, size in rec.pending:
+            for key, blob, size, buf in rec.pending:
                 if self._pinned_store:
-                    self.store.put_owned(key, blob)
+                    version = self.store.put_owned(key, blob)
                 else:
-                    self.store.put(key, bytes(blob))
+                    version = self.store.put(key, bytes(blob))
                 if self._pending_puts.get(key) == seq:
                     del self._pending_puts[key]
                 self.dev_stats.d2h_bytes += size
+                # the cached copy now equals the object the store serves
+                if (self.peers is not None and isinstance(version, int) and buf.ptr
+                        and self.cache.entries.get(key) is buf and not buf.dirty):
+                    self.peers.publish(self.executor_id, buf, version, None)
             for ptr in rec.graveyard:
                 native.free_async(self.s_exec, ptr)
             if self.time_requests:
@@ -557,7 +594,9 @@ class GpuExecutor:
         dropped or ephemeral)."""
         self.clock.advance_ns(plan.advance_ns)
         for nm in plan.dirty_names:
-            resolved[nm].dirty = True
+            b = resolved[nm]
+            b.dirty = True
+            self._fence_lends(b)  # a kernel is about to rewrite it
         if plan.fail_at is not None:
             raise plan.fail_exc
         ev = rec.events
@@ -602,7 +641,7 @@ class GpuExecutor:
                 if blob is None:
                     blob = PinnedBlob(buf.size)
                     native.d2h_async(blob.addr, buf.ptr, buf.size, self.s_out)
-                rec.pending.append((buf.key, blob, buf.size))
+                rec.pending.append((buf.key, blob, buf.size, buf))
                 self.clock.advance_ns(self.backend.timing.flush_time_ns(buf.size))
                 stats.store_puts += 1
                 stats.bytes_flushed += buf.size

@@ -67,23 +67,39 @@ class ObjectStore:
 
 
 class MemoryStore(ObjectStore):
-    """Dict-backed store with the reference semantics."""
+    """Dict-backed store with the reference semantics, plus a per-key put
+    counter (``version``) so peer GPUs can tell whether a cached copy is the
+    object the store serves now (the reference has no versioning,
+    SPEC.md:171; the counter is invisible to reference callers)."""
 
     def __init__(self):
         self._objects: dict[str, bytes] = {}
         self._locks = _KeyLocks()
+        self.version: dict[str, int] = {}
 
-    def put(self, key: str, payload) -> None:
+    def put(self, key: str, payload) -> int:
+        """Store a copy; returns the key's new version."""
         _checked_key(key)
         data = bytes(payload)
         with self._locks.get(key):
             self._objects[key] = data
+            v = self.version[key] = self.version.get(key, 0) + 1
+            return v
 
     def get(self, key: str):
         _checked_key(key)
         with self._locks.get(key):
             try:
                 return self._objects[key]
+            except KeyError:
+                raise NotFoundError(f"no object under key {key!r}") from None
+
+    def get_versioned(self, key: str):
+        """(payload, version) read atomically under the key lock."""
+        _checked_key(key)
+        with self._locks.get(key):
+            try:
+                return self._objects[key], self.version.get(key, 0)
             except KeyError:
                 raise NotFoundError(f"no object under key {key!r}") from None
 
@@ -251,20 +267,20 @@ class PinnedStore(MemoryStore):
     def __init__(self, pool: PinnedPool | None = None):
         super().__init__()
         self.pool = pool or default_pool()
-        self.version: dict[str, int] = {}  # put counter per key (P2P freshness)
 
-    def put(self, key: str, payload) -> None:
+    def put(self, key: str, payload) -> int:
         _checked_key(key)
         # copy, as the reference does (store.py:72): later caller writes
         # must not reach the stored object
-        self._adopt(key, PinnedBlob.from_bytes(payload, self.pool))
+        return self._adopt(key, PinnedBlob.from_bytes(payload, self.pool))
 
-    def put_owned(self, key: str, blob: PinnedBlob) -> None:
+    def put_owned(self, key: str, blob: PinnedBlob) -> int:
         """Store ``blob`` without copying; the caller gives up ownership."""
         _checked_key(key)
-        self._adopt(key, blob)
+        return self._adopt(key, blob)
 
-    def _adopt(self, key: str, blob: PinnedBlob) -> None:
+    def _adopt(self, key: str, blob: PinnedBlob) -> int:
         with self._locks.get(key):
             self._objects[key] = blob
-            self.version[key] = self.version.get(key, 0) + 1
+            v = self.version[key] = self.version.get(key, 0) + 1
+            return v

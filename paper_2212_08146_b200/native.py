@@ -263,6 +263,15 @@ class Event:
             call("kaas_event_destroy", self.handle)
             self.handle = 0
 
+    def __del__(self):
+        # CUDA releases an event's resources once pending work on it is done
+        h = getattr(self, "handle", 0)
+        if h and _lib is not None:
+            try:
+                _lib.kaas_event_destroy(h)
+            except Exception:
+                pass
+
 
 def malloc_async(stream: Stream, nbytes: int) -> int:
     p = C.c_uint64(0)

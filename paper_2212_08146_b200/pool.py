@@ -22,6 +22,7 @@ from concurrent.futures import Future
 from . import native
 from .api import KaasRequest, KaasResponse, Status
 from .gpu_executor import ExecutorConfig, GpuBackend, GpuExecutor
+from .peers import PeerDirectory
 from .placement import Router, parse_policy
 from .timing import TimingModel
 
@@ -35,7 +36,7 @@ class KaasService:
                  policy="affinity:8", timing: TimingModel | None = None,
                  digest_cap: int = 1024, strict_schema: bool = False, debug: bool = False,
                  devices: list[int] | None = None, executor_factory=None,
-                 log_decisions: bool = False, max_inflight: int = 3):
+                 log_decisions: bool = False, max_inflight: int = 3, peer_fills: bool = True):
         if executor_factory is None:
             devices = devices if devices is not None else visible_devices()
             if not devices:
@@ -55,6 +56,18 @@ class KaasService:
                                      debug=debug, device=devices[i % len(devices)])
                 return GpuExecutor(cfg, store, GpuBackend(timing=self.timing))
         self.executors = [executor_factory(i) for i in range(n_executors)]
+        # peer fills between this pool's executors (NVLink across GPUs, D2D on one)
+        self.peers = None
+        gpu_execs = [e for e in self.executors if hasattr(e, "peers")]
+        if peer_fills and len(gpu_execs) > 1:
+            self.peers = PeerDirectory()
+            devs = sorted({e.device for e in gpu_execs})
+            for d in devs:
+                for q in devs:
+                    if d != q:
+                        native.enable_peer(d, q)
+            for e in gpu_execs:
+                e.peers = self.peers
         if isinstance(policy, str):
             policy = parse_policy(policy)
         self.router = Router([e.executor_id for e in self.executors], policy,

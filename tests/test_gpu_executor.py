@@ -164,3 +164,43 @@ def test_pipelined_begin_complete_matches_sequential(cuda, depth):
     for k in ostore.keys():
         _compare_key(k, gstore.get(k), ostore.get(k))
     gex.close()
+
+
+def test_peer_fills_preserve_decisions_and_bytes(cuda):
+    """Two executors sharing a PeerDirectory (same GPU: D2D; across GPUs the
+    same path is an NVLink peer copy).  Fills of objects the other executor
+    holds at the current store version are device-to-device copies; every
+    response, cache state and store byte still equals the reference
+    (two oracle executors over one store, same interleaving)."""
+    from paper_2212_08146_b200.api import BufferArg, KaasRequest, KernelInvocation, LaunchDims, f32, i32
+    from paper_2212_08146_b200.peers import PeerDirectory
+    gstore, ostore = PinnedStore(), DictStore()
+    reqs = make_stream(11, 160, gstore)
+    make_stream(11, 160, ostore)
+    n = 4096
+    # versioned hand-offs: a output written on one executor, read (non-const) on the other
+    for i in range(6):
+        w = KaasRequest(f"w/{i}", (BufferArg("o", 4 * n, "output", key="f/shared"),),
+                        (KernelInvocation("fill", LaunchDims(grid_x=n), (i32(n), f32(1.0 + i)), ("o",)),))
+        r = KaasRequest(f"r/{i}", (BufferArg("x", 4 * n, "input", key="f/shared"),
+                                   BufferArg("y", 4 * n, "output", key=f"f/copy{i}")),
+                        (KernelInvocation("vector_add", LaunchDims(grid_x=n), (i32(n),), ("x", "x", "y")),))
+        reqs[20 * i:20 * i] = [w, r]
+    cap = 4 << 20
+    peers = PeerDirectory()
+    gexs = [GpuExecutor(ExecutorConfig(capacity=cap, executor_id=e, debug=True), gstore) for e in (0, 1)]
+    for g in gexs:
+        g.peers = peers
+    oexs = [OracleExecutor(cap, ostore) for _ in (0, 1)]
+    for j, req in enumerate(reqs):
+        e = j % 2
+        g, o = gexs[e].execute(req), oexs[e].execute(req)
+        assert response_to_doc(g) == response_to_doc(o), req.request_id
+        assert cache_digest((k, *v) for k, v in gexs[e].cache.snapshot().items()) == \
+            cache_digest((k, *v) for k, v in oexs[e].snapshot().items())
+    assert gstore.keys() == ostore.keys()
+    for k in ostore.keys():
+        _compare_key(k, gstore.get(k), ostore.get(k))
+    assert sum(g.dev_stats.p2p_bytes for g in gexs) > 0 and peers.lends > 0
+    for g in gexs:
+        g.close()

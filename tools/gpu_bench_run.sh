@@ -8,9 +8,9 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
     python bench.py --steps 2 --warmup 3 --no-extras --cpu-seconds 0 > gpurun_out/ncu_bench.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:jacobi_rows -s 2 -c 1 \
     -o gpurun_out/jacobi_full python bench.py --steps 1 --warmup 3 --no-extras --cpu-seconds 0 > gpurun_out/ncu_jfull.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:cgemm_tf32 -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:"cgemm_(tf32|fused)" -c 1 \
     -o gpurun_out/cgemm8192_full python tools/kbench.py cgemm 8192 1 > gpurun_out/ncu_cfull.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:cgemm_tf32 -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:"cgemm_(tf32|fused)" -c 1 \
     -o gpurun_out/cgemm1024_full python tools/kbench.py cgemm 1024 1 > gpurun_out/ncu_c1full.log 2>&1
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
 tail -3 gpurun_out/gpu_tests.log; cat gpurun_out/smoke.log; cat gpurun_out/bench.json
