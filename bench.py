@@ -303,6 +303,7 @@ def ours(args, rank, world, local_rank, dist):
     from paper_2212_08146_b200.hoststore import PinnedStore
     from paper_2212_08146_b200.pool import KaasService
 
+    local_rank = local_rank % max(1, native.device_count())  # >1 rank per GPU: dev tests
     native.init_device(local_rank)
     peaks, peak_kind = load_peaks()
     store = PinnedStore()
@@ -500,7 +501,10 @@ def init_dist():
         import torch
         import torch.distributed as td
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        # the process group carries only a barrier and one float (max time):
+        # NCCL on a B200 box, gloo when asked (e.g. several ranks on one GPU)
+        backend = os.environ.get("KAAS_DIST_BACKEND") or (
+            "nccl" if torch.cuda.is_available() else "gloo")
         if backend == "nccl":
             torch.cuda.set_device(local)
         td.init_process_group(backend=backend)

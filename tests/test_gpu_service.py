@@ -53,3 +53,54 @@ def test_gpu_pool_concurrent_clients(cuda):
     for policy, entry in rep["policies"].items():
         assert entry["errors"] == 0, policy
         assert sum(entry["per_executor_requests"]) == 400
+
+
+def test_http_front_end_over_gpu_pool(cuda):
+    """Wire clients -> front end -> GPU pool: a cGEMM and a Jacobi request
+    over HTTP, results fetched back through /v1/objects."""
+    import http.client
+
+    import numpy as np
+
+    from paper_2212_08146_b200 import workloads as W
+    from paper_2212_08146_b200.api import decode_response, encode_request
+    from paper_2212_08146_b200.frontend import start
+
+    store = PinnedStore()
+    svc = KaasService(store, n_executors=2, capacity=256 << 20, policy="affinity:8", devices=[0])
+    srv, port = start(svc)
+
+    def call(method, path, body=None):
+        c = http.client.HTTPConnection("127.0.0.1", port, timeout=60)
+        c.request(method, path, body=body)
+        r = c.getresponse()
+        data = r.read()
+        c.close()
+        return r.status, data
+
+    try:
+        A, B = W.cgemm_data(64, seed=3)
+        assert call("PUT", "/v1/objects/h/A", A.tobytes())[0] == 200
+        assert call("PUT", "/v1/objects/h/B", B.tobytes())[0] == 200
+        code, body = call("POST", "/v1/invoke",
+                          encode_request(W.cgemm_request("h1", 64, "h/A", "h/B", "h/C")))
+        assert code == 200 and decode_response(body, strict=True).status.ok
+        code, data = call("GET", "/v1/objects/h/C")
+        got = np.frombuffer(data, "<c8").astype(np.complex128).reshape(64, 64)
+        truth = A.astype(np.complex128) @ B.astype(np.complex128)
+        assert np.linalg.norm(got - truth) / np.linalg.norm(truth) <= 1e-4
+        from oracle.executor import DictStore, OracleExecutor
+        W.seed_jacobi(store, 256, prefix="hj")
+        ostore = DictStore()
+        W.seed_jacobi(ostore, 256, prefix="hj")
+        jreq = W.jacobi_request("h2", 256, 50, "hj/A/256", "hj/b/256", "hj/x0/256", "hj/x", "hj/r")
+        code, body = call("POST", "/v1/invoke", encode_request(jreq))
+        assert code == 200 and decode_response(body).status.ok
+        OracleExecutor(1 << 30, ostore).execute(jreq)
+        x = np.frombuffer(call("GET", "/v1/objects/hj/x")[1], "<f4").astype(np.float64)
+        ox = np.frombuffer(ostore.get("hj/x"), "<f4").astype(np.float64)
+        assert np.abs(x - ox).max() <= 1e-5
+    finally:
+        srv.shutdown()
+        srv.server_close()
+        svc.close()
