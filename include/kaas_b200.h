@@ -45,6 +45,17 @@ extern "C" {
 #define KAAS_K_CGEMM 6       /* new: (i32 n,m,k; A, B, C) complex64, 4M x 3xTF32 */
 #define KAAS_K_JACOBI 7      /* new: (i32 n; A, b, x_in, x_out, resid)         */
 
+/* kaas_launch_desc.flags for KAAS_K_CGEMM: prepared-operand cache.  ptrs[3] /
+ * ptrs[4] (sizes[3] / sizes[4]) then hold the executor-owned buffers for the
+ * 3xTF32-split A ([A_hi; A_lo], 2*n*ldk f32) and 4M-expanded, transposed,
+ * split B ([Bt_hi; Bt_lo], 4*m*ldk f32), ldk = 2k rounded up to 32.  USE:
+ * the buffer already holds them; FILL: compute them into it (else the
+ * per-stream scratch is used and nothing is kept). */
+#define KAAS_F_CG_A_USE 1
+#define KAAS_F_CG_B_USE 2
+#define KAAS_F_CG_A_FILL 4
+#define KAAS_F_CG_B_FILL 8
+
 /* literal tags, protocol.py:27 LITERAL_TYPES order */
 #define KAAS_LIT_I32 0
 #define KAAS_LIT_I64 1

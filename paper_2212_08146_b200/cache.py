@@ -37,7 +37,8 @@ class DeviceBuffer:
     """
 
     __slots__ = ("key", "size", "is_const", "_pinned", "_dirty", "last_use",
-                 "ptr", "dev", "_cache", "_epoch", "_req", "_lends", "_ready", "__weakref__")
+                 "ptr", "dev", "_cache", "_epoch", "_req", "_lends", "_ready", "_derived",
+                 "__weakref__")
 
     def __init__(self, key: str | None, size: int, is_const: bool):
         self.key = key
@@ -53,6 +54,7 @@ class DeviceBuffer:
         self._req = -1      # last request (executor sequence no.) that used it
         self._lends = []    # events of peer copies reading this buffer (peers.py)
         self._ready = None  # event recorded after the last fill (peers.py)
+        self._derived = None  # kernel-prepared forms of the contents (gpu_executor.py)
 
     @property
     def pinned(self) -> int:

@@ -726,7 +726,8 @@ static int plain_copy_after(cudaStream_t s, const ProgressiveOut *po, const floa
 }
 
 int launch_cgemm(cudaStream_t s, int dev, int n, int m, int k, uint64_t cov, const float *A,
-                 const float *B, float *C, StreamScratch *sc, const ProgressiveOut *po) {
+                 const float *B, float *C, StreamScratch *sc, const ProgressiveOut *po,
+                 const CgemmPrepared *prep) {
   if (n == 0 || m == 0 || cov == 0) return po ? plain_copy_after(s, po, C) : 0;
   if (k == 0) {
     // empty contraction: covered cells are 0 + 0i
@@ -738,19 +739,29 @@ int launch_cgemm(cudaStream_t s, int dev, int n, int m, int k, uint64_t cov, con
   const int k2 = 2 * k;
   const int ldk = (k2 + BK - 1) / BK * BK;
   const size_t a_elems = (size_t)n * ldk, b_elems = (size_t)2 * m * ldk;
-  const size_t need = (2 * a_elems + 2 * b_elems) * sizeof(float);
-  int rc = ensure_cgemm_scratch(sc, s, need);
+  // operands come from the executor's prepared-operand cache when it has
+  // them; otherwise from per-stream scratch (only the missing side)
+  const bool a_ext = prep && prep->a, b_ext = prep && prep->b;
+  const size_t need = ((a_ext ? 0 : 2 * a_elems) + (b_ext ? 0 : 2 * b_elems)) * sizeof(float);
+  int rc = need ? ensure_cgemm_scratch(sc, s, need) : 0;
   if (rc) return rc;
-  float *Ahi = (float *)sc->cg_buf;
+  float *scratch = (float *)sc->cg_buf;
+  float *Ahi = a_ext ? prep->a : scratch;
   float *Alo = Ahi + a_elems;
-  float *Bhi = Alo + a_elems;
+  float *Bhi = b_ext ? prep->b : scratch + (a_ext ? 0 : 2 * a_elems);
   float *Blo = Bhi + b_elems;
 
   const int sms = device_props(dev).sm_count;
-  k_prep_a<<<n < sms * 16 ? n : sms * 16, 256, 0, s>>>(n, k2, ldk, A, Ahi, Alo);
-  dim3 gb((m + 31) / 32, (k + 31) / 32);
-  k_prep_b<<<gb, dim3(32, 8), 0, s>>>(k, m, ldk, reinterpret_cast<const float2 *>(B), Bhi, Blo);
-  count_launch(2);  // k_prep_b also zero-fills the K padding columns [2k, ldk)
+  if (!(a_ext && prep->a_ready)) {
+    k_prep_a<<<n < sms * 16 ? n : sms * 16, 256, 0, s>>>(n, k2, ldk, A, Ahi, Alo);
+    count_launch();
+  }
+  if (!(b_ext && prep->b_ready)) {
+    dim3 gb((m + 31) / 32, (k + 31) / 32);
+    // also zero-fills the K padding columns [2k, ldk)
+    k_prep_b<<<gb, dim3(32, 8), 0, s>>>(k, m, ldk, reinterpret_cast<const float2 *>(B), Bhi, Blo);
+    count_launch();
+  }
   KAAS_CUDA(cudaGetLastError());
 
   // Small problems: narrower N tiles so the grid covers the SMs.

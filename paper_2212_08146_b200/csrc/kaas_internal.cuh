@@ -83,8 +83,14 @@ struct JacobiChain {
   float *const *resid;       // [sweeps]
 };
 int launch_jacobi_chain(cudaStream_t s, int dev, const JacobiChain &c, StreamScratch *sc);
+// Prepared-operand buffers for cGEMM (nullptr = use per-stream scratch).
+struct CgemmPrepared {
+  float *a = nullptr;  // [A_hi; A_lo]
+  float *b = nullptr;  // [Bt_hi; Bt_lo]
+  bool a_ready = false, b_ready = false;
+};
 int launch_cgemm(cudaStream_t s, int dev, int n, int m, int k, uint64_t cov,
                  const float *A, const float *B, float *C, StreamScratch *sc,
-                 const ProgressiveOut *po = nullptr);
+                 const ProgressiveOut *po = nullptr, const CgemmPrepared *prep = nullptr);
 
 }  // namespace kaas

@@ -70,6 +70,9 @@ class ExecutorConfig:
     executor_id: int = 0
     debug: bool = False
     device: int = 0
+    # device bytes for cGEMM's prepared operands of const inputs (outside the
+    # ledger, which stays the reference's; None = 4x capacity, 0 = off)
+    prepared_capacity: int | None = None
 
     def __post_init__(self):
         if not isinstance(self.capacity, int) or self.capacity <= 0:
@@ -135,7 +138,7 @@ class _Plan:
     request costs a few numpy ops on the host instead of ~4 ms of Python."""
 
     __slots__ = ("error", "kernels", "fail_at", "fail_exc", "advance_ns", "per_inv",
-                 "template", "slots", "names", "dirty_names", "n", "stream_outs")
+                 "template", "slots", "names", "dirty_names", "n", "stream_outs", "prepared")
 
 
 class _LRU(OrderedDict):
@@ -206,6 +209,9 @@ class GpuExecutor:
         self._closed = False
         self._plans_by_id: _LRU = _LRU(256)     # id(req) -> (req, plan)
         self._plans_by_value: _LRU = _LRU(256)  # (buffers, invocations) -> plan
+        pc = config.prepared_capacity
+        self._prep_cap = 4 * config.capacity if pc is None else pc
+        self._prep_bytes = 0
 
     # -- device memory ------------------------------------------------------
 
@@ -227,7 +233,11 @@ class GpuExecutor:
         if not buf.ptr:
             return
         self._fence_lends(buf)
+        self._clear_derived(buf)
         ptr, buf.ptr = buf.ptr, 0
+        self._free_after_user(buf, ptr)
+
+    def _free_after_user(self, buf: DeviceBuffer, ptr: int) -> None:
         owner = self._inflight.get(buf._req)
         if owner is None and self._cur is not None and buf._req == self._cur.seq:
             owner = self._cur
@@ -235,6 +245,38 @@ class GpuExecutor:
             owner.graveyard.append(ptr)
         else:
             native.free_async(self.s_in, ptr)
+
+    # -- prepared operands ------------------------------------------------------
+    # cGEMM's 3xTF32 split of A and split + 4M expansion + transpose of B are
+    # pure functions of a const input's bytes: they are kept beside the cache
+    # entry, so a warm request skips the preparation pass.  They die with the
+    # entry's contents (fill, kernel write, eviction); decisions are unaffected.
+
+    def _clear_derived(self, buf: DeviceBuffer) -> None:
+        d = buf._derived
+        if not d:
+            return
+        buf._derived = None
+        for ptr, nbytes, _ in d.values():
+            self._prep_bytes -= nbytes
+            self._free_after_user(buf, ptr)
+
+    def _derived_slot(self, buf: DeviceBuffer, key, nbytes: int):
+        """-> [ptr, nbytes, ready] for ``key`` on ``buf``, allocating (on the
+        exec stream) within the prepared-operand budget; None when over it."""
+        d = buf._derived
+        if d is not None:
+            hit = d.get(key)
+            if hit is not None:
+                return hit
+        if self._prep_bytes + nbytes > self._prep_cap:
+            return None
+        slot = [native.malloc_async(self.s_exec, nbytes), nbytes, False]
+        self._prep_bytes += nbytes
+        if d is None:
+            buf._derived = d = {}
+        d[key] = slot
+        return slot
 
     def _fence_lends(self, buf: DeviceBuffer) -> None:
         """Withdraw ``buf`` from the peer directory and order any later free
@@ -342,6 +384,7 @@ class GpuExecutor:
         if buf.ptr:
             self._wait_for_user(buf)
             self._fence_lends(buf)
+            self._clear_derived(buf)
         self._mark(buf)
         if not buf.ptr:
             self._alloc(buf, self.s_in)
@@ -461,6 +504,25 @@ class GpuExecutor:
                 if not later and all(o[2] != nm for o in outs):
                     outs = [o for o in outs if o[2] != nm] + [(i, 2, nm)]
         p.stream_outs = tuple(outs)
+        # cgemm operands whose prepared forms may be cached: const inputs the
+        # request does not rewrite
+        prep = []
+        if p.fail_at is None:
+            for i, (inv, kernel) in enumerate(zip(req.invocations, kernels)):
+                if kernel.kernel_id != "cgemm":
+                    continue
+                n_, m_, k_ = (lit.value for lit in inv.literals)
+                if n_ * m_ * k_ == 0 or inv.dims.total_threads == 0:
+                    continue  # nothing is computed, so nothing would be prepared
+                ldk = (2 * k_ + 31) // 32 * 32
+                sides = []
+                for j, nbytes in ((0, 8 * n_ * ldk), (1, 16 * m_ * ldk)):
+                    arg = by_name[inv.args[j]]
+                    ok = arg.is_const and not arg.is_ephemeral and arg.name not in dirty
+                    sides.append((arg.name, ("cg", j, n_, m_, k_), nbytes) if ok else None)
+                if any(sides):
+                    prep.append((i, sides[0], sides[1]))
+        p.prepared = tuple(prep)
         p.advance_ns = advance
         p.per_inv = tuple(per_inv)
         p.dirty_names = tuple(dirty)
@@ -597,6 +659,7 @@ class GpuExecutor:
             b = resolved[nm]
             b.dirty = True
             self._fence_lends(b)  # a kernel is about to rewrite it
+            self._clear_derived(b)
         if plan.fail_at is not None:
             raise plan.fail_exc
         ev = rec.events
@@ -608,6 +671,7 @@ class GpuExecutor:
             table = np.append(table, np.uint64(0))
             descs = plan.template.copy()
             descs["ptrs"] = table[plan.slots]
+            filled = self._attach_prepared(plan, descs, resolved) if plan.prepared else ()
             self._ev_fill.record(self.s_in)
             self.s_exec.wait(self._ev_fill)
             outs = []
@@ -620,10 +684,33 @@ class GpuExecutor:
             if self.time_requests:
                 ev[2].record(self.s_exec)
             native.launch_batch(self.device, self.s_exec, descs, outs)
+            for slot in filled:
+                slot[2] = True  # later launches on s_exec are ordered after the fill
             if self.time_requests:
                 ev[3].record(self.s_exec)
             rec.has_kernels = True
             self.dev_stats.kernel_launches += plan.n
+
+    def _attach_prepared(self, plan: _Plan, descs, resolved):
+        filled = []
+        for i, *sides in plan.prepared:
+            flags = 0
+            for j, side in enumerate(sides):
+                if side is None:
+                    continue
+                name, key, nbytes = side
+                slot = self._derived_slot(resolved[name], key, nbytes)
+                if slot is None:
+                    continue
+                descs["ptrs"][i, 3 + j] = slot[0]
+                descs["sizes"][i, 3 + j] = nbytes
+                if slot[2]:
+                    flags |= (native.F_CG_A_USE, native.F_CG_B_USE)[j]
+                else:
+                    flags |= (native.F_CG_A_FILL, native.F_CG_B_FILL)[j]
+                    filled.append(slot)
+            descs["flags"][i] = flags
+        return filled
 
     def _enqueue_flush(self, rec: _Req, names, resolved, stats: _ReqStats) -> None:
         """Write-back of dirty keyed buffers in table order
@@ -712,6 +799,7 @@ class GpuExecutor:
         self._drain_streams_quietly()
         for key in list(self.cache.entries):
             buf = self.cache.entries[key]
+            self._clear_derived(buf)
             buf._pinned = 0
             buf._dirty = False
             self.cache.remove(key)

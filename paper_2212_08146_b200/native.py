@@ -93,6 +93,9 @@ _pu64 = C.POINTER(C.c_uint64)
 _vp = C.c_void_p
 
 # name -> (argtypes) ; every function returns int
+# kaas_launch_desc.flags for cgemm (include/kaas_b200.h)
+F_CG_A_USE, F_CG_B_USE, F_CG_A_FILL, F_CG_B_FILL = 1, 2, 4, 8
+
 EXPORTS = {
     "kaas_last_error": [C.c_char_p, C.c_size_t],
     "kaas_version": [C.POINTER(C.c_int), C.POINTER(C.c_int)],

@@ -144,6 +144,55 @@ def test_cgemm_config1_1024(gpu):
     assert err < 2e-5
 
 
+def test_cgemm_prepared_operand_cache(cuda):
+    """Warm cGEMMs reuse the cached 3xTF32 operands: results are bit-identical
+    to a run without the cache; a refill of the key through a non-const
+    binding, and eviction, discard the prepared forms."""
+    n, m, k = 192, 160, 96
+    rng = np.random.default_rng(5)
+
+    def cplx(r, c):
+        return (rng.standard_normal((r, c)) + 1j * rng.standard_normal((r, c))).astype("<c8")
+
+    A, B, A2 = cplx(n, k), cplx(k, m), cplx(n, k)
+    req = W.cgemm_request("pc", n, "pc/A", "pc/B", "pc/C", m=m, k=k)
+    refill = KaasRequest("pr", (BufferArg("A", A.nbytes, "input", key="pc/A"),
+                                BufferArg("B", B.nbytes, "input", key="pc/B", is_const=True),
+                                BufferArg("C", 8 * n * m, "output", key="pc/C")), req.invocations)
+    outs = {}
+    for cap in (0, None):
+        store = PinnedStore()
+        store.put("pc/A", A.tobytes())
+        store.put("pc/B", B.tobytes())
+        ex = GpuExecutor(ExecutorConfig(capacity=64 << 20, prepared_capacity=cap), store)
+        try:
+            got = []
+            for _ in range(3):
+                _run(ex, req)
+                got.append(bytes(store.get("pc/C")))
+            assert got[0] == got[1] == got[2]
+            if cap is None:
+                assert ex._prep_bytes > 0
+            store.put("pc/A", A2.tobytes())
+            _run(ex, refill)       # non-const fetch rewrites the cached entry
+            got.append(bytes(store.get("pc/C")))
+            _run(ex, req)          # const hit on the new contents
+            got.append(bytes(store.get("pc/C")))
+            assert got[3] == got[4] != got[0]
+            ex.cache.evict_until(64 << 20)  # drops every unpinned entry
+            assert ex._prep_bytes == 0
+            _run(ex, req)
+            got.append(bytes(store.get("pc/C")))
+            assert got[5] == got[4]
+            outs[cap] = got
+        finally:
+            ex.close()
+    assert outs[0] == outs[None]
+    truth = A2.astype(np.complex128) @ B.astype(np.complex128)
+    c = np.frombuffer(outs[None][4], "<c8").reshape(n, m)
+    assert np.linalg.norm(c - truth) / np.linalg.norm(truth) <= 1e-4
+
+
 def test_jacobi_config2_parity(gpu):
     """BASELINE configs[1]: N = 4096, 500 sweeps; max |dx| <= 1e-5 vs oracle."""
     ex, store = gpu
