@@ -75,8 +75,12 @@ class ScalarLiteral:
             return NotImplemented
         if self.type != other.type or type(self.value) is not type(other.value):
             return False
-        if isinstance(self.value, float) and math.isnan(self.value) and math.isnan(other.value):
-            return True
+        if isinstance(self.value, float):
+            if math.isnan(self.value) and math.isnan(other.value):
+                return True
+            # 0.0 == -0.0, but the sign bit reaches the kernel
+            return (self.value == other.value
+                    and math.copysign(1.0, self.value) == math.copysign(1.0, other.value))
         return self.value == other.value
 
     def __hash__(self):

@@ -15,6 +15,8 @@
 // elsewhere ("bit-exact").
 #include "kaas_internal.cuh"
 
+#include <atomic>
+
 namespace kaas {
 namespace {
 
@@ -114,92 +116,141 @@ __global__ void k_reduce_sum(uint64_t n, const float *x, float *out) {
 // ---- matmul: per cell acc = 0; acc = fl(acc + fl(a*b)), k ascending --------
 // (backend.py:174-189, oracle pkg/tests/oracles.py:25-33).  Bit-exactness
 // forbids split-K, so all parallelism comes from output cells: 256 threads
-// (16 x 16) each own TM x TN cells of a (16*TM) x (16*TN) tile, k staged
-// through smem BK at a time.  The tile shape is picked per launch so small-M
-// / long-K layers (ResNet stage 4: M = 49, K = 4608) still fill the SMs,
-// while big layers get 4x4 register blocking (0.5 smem loads per MAC).
+// (16 x 16) each own TM x TN cells of a (16*TM) x (16*TN) tile.  The tile
+// shape is picked per launch so small-M / long-K layers (ResNet stage 4:
+// M = 49, K = 4608) still fill the SMs, while big layers get 4x4 blocking.
+//
+// Operands stream through an S-deep ring of BK = 32 k-chunks filled by
+// cp.async (4-byte copies, zero-filled out of bounds, so any shape and
+// alignment works): S-1 chunks of loads are in flight behind the chunk being
+// computed, which is what long-K layers need -- a 2-deep ring pays the full
+// L2/HBM latency once per chunk.  A tiles are row-major in smem (k
+// contiguous, rows padded to 36 floats) so a thread reads 4 k of a row with
+// one LDS.128; a thread owns TN contiguous columns of B, read as one vector.
 // Padding products are never added (0*Inf would be NaN and +0 would flip
-// the sign of a -0.0 accumulator), so the k loop uses the true extent.
-constexpr int MM_BK = 16;
+// the sign of a -0.0 accumulator), so the tail chunk uses the true extent.
+constexpr int MM_BK = 32, MM_LDA = MM_BK + 4;
 
-template <int TM, int TN>
+__device__ __forceinline__ void cp_async4(float *dst, const float *src, bool ok) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(src),
+               "r"(ok ? 4 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+template <int TN>
+__device__ __forceinline__ void lds_vec(const float *p, float (&v)[TN]) {
+  if constexpr (TN == 4) {
+    const float4 t = *reinterpret_cast<const float4 *>(p);
+    v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+  } else if constexpr (TN == 2) {
+    const float2 t = *reinterpret_cast<const float2 *>(p);
+    v[0] = t.x; v[1] = t.y;
+  } else {
+#pragma unroll
+    for (int j = 0; j < TN; ++j) v[j] = p[j];
+  }
+}
+
+template <int TM, int TN, int S>
+constexpr int mm_smem_bytes() {
+  return S * (16 * TM * MM_LDA + MM_BK * 16 * TN) * 4;
+}
+
+template <int TM, int TN, int S>
 __global__ void __launch_bounds__(256)
 k_matmul(int n, int m, int k, uint64_t cov, const float *__restrict__ a,
          const float *__restrict__ b, float *__restrict__ out) {
   constexpr int BM = 16 * TM, BN = 16 * TN;
-  constexpr int LA = BM * MM_BK / 256, LB = MM_BK * BN / 256;  // elements per thread
-  __shared__ float As[2][MM_BK][BM];
-  __shared__ float Bs[2][MM_BK][BN];
+  constexpr int A_ST = BM * MM_LDA, B_ST = MM_BK * BN;
+  extern __shared__ __align__(16) float mm_smem[];
+  float *As = mm_smem, *Bs = mm_smem + S * A_ST;
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   const int bm = blockIdx.y * BM, bn = blockIdx.x * BN;
+  const int nk = (k + MM_BK - 1) / MM_BK;
+
+  auto issue = [&](int t) {
+    const int k0 = t * MM_BK;
+    float *as = As + (t % S) * A_ST, *bs = Bs + (t % S) * B_ST;
+#pragma unroll
+    for (int u = 0; u < BM * MM_BK / 256; ++u) {
+      const int e = threadIdx.x + 256 * u;
+      const int r = e / MM_BK, kk = e % MM_BK;
+      const bool ok = bm + r < n && k0 + kk < k;
+      cp_async4(as + r * MM_LDA + kk, ok ? a + (size_t)(bm + r) * k + k0 + kk : a, ok);
+    }
+#pragma unroll
+    for (int u = 0; u < MM_BK * BN / 256; ++u) {
+      const int e = threadIdx.x + 256 * u;
+      const int kk = e / BN, c = e % BN;
+      const bool ok = bn + c < m && k0 + kk < k;
+      cp_async4(bs + kk * BN + c, ok ? b + (size_t)(k0 + kk) * m + bn + c : b, ok);
+    }
+  };
+
   float acc[TM][TN];
 #pragma unroll
   for (int i = 0; i < TM; ++i)
 #pragma unroll
     for (int j = 0; j < TN; ++j) acc[i][j] = 0.0f;
 
-  // register staging: the next k-chunk's global loads are in flight while
-  // the current chunk computes out of the other smem buffer
-  float ra[LA], rb[LB];
-  auto load = [&](int k0) {
-    const int kc = min(MM_BK, k - k0);
 #pragma unroll
-    for (int u = 0; u < LA; ++u) {
-      const int e = threadIdx.x + 256 * u;
-      const int r = e / MM_BK, kk = e % MM_BK;
-      ra[u] = (bm + r < n && kk < kc) ? __ldg(a + (size_t)(bm + r) * k + k0 + kk) : 0.0f;
-    }
-#pragma unroll
-    for (int u = 0; u < LB; ++u) {
-      const int e = threadIdx.x + 256 * u;
-      const int kk = e / BN, c = e % BN;
-      rb[u] = (bn + c < m && kk < kc) ? __ldg(b + (size_t)(k0 + kk) * m + bn + c) : 0.0f;
-    }
-  };
-  auto stash = [&](int buf) {
-#pragma unroll
-    for (int u = 0; u < LA; ++u) {
-      const int e = threadIdx.x + 256 * u;
-      As[buf][e % MM_BK][e / MM_BK] = ra[u];
-    }
-#pragma unroll
-    for (int u = 0; u < LB; ++u) {
-      const int e = threadIdx.x + 256 * u;
-      Bs[buf][e / BN][e % BN] = rb[u];
-    }
-  };
-  if (k > 0) load(0);
-  int buf = 0;
-  for (int k0 = 0; k0 < k; k0 += MM_BK, buf ^= 1) {
-    const int kc = min(MM_BK, k - k0);
-    stash(buf);
-    __syncthreads();
-    if (k0 + MM_BK < k) load(k0 + MM_BK);
-    auto step = [&](int kk) {
-      float av[TM], bv[TN];
-#pragma unroll
-      for (int i = 0; i < TM; ++i) av[i] = As[buf][kk][ty + 16 * i];
-#pragma unroll
-      for (int j = 0; j < TN; ++j) bv[j] = Bs[buf][kk][tx + 16 * j];
-#pragma unroll
-      for (int i = 0; i < TM; ++i)
-#pragma unroll
-        for (int j = 0; j < TN; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(av[i], bv[j]));
-    };
+  for (int t = 0; t < S - 1; ++t) {
+    if (t < nk) issue(t);
+    cp_async_commit();
+  }
+  for (int t = 0; t < nk; ++t) {
+    cp_async_wait<S - 2>();
+    __syncthreads();  // chunk t landed; everyone is done with chunk t-1's stage
+    if (t + S - 1 < nk) issue(t + S - 1);
+    cp_async_commit();
+    const float *as = As + (t % S) * A_ST + ty * TM * MM_LDA;
+    const float *bs = Bs + (t % S) * B_ST + tx * TN;
+    const int kc = min(MM_BK, k - t * MM_BK);
     if (kc == MM_BK) {
 #pragma unroll
-      for (int kk = 0; kk < MM_BK; ++kk) step(kk);
+      for (int k4 = 0; k4 < MM_BK; k4 += 4) {
+        float4 av[TM];
+#pragma unroll
+        for (int i = 0; i < TM; ++i) av[i] = *reinterpret_cast<const float4 *>(as + i * MM_LDA + k4);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float bv[TN];
+          lds_vec<TN>(bs + (k4 + q) * BN, bv);
+#pragma unroll
+          for (int i = 0; i < TM; ++i) {
+            const float x = q == 0 ? av[i].x : q == 1 ? av[i].y : q == 2 ? av[i].z : av[i].w;
+#pragma unroll
+            for (int j = 0; j < TN; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(x, bv[j]));
+          }
+        }
+      }
     } else {
-      for (int kk = 0; kk < kc; ++kk) step(kk);
+      for (int kk = 0; kk < kc; ++kk) {
+        float bv[TN];
+        lds_vec<TN>(bs + kk * BN, bv);
+#pragma unroll
+        for (int i = 0; i < TM; ++i) {
+          const float x = as[i * MM_LDA + kk];
+#pragma unroll
+          for (int j = 0; j < TN; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(x, bv[j]));
+        }
+      }
     }
   }
+  cp_async_wait<0>();
 #pragma unroll
   for (int i = 0; i < TM; ++i) {
-    const int r = bm + ty + 16 * i;
+    const int r = bm + ty * TM + i;
     if (r >= n) continue;
 #pragma unroll
     for (int j = 0; j < TN; ++j) {
-      const int c = bn + tx + 16 * j;
+      const int c = bn + tx * TN + j;
       if (c >= m) continue;
       const uint64_t g = (uint64_t)r * m + c;
       if (g < cov) out[g] = acc[i][j];
@@ -253,8 +304,18 @@ int launch_matmul(cudaStream_t s, int dev, uint64_t n, uint64_t m, uint64_t k, u
   const uint64_t gy = (n + 16 * tm - 1) / (16 * tm), gx = (m + 16 * tn - 1) / (16 * tn);
   if (gy > 65535) return fail(KAAS_E_INVALID, "matmul: n too large for grid.y");
   dim3 grid((unsigned)gx, (unsigned)gy);
-#define MM_LAUNCH(TM, TN) \
-  k_matmul<TM, TN><<<grid, 256, 0, s>>>((int)n, (int)m, (int)k, cov, a, b, out)
+#define MM_LAUNCH(TM, TN)                                                               \
+  do {                                                                                  \
+    constexpr int S_ = (TM) * (TN) >= 8 ? 4 : 8;                                        \
+    constexpr int SM_ = mm_smem_bytes<TM, TN, S_>();                                    \
+    static std::atomic<uint64_t> attr_done{0}; /* per device (dev < 64) */               \
+    if (!(attr_done.load(std::memory_order_relaxed) >> (dev & 63) & 1)) {               \
+      KAAS_CUDA(cudaFuncSetAttribute(k_matmul<TM, TN, S_>,                              \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, SM_)); \
+      attr_done.fetch_or(1ull << (dev & 63));                                           \
+    }                                                                                   \
+    k_matmul<TM, TN, S_><<<grid, 256, SM_, s>>>((int)n, (int)m, (int)k, cov, a, b, out); \
+  } while (0)
   if (tm == 4 && tn == 4) MM_LAUNCH(4, 4);
   else if (tm == 2 && tn == 4) MM_LAUNCH(2, 4);
   else if (tm == 4 && tn == 2) MM_LAUNCH(4, 2);

@@ -827,6 +827,247 @@ k_jacobi_rows(const __grid_constant__ ChainParams p, float *partials, unsigned *
   }
 }
 
+// ---- column-split kernel with A kept on chip (n <= 4096) ---------------------
+//
+// The row kernel is bound by the SM's load-return path, not by L2: every
+// warp re-reads all of x through L1 for each of its rows, so per sweep an SM
+// moves its 453 KB band of A plus 28 x 16 KB of x into registers (ncu:
+// l1tex writeback 60% active over the whole chain).  Here the band is
+// transposed onto the CTA instead: 8 warps split the columns (each lane owns
+// 4 float4 columns and holds its x values in registers, so x crosses the
+// load path once per CTA), and every thread keeps its slice of the band's
+// rows in three tiers that persist across all sweeps of the launch:
+//   rows 0..5    registers (96 KB per SM)
+//   rows 6..19   thread-private shared memory (224 KB per SM, LDS.128,
+//                conflict-free: [row][u][thread])
+//   rows 20..27  re-read from L2 (evict_last) in two groups of 4; the first
+//                group's loads are issued before the grid barrier
+// Each lane accumulates one FMA chain per row over its 16 columns; the 28
+// row partials are reduced across the warp with a 31-shuffle transpose
+// reduction (lane l ends with row l) and across warps in fixed order, so the
+// result is deterministic.  The diagonal is zeroed as A is loaded.
+constexpr int kColW = 8;
+constexpr int kColT = kColW * 32;
+constexpr int kColC4 = 4;            // float4 columns per lane: n4 <= 8 * 32 * 4
+constexpr int kColRows = 28;         // band rows per CTA
+constexpr int kColRR = 6;            // register rows
+constexpr int kColRS = 14;           // shared-memory rows
+constexpr int kColG = 4;             // L2 rows per load group
+static_assert(kColRR + kColRS + 2 * kColG == kColRows, "row tiers must cover the band");
+constexpr size_t kColSmem = (size_t)kColRS * kColC4 * kColT * sizeof(float4);
+
+__device__ __forceinline__ float4 zero4() { return make_float4(0.f, 0.f, 0.f, 0.f); }
+
+// band row held by reduction slot l (see the two slot sets in k_jacobi_cols);
+// 32 = empty slot
+__device__ __forceinline__ int col_slot_row(int l) {
+  constexpr int L2R0 = kColRR + kColRS, S0 = 16 - kColG - kColRR;
+  if (l < kColG) return L2R0 + l;                       // L2 group 0
+  if (l < kColG + kColRR) return l - kColG;             // register rows
+  if (l < 16) return kColRR + (l - kColG - kColRR);     // smem rows 0..S0-1
+  const int k = l - 16;
+  if (k < kColRS - S0) return kColRR + S0 + k;          // smem rows S0..
+  if (k < kColRS - S0 + kColG) return L2R0 + kColG + (k - (kColRS - S0));  // L2 group 1
+  return 32;
+}
+
+__global__ void __launch_bounds__(kColT, 1)
+k_jacobi_cols(const __grid_constant__ ChainParams p, float *partials, unsigned *sync) {
+  extern __shared__ __align__(16) float4 acache[];  // [kColRS][kColC4][kColT]
+  __shared__ float red[kColW][32];
+  const int n = p.n, n4 = n >> 2;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  int r0, r1;
+  band(p.cov, r0, r1);
+  const int R = r1 - r0;
+  const uint64_t pol = l2_policy(p.keep_l2 != 0);
+  const int cbase = warp * 32 * kColC4 + lane;  // this lane's float4 columns: cbase + 32u
+
+  // A[r0 + rl][cbase + 32u]; rows past the band and columns past n read as
+  // 0 (predicated loads: nothing consumes the value at issue, so the L2 tier
+  // really is in flight while other rows compute).  `z` is an opaque 0 from
+  // the caller: it keeps the compiler from hoisting 8 rows x 4 addresses out
+  // of the sweep loop into registers (they are a few IMADs to recompute).
+  auto lda_raw = [&](int rl, int u, int z) -> float4 {
+    const int c4 = cbase + 32 * u;
+    float4 a = zero4();
+    if (rl < R && c4 < n4) a = ld_a(p.A + (size_t)(r0 + rl + z) * n + 4 * c4, pol);
+    return a;
+  };
+  // the cached tiers hold A with the diagonal zeroed
+  auto lda = [&](int rl, int u, int z) -> float4 {
+    float4 a = lda_raw(rl, u, z);
+    const int c4 = cbase + 32 * u, i = r0 + rl;
+    if (c4 == (i >> 2)) {
+      const int d = i & 3;
+      a.x = d == 0 ? 0.f : a.x;
+      a.y = d == 1 ? 0.f : a.y;
+      a.z = d == 2 ? 0.f : a.z;
+      a.w = d == 3 ? 0.f : a.w;
+    }
+    return a;
+  };
+  auto opaque0 = [] {
+    int z;
+    asm volatile("mov.u32 %0, 0;" : "=r"(z));
+    return z;
+  };
+  float4 areg[kColRR][kColC4];
+#pragma unroll
+  for (int r = 0; r < kColRR; ++r)
+#pragma unroll
+    for (int u = 0; u < kColC4; ++u) areg[r][u] = lda(r, u, 0);
+#pragma unroll 1
+  for (int r = 0; r < kColRS; ++r)
+#pragma unroll
+    for (int u = 0; u < kColC4; ++u) acache[(r * kColC4 + u) * kColT + tid] = lda(kColRR + r, u, 0);
+  const int my_rl = col_slot_row(lane);  // warp 0, lane l finishes slot l's row
+  float bi = 0.f, di = 1.f;
+  if (warp == 0 && my_rl < R) {
+    bi = __ldg(p.b + r0 + my_rl);
+    di = __ldg(p.A + (size_t)(r0 + my_rl) * n + r0 + my_rl);
+  }
+  constexpr int L2R0 = kColRR + kColRS;
+  float4 pf[kColG][kColC4];
+  auto issue = [&](int g) {
+    const int z = opaque0();
+#pragma unroll
+    for (int j = 0; j < kColG; ++j)
+#pragma unroll
+      for (int u = 0; u < kColC4; ++u) pf[j][u] = lda_raw(L2R0 + g * kColG + j, u, z);
+  };
+  // L2-tier rows whose diagonal lies in this lane's columns (bit = L2 row)
+  unsigned dmask = 0;
+#pragma unroll
+  for (int j = 0; j < 2 * kColG; ++j) {
+    const int off = ((r0 + L2R0 + j) >> 2) - cbase;
+    if (L2R0 + j < R && off >= 0 && off % 32 == 0 && off / 32 < kColC4) dmask |= 1u << j;
+  }
+  issue(0);
+
+  for (int s = 0; s < p.sweeps; ++s) {
+    const float *x_in = p.ptrs[p.idx[s][0]];
+    float *x_out = p.ptrs[p.idx[s][1]];
+    const bool want_resid = (p.idx[s][2] & 0x80) != 0;
+    float4 xr[kColC4];
+#pragma unroll
+    for (int u = 0; u < kColC4; ++u)
+      xr[u] = cbase + 32 * u < n4 ? __ldcg(reinterpret_cast<const float4 *>(x_in) + cbase + 32 * u)
+                                  : zero4();
+    auto dot = [&](const float4 (&a)[kColC4]) {
+      float acc = 0.f;
+#pragma unroll
+      for (int u = 0; u < kColC4; ++u) {
+        acc = fmaf(a[u].x, xr[u].x, acc);
+        acc = fmaf(a[u].y, xr[u].y, acc);
+        acc = fmaf(a[u].z, xr[u].z, acc);
+        acc = fmaf(a[u].w, xr[u].w, acc);
+      }
+      return acc;
+    };
+    // Rows are reduced in two sets of 16 slots so only 16 partials are live:
+    // set 0 = L2 group 0, register rows, smem rows 0..5; set 1 = smem rows
+    // 6..13, L2 group 1, 4 empty slots (slot -> row: col_slot_row()).
+    // Reduction of one set: after the h-step (h = 8..1), v[k] (k < h) holds
+    // a lane-pair sum of slot k + (lane's bits below 16); a final xor-16 add
+    // completes it, and lane l ends with slot l & 15.
+    // L2-tier row j: diagonal excluded at consumption (rare lanes only)
+    auto dot_l2 = [&](float4 (&a)[kColC4], int j) {
+      if ((dmask >> j) & 1u) {
+        const int i = r0 + L2R0 + j, u = (((i >> 2) - cbase) / 32), d = i & 3;
+#pragma unroll
+        for (int q = 0; q < kColC4; ++q) {
+          if (q == u) {
+            a[q].x = d == 0 ? 0.f : a[q].x;
+            a[q].y = d == 1 ? 0.f : a[q].y;
+            a[q].z = d == 2 ? 0.f : a[q].z;
+            a[q].w = d == 3 ? 0.f : a[q].w;
+          }
+        }
+      }
+      return dot(a);
+    };
+    auto reduce16 = [&](float (&v)[16]) {
+#pragma unroll
+      for (int h = 8; h >= 1; h >>= 1) {
+        const bool up = (lane & h) != 0;
+#pragma unroll
+        for (int k = 0; k < h; ++k) {
+          const float send = up ? v[k] : v[k + h];
+          const float keep = up ? v[k + h] : v[k];
+          v[k] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+        }
+      }
+      return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 16);
+    };
+    float mine;
+    {
+      float v[16];
+#pragma unroll
+      for (int j = 0; j < kColG; ++j) v[j] = dot_l2(pf[j], j);  // prefetched group 0
+      issue(1);
+#pragma unroll
+      for (int r = 0; r < kColRR; ++r) v[kColG + r] = dot(areg[r]);
+#pragma unroll
+      for (int r = 0; r < 16 - kColG - kColRR; ++r) {
+        float4 a[kColC4];
+#pragma unroll
+        for (int u = 0; u < kColC4; ++u) a[u] = acache[(r * kColC4 + u) * kColT + tid];
+        v[kColG + kColRR + r] = dot(a);
+      }
+      mine = reduce16(v);
+    }
+    {
+      float v[16];
+      constexpr int S0 = 16 - kColG - kColRR;
+#pragma unroll
+      for (int r = S0; r < kColRS; ++r) {
+        float4 a[kColC4];
+#pragma unroll
+        for (int u = 0; u < kColC4; ++u) a[u] = acache[(r * kColC4 + u) * kColT + tid];
+        v[r - S0] = dot(a);
+      }
+#pragma unroll
+      for (int j = 0; j < kColG; ++j) v[kColRS - S0 + j] = dot_l2(pf[j], kColG + j);
+#pragma unroll
+      for (int k = kColRS - S0 + kColG; k < 16; ++k) v[k] = 0.f;
+      if (s + 1 < p.sweeps) issue(0);  // A is the same every sweep: in flight across the barrier
+      const float other = reduce16(v);
+      mine = lane < 16 ? mine : other;
+    }
+    red[warp][lane] = mine;  // slot "lane"
+    __syncthreads();
+    float *slot = partials + (s & 1) * kMaxJacobiBlocks;
+    if (warp == 0) {
+      float tot = 0.f;
+#pragma unroll
+      for (int w = 0; w < kColW; ++w) tot += red[w][lane];
+      float res = 0.f;
+      if (my_rl < R) {
+        const float xn = (bi - tot) / di;  // IEEE div.rn
+        x_out[r0 + my_rl] = xn;
+        res = fabsf(xn - __ldcg(x_in + r0 + my_rl));
+      }
+      if (want_resid) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) res += __shfl_xor_sync(0xffffffffu, res, off);
+        if (lane == 0) slot[blockIdx.x] = res;
+      }
+    }
+    grid_sync_mono(sync + 3, (unsigned)s);  // also orders red[] reuse
+    if (want_resid && blockIdx.x == 0 && threadIdx.x < 32)
+      finish_resid(slot, gridDim.x, p.ptrs[p.idx[s][2] & 0x7f]);
+  }
+}
+
+bool use_cols_kernel(int dev, int n, uint64_t cov, int blocks) {
+  const char *e = getenv("KAAS_JACOBI_PATH");  // dev A/B: cols (default where it fits)
+  if (e && e[0] != 'c') return false;
+  return n % 4 == 0 && n >= 2048 && n <= kColW * 32 * kColC4 * 4 &&
+         (cov + blocks - 1) / blocks <= (uint64_t)kColRows &&
+         device_props(dev).max_smem_optin >= (int)(kColSmem + sizeof(float) * kColW * 32);
+}
+
 // threads for the row kernel: one warp per band row, 4..32 warps
 int rows_threads(int dev, uint64_t cov) {
   const int sms = device_props(dev).sm_count;
@@ -1097,7 +1338,14 @@ int launch_jacobi_chain(cudaStream_t s, int dev, const JacobiChain &c, StreamScr
     if ((uint64_t)blocks > c.cov) blocks = c.cov > 0 ? (int)c.cov : 1;
     float *partials = sc->jac_partials;
     unsigned *sync = sc->jac_sync;
-    if (use_rows) {
+    if (use_rows && use_cols_kernel(dev, c.n, c.cov, blocks)) {
+      KAAS_CUDA(cudaFuncSetAttribute((const void *)k_jacobi_cols,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kColSmem));
+      KAAS_CUDA(cudaMemsetAsync(sync + 3, 0, sizeof(unsigned), s));  // monotonic barrier counter
+      void *cargs[] = {(void *)&p, (void *)&partials, (void *)&sync};
+      KAAS_CUDA(cudaLaunchCooperativeKernel((const void *)k_jacobi_cols, dim3(blocks), dim3(kColT),
+                                            cargs, kColSmem, s));
+    } else if (use_rows) {
       KAAS_CUDA(cudaMemsetAsync(sync + 3, 0, sizeof(unsigned), s));  // monotonic barrier counter
       void *rargs[] = {(void *)&p, (void *)&partials, (void *)&sync};
       KAAS_CUDA(cudaLaunchCooperativeKernel(rfn, dim3(blocks),

@@ -153,6 +153,28 @@ class _LRU(OrderedDict):
             self.popitem(last=False)
 
 
+def _plan_key(req: KaasRequest):
+    """Exact structural key of what a plan depends on: the buffer table and
+    the invocation list.  Numeric fields carry their types (``4``, ``4.0``
+    and ``True`` compare equal in Python, but validation tells them apart),
+    floats are keyed by their exact bits (``0.0 == -0.0``), and the tuples
+    are plain, so hashing and comparing run at C speed."""
+    bufs = tuple([(b.name, b.size, type(b.size), b.direction, b.key, b.is_const,
+                   type(b.is_const), b.is_ephemeral, type(b.is_ephemeral))
+                  for b in req.buffers])
+    out = []
+    ap = out.append
+    for i in req.invocations:
+        d = i.dims
+        ap((i.kernel_id, d.grid_x, d.grid_y, d.grid_z, d.block_x, d.block_y, d.block_z,
+            type(d.grid_x), type(d.grid_y), type(d.grid_z),
+            type(d.block_x), type(d.block_y), type(d.block_z),
+            tuple([(lit.type, type(lit.value),
+                    lit.value.hex() if type(lit.value) is float else lit.value)
+                   for lit in i.literals]), i.args))
+    return bufs, tuple(out)
+
+
 class _Req:
     """One request between ``begin`` (decisions made, device work enqueued)
     and ``complete`` (device done, store puts, response)."""
@@ -428,8 +450,8 @@ class GpuExecutor:
             return hit[1]
         if not isinstance(req.request_id, str) or not req.request_id:
             return self._build_plan(req)  # invalid id: never cached
-        key = (req.buffers, req.invocations)
         try:
+            key = _plan_key(req)
             plan = self._plans_by_value.get(key)
         except TypeError:  # unhashable field values: plan without caching
             return self._build_plan(req)

@@ -214,9 +214,12 @@ def test_jacobi_config2_parity(gpu):
     assert abs(gr - orr) <= 1e-4 * abs(orr) + 1e-6
 
 
-@pytest.mark.parametrize("n,sweeps,cov", [(1001, 9, None), (64, 5, 40), (4100, 3, None), (12, 1, None)])
+@pytest.mark.parametrize("n,sweeps,cov", [(1001, 9, None), (64, 5, 40), (4100, 3, None), (12, 1, None),
+                                          (2048, 7, None), (3000, 6, 2999), (4096, 4, 4001)])
 def test_jacobi_edge_shapes(gpu, n, sweeps, cov):
-    """n % 4 != 0 (scalar path), partial coverage, single sweep, odd widths."""
+    """n % 4 != 0 (scalar path), partial coverage, single sweep, odd widths;
+    2048..4096 run the column-split on-chip kernel (short bands, columns past
+    n in the last warp, a partial last band)."""
     ex, store = gpu
     A, b = W.seed_jacobi(store, n, prefix=f"je{n}")
     req = W.jacobi_request(f"je{n}", n, sweeps, f"je{n}/A/{n}", f"je{n}/b/{n}", f"je{n}/x0/{n}",

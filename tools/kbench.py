@@ -3,6 +3,7 @@
     python tools/kbench.py jacobi [n] [sweeps] [reps]
     python tools/kbench.py cgemm [n] [reps]
     python tools/kbench.py matmul M N K [reps]
+    python tools/kbench.py resnet [reps]      per-layer bit-exact matmul vs. its floor
 """
 
 import sys
@@ -97,9 +98,33 @@ def matmul(M, N, K, reps=5):
               [4 * M * K, 4 * K * N, 4 * M * N])
     ms = timed(s, lambda: native.launch_batch(0, s, d), reps)
     print(f"matmul {M}x{N}x{K}: {ms*1e3:.1f} us  {M*N*K/ms/1e9:.2f} TMAC/s")
+    for p in (pa, pb, pc):
+        native.free_async(s, p)
+    s.sync()
+    return ms
+
+
+def resnet(reps=20):
+    """Each ResNet-50 conv-as-GEMM layer alone, against its floor: issue
+    (FMUL+FADD per MAC over 148x128 lanes) or the serial FADD chain (4
+    cycles per k), at 1.9 GHz; then the whole chain as one batch."""
+    from paper_2212_08146_b200.workloads import resnet50_gemms
+    layers = resnet50_gemms()
+    seen, tot, floor_tot = {}, 0.0, 0.0
+    for name, m, n, k in layers:
+        key = (m, n, k)
+        if key not in seen:
+            seen[key] = matmul(m, n, k, reps)
+        ms = seen[key]
+        fl = max(m * n * k * 2 / (148 * 128), 4 * k) / 1.9e6
+        tot += ms
+        floor_tot += fl
+        print(f"  {name:12s} {ms*1e3:8.1f} us  floor {fl*1e3:6.1f} us  x{ms/fl:5.1f}")
+    print(f"sum of layers {tot*1e3:.1f} us, floor {floor_tot*1e3:.1f} us, "
+          f"{sum(m*n*k for _, m, n, k in layers)/tot/1e9:.2f} TMAC/s")
 
 
 if __name__ == "__main__":
     what = sys.argv[1]
     args = [int(a) for a in sys.argv[2:]]
-    {"jacobi": jacobi, "cgemm": cgemm, "matmul": matmul}[what](*args)
+    {"jacobi": jacobi, "cgemm": cgemm, "matmul": matmul, "resnet": resnet}[what](*args)
