@@ -236,6 +236,12 @@ struct ChainParams {
   // per sweep: x_in, x_out, resid indices into ptrs
   unsigned char idx[kChainMaxSweeps][3];
   int n, cov, sweeps, keep_l2;
+  // column kernel only: x of sweep s >= 1 published as (value, tag0 + s)
+  // words in xt[s & 1] instead of behind a grid barrier (tagged != 0)
+  unsigned long long *xt;
+  unsigned tag0;
+  int tagged;
+  int poll_ns;  // back-off between unsuccessful polls
 };
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
@@ -858,6 +864,20 @@ constexpr size_t kColSmem = (size_t)kColRS * kColC4 * kColT * sizeof(float4);
 
 __device__ __forceinline__ float4 zero4() { return make_float4(0.f, 0.f, 0.f, 0.f); }
 
+// (value, tag) words: 8-byte aligned accesses are single-copy atomic, so a
+// reader that sees the tag it waits for also sees that sweep's value
+__device__ __forceinline__ ulonglong2 ld_relaxed_u64x2(const unsigned long long *p) {
+  ulonglong2 v;
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long tagged_word(float v, unsigned tag) {
+  return ((unsigned long long)tag << 32) | __float_as_uint(v);
+}
+
 // band row held by reduction slot l (see the two slot sets in k_jacobi_cols);
 // 32 = empty slot
 __device__ __forceinline__ int col_slot_row(int l) {
@@ -883,19 +903,25 @@ k_jacobi_cols(const __grid_constant__ ChainParams p, float *partials, unsigned *
   const uint64_t pol = l2_policy(p.keep_l2 != 0);
   const int cbase = warp * 32 * kColC4 + lane;  // this lane's float4 columns: cbase + 32u
 
-  // A[r0 + rl][cbase + 32u]; rows past the band and columns past n read as
-  // 0 (predicated loads: nothing consumes the value at issue, so the L2 tier
-  // really is in flight while other rows compute).  `z` is an opaque 0 from
-  // the caller: it keeps the compiler from hoisting 8 rows x 4 addresses out
-  // of the sweep loop into registers (they are a few IMADs to recompute).
+  // A[r0 + rl][cbase + 32u].  Rows past the band are clamped to a valid row
+  // (their partials are discarded); columns past n read as 0, which only a
+  // narrow system (n4 < 1024) needs, so the full-width case has no
+  // predicates at all.  Nothing consumes a value at issue, so the L2 tier
+  // really is in flight while other rows compute.  `z` is an opaque 0 from
+  // the caller: it keeps the compiler from hoisting 8 row addresses out of
+  // the sweep loop into registers (one IMAD.WIDE per row to recompute).
+  const bool full = cbase + 32 * (kColC4 - 1) < n4;  // all of this lane's columns exist
   auto lda_raw = [&](int rl, int u, int z) -> float4 {
-    const int c4 = cbase + 32 * u;
+    const float4 *rp = reinterpret_cast<const float4 *>(p.A) +
+                       (size_t)(r0 + min(rl, R - 1) + z) * n4 + cbase;
+    if (full) return ld_a(reinterpret_cast<const float *>(rp + 32 * u), pol);
     float4 a = zero4();
-    if (rl < R && c4 < n4) a = ld_a(p.A + (size_t)(r0 + rl + z) * n + 4 * c4, pol);
+    if (cbase + 32 * u < n4) a = ld_a(reinterpret_cast<const float *>(rp + 32 * u), pol);
     return a;
   };
   // the cached tiers hold A with the diagonal zeroed
   auto lda = [&](int rl, int u, int z) -> float4 {
+    if (rl >= R) return zero4();
     float4 a = lda_raw(rl, u, z);
     const int c4 = cbase + 32 * u, i = r0 + rl;
     if (c4 == (i >> 2)) {
@@ -945,15 +971,44 @@ k_jacobi_cols(const __grid_constant__ ChainParams p, float *partials, unsigned *
   }
   issue(0);
 
+  float xprev = 0.f;    // warp 0: this lane's row value from the previous sweep
+  unsigned epoch = 0;   // grid barriers passed (monotonic counter target)
   for (int s = 0; s < p.sweeps; ++s) {
     const float *x_in = p.ptrs[p.idx[s][0]];
     float *x_out = p.ptrs[p.idx[s][1]];
     const bool want_resid = (p.idx[s][2] & 0x80) != 0;
+    const bool from_tags = p.tagged && s > 0;
     float4 xr[kColC4];
+    if (!from_tags) {
 #pragma unroll
-    for (int u = 0; u < kColC4; ++u)
-      xr[u] = cbase + 32 * u < n4 ? __ldcg(reinterpret_cast<const float4 *>(x_in) + cbase + 32 * u)
-                                  : zero4();
+      for (int u = 0; u < kColC4; ++u)
+        xr[u] = cbase + 32 * u < n4 ? __ldcg(reinterpret_cast<const float4 *>(x_in) + cbase + 32 * u)
+                                    : zero4();
+    } else {
+      // wait for this lane's 16 x values of sweep s by polling their tags:
+      // the producers' stores are the only synchronisation
+      const unsigned want = p.tag0 + (unsigned)s;
+      const unsigned long long *src = p.xt + (size_t)(s & 1) * kJacTaggedMaxN;
+#pragma unroll
+      for (int u = 0; u < kColC4; ++u) {
+        const int c4 = cbase + 32 * u;
+        if (c4 < n4) {
+          ulonglong2 q0, q1;
+          unsigned spins = 0;
+          do {
+            if (++spins > (1u << 22)) __trap();  // a lost producer: fail loudly, never hang
+            if (spins > 1 && p.poll_ns) __nanosleep(p.poll_ns);
+            q0 = ld_relaxed_u64x2(src + 4 * c4);
+            q1 = ld_relaxed_u64x2(src + 4 * c4 + 2);
+          } while ((unsigned)(q0.x >> 32) != want || (unsigned)(q0.y >> 32) != want ||
+                   (unsigned)(q1.x >> 32) != want || (unsigned)(q1.y >> 32) != want);
+          xr[u] = make_float4(__uint_as_float((unsigned)q0.x), __uint_as_float((unsigned)q0.y),
+                              __uint_as_float((unsigned)q1.x), __uint_as_float((unsigned)q1.y));
+        } else {
+          xr[u] = zero4();
+        }
+      }
+    }
     auto dot = [&](const float4 (&a)[kColC4]) {
       float acc = 0.f;
 #pragma unroll
@@ -971,21 +1026,26 @@ k_jacobi_cols(const __grid_constant__ ChainParams p, float *partials, unsigned *
     // Reduction of one set: after the h-step (h = 8..1), v[k] (k < h) holds
     // a lane-pair sum of slot k + (lane's bits below 16); a final xor-16 add
     // completes it, and lane l ends with slot l & 15.
-    // L2-tier row j: diagonal excluded at consumption (rare lanes only)
-    auto dot_l2 = [&](float4 (&a)[kColC4], int j) {
-      if ((dmask >> j) & 1u) {
-        const int i = r0 + L2R0 + j, u = (((i >> 2) - cbase) / 32), d = i & 3;
+    // L2-tier group g: the diagonal is excluded at consumption; only the few
+    // lanes that own one of the group's diagonals take the branch
+    auto mask_group = [&](int g) {
+      if ((dmask >> (g * kColG)) & ((1u << kColG) - 1u)) {
 #pragma unroll
-        for (int q = 0; q < kColC4; ++q) {
-          if (q == u) {
-            a[q].x = d == 0 ? 0.f : a[q].x;
-            a[q].y = d == 1 ? 0.f : a[q].y;
-            a[q].z = d == 2 ? 0.f : a[q].z;
-            a[q].w = d == 3 ? 0.f : a[q].w;
+        for (int j = 0; j < kColG; ++j) {
+          if ((dmask >> (g * kColG + j)) & 1u) {
+            const int i = r0 + L2R0 + g * kColG + j, u = ((i >> 2) - cbase) / 32, d = i & 3;
+#pragma unroll
+            for (int q = 0; q < kColC4; ++q) {
+              if (q == u) {
+                pf[j][q].x = d == 0 ? 0.f : pf[j][q].x;
+                pf[j][q].y = d == 1 ? 0.f : pf[j][q].y;
+                pf[j][q].z = d == 2 ? 0.f : pf[j][q].z;
+                pf[j][q].w = d == 3 ? 0.f : pf[j][q].w;
+              }
+            }
           }
         }
       }
-      return dot(a);
     };
     auto reduce16 = [&](float (&v)[16]) {
 #pragma unroll
@@ -1003,8 +1063,9 @@ k_jacobi_cols(const __grid_constant__ ChainParams p, float *partials, unsigned *
     float mine;
     {
       float v[16];
+      mask_group(0);
 #pragma unroll
-      for (int j = 0; j < kColG; ++j) v[j] = dot_l2(pf[j], j);  // prefetched group 0
+      for (int j = 0; j < kColG; ++j) v[j] = dot(pf[j]);  // prefetched group 0
       issue(1);
 #pragma unroll
       for (int r = 0; r < kColRR; ++r) v[kColG + r] = dot(areg[r]);
@@ -1027,8 +1088,9 @@ k_jacobi_cols(const __grid_constant__ ChainParams p, float *partials, unsigned *
         for (int u = 0; u < kColC4; ++u) a[u] = acache[(r * kColC4 + u) * kColT + tid];
         v[r - S0] = dot(a);
       }
+      mask_group(1);
 #pragma unroll
-      for (int j = 0; j < kColG; ++j) v[kColRS - S0 + j] = dot_l2(pf[j], kColG + j);
+      for (int j = 0; j < kColG; ++j) v[kColRS - S0 + j] = dot(pf[j]);
 #pragma unroll
       for (int k = kColRS - S0 + kColG; k < 16; ++k) v[k] = 0.f;
       if (s + 1 < p.sweeps) issue(0);  // A is the same every sweep: in flight across the barrier
@@ -1045,8 +1107,14 @@ k_jacobi_cols(const __grid_constant__ ChainParams p, float *partials, unsigned *
       float res = 0.f;
       if (my_rl < R) {
         const float xn = (bi - tot) / di;  // IEEE div.rn
-        x_out[r0 + my_rl] = xn;
-        res = fabsf(xn - __ldcg(x_in + r0 + my_rl));
+        const int i = r0 + my_rl;
+        x_out[i] = xn;
+        if (p.tagged)
+          st_relaxed_u64(p.xt + (size_t)((s + 1) & 1) * kJacTaggedMaxN + i,
+                         tagged_word(xn, p.tag0 + (unsigned)s + 1));
+        // x_in[i] is this lane's own previous result once sweeps are chained
+        res = fabsf(xn - (from_tags ? xprev : __ldcg(x_in + i)));
+        xprev = xn;
       }
       if (want_resid) {
 #pragma unroll
@@ -1054,9 +1122,13 @@ k_jacobi_cols(const __grid_constant__ ChainParams p, float *partials, unsigned *
         if (lane == 0) slot[blockIdx.x] = res;
       }
     }
-    grid_sync_mono(sync + 3, (unsigned)s);  // also orders red[] reuse
-    if (want_resid && blockIdx.x == 0 && threadIdx.x < 32)
-      finish_resid(slot, gridDim.x, p.ptrs[p.idx[s][2] & 0x7f]);
+    if (want_resid || !p.tagged) {
+      grid_sync_mono(sync + 3, epoch++);  // also orders red[] reuse
+      if (want_resid && blockIdx.x == 0 && threadIdx.x < 32)
+        finish_resid(slot, gridDim.x, p.ptrs[p.idx[s][2] & 0x7f]);
+    } else {
+      __syncthreads();  // red[] reuse; the tags order everything else
+    }
   }
 }
 
@@ -1338,7 +1410,30 @@ int launch_jacobi_chain(cudaStream_t s, int dev, const JacobiChain &c, StreamScr
     if ((uint64_t)blocks > c.cov) blocks = c.cov > 0 ? (int)c.cov : 1;
     float *partials = sc->jac_partials;
     unsigned *sync = sc->jac_sync;
+    p.xt = sc->jac_xt;
+    p.tag0 = 0;
+    p.tagged = 0;
     if (use_rows && use_cols_kernel(dev, c.n, c.cov, blocks)) {
+      // a pure ping-pong run (each sweep reads the previous one's output, no
+      // in-place sweep) publishes x through tags instead of grid barriers
+      // (every row must be produced each sweep: full coverage)
+      bool chained = sc->jac_xt != nullptr && c.n <= kJacTaggedMaxN && c.cov >= (uint64_t)c.n;
+      if (const char *e = getenv("KAAS_JACOBI_TAGS"))  // dev A/B: 0 = grid barrier per sweep
+        chained = chained && e[0] != '0';
+      for (int t = done; t < done + cnt && chained; ++t)
+        chained = c.x_in[t] != c.x_out[t] && (t == done || c.x_in[t] == c.x_out[t - 1]);
+      if (chained) {
+        if (sc->jac_tag > 0x7fffffffu - (unsigned)cnt - 2u) {  // tag space wrap: start over
+          KAAS_CUDA(cudaMemsetAsync(sc->jac_xt, 0,
+                                    2 * kJacTaggedMaxN * sizeof(unsigned long long), s));
+          sc->jac_tag = 1;
+        }
+        p.tagged = 1;
+        const char *pe = getenv("KAAS_JACOBI_POLL_NS");  // dev A/B
+        p.poll_ns = pe ? atoi(pe) : 0;
+        p.tag0 = sc->jac_tag;
+        sc->jac_tag += (unsigned)cnt + 1u;
+      }
       KAAS_CUDA(cudaFuncSetAttribute((const void *)k_jacobi_cols,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kColSmem));
       KAAS_CUDA(cudaMemsetAsync(sync + 3, 0, sizeof(unsigned), s));  // monotonic barrier counter

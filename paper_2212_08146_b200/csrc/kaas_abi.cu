@@ -443,6 +443,10 @@ int kaas_stream_create(int dev, int priority, uint64_t *stream) {
   cudaError_t e = cudaMallocAsync((void **)&sc->jac_partials, 2 * kMaxJacobiBlocks * sizeof(float), s);
   if (e == cudaSuccess) e = cudaMallocAsync((void **)&sc->jac_sync, 16 * sizeof(unsigned), s);
   if (e == cudaSuccess) e = cudaMemsetAsync(sc->jac_sync, 0, 16 * sizeof(unsigned), s);
+  if (e == cudaSuccess)
+    e = cudaMallocAsync((void **)&sc->jac_xt, 2 * kJacTaggedMaxN * sizeof(unsigned long long), s);
+  if (e == cudaSuccess)
+    e = cudaMemsetAsync(sc->jac_xt, 0, 2 * kJacTaggedMaxN * sizeof(unsigned long long), s);
   // stream memory operations (cuStreamWaitValue32) target plain device memory
   if (e == cudaSuccess) e = cudaMalloc((void **)&sc->panel_done, kMaxPanels * sizeof(unsigned));
   if (e != cudaSuccess) {
@@ -473,6 +477,7 @@ int kaas_stream_destroy(uint64_t stream) {
     cudaSetDevice(sc->dev);
     if (sc->jac_partials) cudaFreeAsync(sc->jac_partials, s);
     if (sc->jac_sync) cudaFreeAsync(sc->jac_sync, s);
+    if (sc->jac_xt) cudaFreeAsync(sc->jac_xt, s);
     if (sc->cg_buf) cudaFreeAsync(sc->cg_buf, s);
     cudaStreamSynchronize(s);
     if (sc->panel_done) cudaFree(sc->panel_done);

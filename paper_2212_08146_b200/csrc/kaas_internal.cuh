@@ -35,7 +35,11 @@ struct StreamScratch {
   size_t cg_bytes = 0;
   // per-row-panel tile completion counters for progressive write-back
   unsigned *panel_done = nullptr;  // [kMaxPanels], plain cudaMalloc (stream mem-op target)
+  // Jacobi column kernel: x published as (value, tag) words, ping-pong
+  unsigned long long *jac_xt = nullptr;  // [2][kJacTaggedMaxN], zeroed at creation
+  unsigned jac_tag = 1;                  // next launch's tag base (host side, stream-ordered)
 };
+constexpr int kJacTaggedMaxN = 4096;
 constexpr int kMaxPanels = 1024;
 
 // Progressive write-back of one kernel output (see kaas_launch_batch_ex).
