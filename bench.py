@@ -401,7 +401,7 @@ def ours(args, rank, world, local_rank, dist):
                 "peak": peaks["hbm_gbs"], "peak_kind": peak_kind,
                 "frac": achieved / peaks["hbm_gbs"],
                 "traffic": profile_traffic("jacobi_sweep"),
-                "kernel": "k_jacobi_rows<chain> (500 sweeps, one cooperative launch)",
+                "kernel": "k_jacobi_cols (500 sweeps, one cooperative launch; A on chip, x via tagged words)",
                 "unit_bytes": alg_bytes, "sweep_us": sweep_s * 1e6,
                 "note": "A (64 MiB) is re-read by every sweep and stays L2-resident within a "
                         "request (L2 flushed between requests): the binding ceiling is L2->SM "

@@ -242,6 +242,7 @@ struct ChainParams {
   unsigned tag0;
   int tagged;
   int poll_ns;  // back-off between unsuccessful polls
+  unsigned *trace;  // dev: [32 sweeps][148 CTAs][3] globaltimer_lo stamps, or nullptr
 };
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
@@ -874,6 +875,11 @@ __device__ __forceinline__ ulonglong2 ld_relaxed_u64x2(const unsigned long long 
 __device__ __forceinline__ void st_relaxed_u64(unsigned long long *p, unsigned long long v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ unsigned gtimer_lo() {
+  unsigned t;
+  asm volatile("mov.u32 %0, %%globaltimer_lo;" : "=r"(t));
+  return t;
+}
 __device__ __forceinline__ unsigned long long tagged_word(float v, unsigned tag) {
   return ((unsigned long long)tag << 32) | __float_as_uint(v);
 }
@@ -986,29 +992,45 @@ k_jacobi_cols(const __grid_constant__ ChainParams p, float *partials, unsigned *
                                     : zero4();
     } else {
       // wait for this lane's 16 x values of sweep s by polling their tags:
-      // the producers' stores are the only synchronisation
+      // the producers' stores are the only synchronisation.  All chunks are
+      // polled at once (4 producers per lane: one round trip, not four).
       const unsigned want = p.tag0 + (unsigned)s;
       const unsigned long long *src = p.xt + (size_t)(s & 1) * kJacTaggedMaxN;
+      ulonglong2 q[kColC4][2];
+      unsigned pending = 0;
 #pragma unroll
-      for (int u = 0; u < kColC4; ++u) {
-        const int c4 = cbase + 32 * u;
-        if (c4 < n4) {
-          ulonglong2 q0, q1;
-          unsigned spins = 0;
-          do {
-            if (++spins > (1u << 22)) __trap();  // a lost producer: fail loudly, never hang
-            if (spins > 1 && p.poll_ns) __nanosleep(p.poll_ns);
-            q0 = ld_relaxed_u64x2(src + 4 * c4);
-            q1 = ld_relaxed_u64x2(src + 4 * c4 + 2);
-          } while ((unsigned)(q0.x >> 32) != want || (unsigned)(q0.y >> 32) != want ||
-                   (unsigned)(q1.x >> 32) != want || (unsigned)(q1.y >> 32) != want);
-          xr[u] = make_float4(__uint_as_float((unsigned)q0.x), __uint_as_float((unsigned)q0.y),
-                              __uint_as_float((unsigned)q1.x), __uint_as_float((unsigned)q1.y));
-        } else {
-          xr[u] = zero4();
+      for (int u = 0; u < kColC4; ++u)
+        if (cbase + 32 * u < n4) pending |= 1u << u;
+      unsigned spins = 0;
+      while (pending) {
+        if (++spins > (1u << 22)) __trap();  // a lost producer: fail loudly, never hang
+        if (spins > 1 && p.poll_ns) __nanosleep(p.poll_ns);
+#pragma unroll
+        for (int u = 0; u < kColC4; ++u) {
+          if (pending & (1u << u)) {
+            const int c4 = cbase + 32 * u;
+            q[u][0] = ld_relaxed_u64x2(src + 4 * c4);
+            q[u][1] = ld_relaxed_u64x2(src + 4 * c4 + 2);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kColC4; ++u) {
+          if ((pending & (1u << u)) && (unsigned)(q[u][0].x >> 32) == want &&
+              (unsigned)(q[u][0].y >> 32) == want && (unsigned)(q[u][1].x >> 32) == want &&
+              (unsigned)(q[u][1].y >> 32) == want)
+            pending &= ~(1u << u);
         }
       }
+#pragma unroll
+      for (int u = 0; u < kColC4; ++u)
+        xr[u] = cbase + 32 * u < n4
+                    ? make_float4(__uint_as_float((unsigned)q[u][0].x), __uint_as_float((unsigned)q[u][0].y),
+                                  __uint_as_float((unsigned)q[u][1].x), __uint_as_float((unsigned)q[u][1].y))
+                    : zero4();
     }
+    const bool tr = p.trace != nullptr && s >= 100 && s < 132 && threadIdx.x == 0;
+    unsigned *trp = tr ? p.trace + ((s - 100) * 148 + (blockIdx.x < 148 ? blockIdx.x : 147)) * 3 : nullptr;
+    if (tr) trp[0] = gtimer_lo();  // warp 0's x has arrived
     auto dot = [&](const float4 (&a)[kColC4]) {
       float acc = 0.f;
 #pragma unroll
@@ -1098,6 +1120,7 @@ k_jacobi_cols(const __grid_constant__ ChainParams p, float *partials, unsigned *
       mine = lane < 16 ? mine : other;
     }
     red[warp][lane] = mine;  // slot "lane"
+    if (tr) trp[1] = gtimer_lo();  // warp 0's compute done
     __syncthreads();
     float *slot = partials + (s & 1) * kMaxJacobiBlocks;
     if (warp == 0) {
@@ -1122,6 +1145,7 @@ k_jacobi_cols(const __grid_constant__ ChainParams p, float *partials, unsigned *
         if (lane == 0) slot[blockIdx.x] = res;
       }
     }
+    if (tr) trp[2] = gtimer_lo();  // rows published
     if (want_resid || !p.tagged) {
       grid_sync_mono(sync + 3, epoch++);  // also orders red[] reuse
       if (want_resid && blockIdx.x == 0 && threadIdx.x < 32)
@@ -1130,6 +1154,11 @@ k_jacobi_cols(const __grid_constant__ ChainParams p, float *partials, unsigned *
       __syncthreads();  // red[] reuse; the tags order everything else
     }
   }
+}
+
+unsigned *&jacobi_trace_buffer() {
+  static unsigned *buf = nullptr;
+  return buf;
 }
 
 bool use_cols_kernel(int dev, int n, uint64_t cov, int blocks) {
@@ -1413,6 +1442,7 @@ int launch_jacobi_chain(cudaStream_t s, int dev, const JacobiChain &c, StreamScr
     p.xt = sc->jac_xt;
     p.tag0 = 0;
     p.tagged = 0;
+    p.trace = nullptr;
     if (use_rows && use_cols_kernel(dev, c.n, c.cov, blocks)) {
       // a pure ping-pong run (each sweep reads the previous one's output, no
       // in-place sweep) publishes x through tags instead of grid barriers
@@ -1429,6 +1459,10 @@ int launch_jacobi_chain(cudaStream_t s, int dev, const JacobiChain &c, StreamScr
           sc->jac_tag = 1;
         }
         p.tagged = 1;
+        static unsigned *trace_buf = nullptr;  // dev: KAAS_JACOBI_TRACE=1 (tools/jtrace.py)
+        if (getenv("KAAS_JACOBI_TRACE") && !trace_buf) cudaMalloc((void **)&trace_buf, 32 * 148 * 3 * 4);
+        p.trace = getenv("KAAS_JACOBI_TRACE") ? trace_buf : nullptr;
+        jacobi_trace_buffer() = p.trace;
         const char *pe = getenv("KAAS_JACOBI_POLL_NS");  // dev A/B
         p.poll_ns = pe ? atoi(pe) : 0;
         p.tag0 = sc->jac_tag;
@@ -1464,3 +1498,12 @@ int launch_jacobi_chain(cudaStream_t s, int dev, const JacobiChain &c, StreamScr
 }
 
 }  // namespace kaas
+
+// dev only (not in include/kaas_b200.h): copy the last traced Jacobi chain's
+// per-CTA timestamps (KAAS_JACOBI_TRACE=1) to the host; tools/jtrace.py
+extern "C" int kaas_dev_jacobi_trace(void *host, unsigned long bytes) {
+  unsigned *buf = kaas::jacobi_trace_buffer();
+  if (!buf) return 1;
+  if (bytes > 32ul * 148 * 3 * 4) bytes = 32ul * 148 * 3 * 4;
+  return cudaMemcpy(host, buf, bytes, cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 2;
+}
