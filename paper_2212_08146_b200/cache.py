@@ -37,7 +37,7 @@ class DeviceBuffer:
     """
 
     __slots__ = ("key", "size", "is_const", "_pinned", "_dirty", "last_use",
-                 "ptr", "dev", "_cache", "_epoch", "_req", "_lends", "_ready", "_derived",
+                 "ptr", "dev", "_cache", "_epoch", "_req", "_lends", "_ready", "_derived", "_hits",
                  "__weakref__")
 
     def __init__(self, key: str | None, size: int, is_const: bool):
@@ -55,6 +55,7 @@ class DeviceBuffer:
         self._lends = []    # events of peer copies reading this buffer (peers.py)
         self._ready = None  # event recorded after the last fill (peers.py)
         self._derived = None  # kernel-prepared forms of the contents (gpu_executor.py)
+        self._hits = 0        # const cache hits since the last fill
 
     @property
     def pinned(self) -> int:

@@ -34,6 +34,8 @@ touch it is freed only after the request's streams drain.
 
 from __future__ import annotations
 
+import os
+
 from collections import OrderedDict
 from dataclasses import dataclass, field
 
@@ -232,6 +234,8 @@ class GpuExecutor:
         self._plans_by_id: _LRU = _LRU(256)     # id(req) -> (req, plan)
         self._plans_by_value: _LRU = _LRU(256)  # (buffers, invocations) -> plan
         pc = config.prepared_capacity
+        if pc is None and os.environ.get("KAAS_PREPARED_CAP"):  # dev A/B
+            pc = int(os.environ["KAAS_PREPARED_CAP"])
         self._prep_cap = 4 * config.capacity if pc is None else pc
         self._prep_bytes = 0
 
@@ -259,14 +263,14 @@ class GpuExecutor:
         ptr, buf.ptr = buf.ptr, 0
         self._free_after_user(buf, ptr)
 
-    def _free_after_user(self, buf: DeviceBuffer, ptr: int) -> None:
+    def _free_after_user(self, buf: DeviceBuffer, ptr: int, stream=None) -> None:
         owner = self._inflight.get(buf._req)
         if owner is None and self._cur is not None and buf._req == self._cur.seq:
             owner = self._cur
         if owner is not None:
-            owner.graveyard.append(ptr)
+            owner.graveyard.append(ptr)  # freed on s_exec when the owner completes
         else:
-            native.free_async(self.s_in, ptr)
+            native.free_async(self.s_in if stream is None else stream, ptr)
 
     # -- prepared operands ------------------------------------------------------
     # cGEMM's 3xTF32 split of A and split + 4M expansion + transpose of B are
@@ -275,23 +279,29 @@ class GpuExecutor:
     # entry's contents (fill, kernel write, eviction); decisions are unaffected.
 
     def _clear_derived(self, buf: DeviceBuffer) -> None:
+        buf._hits = 0
         d = buf._derived
         if not d:
             return
         buf._derived = None
         for ptr, nbytes, _ in d.values():
             self._prep_bytes -= nbytes
-            self._free_after_user(buf, ptr)
+            # allocated and used on s_exec: free there too, so the pool can
+            # hand the block straight to the next prepared operand
+            self._free_after_user(buf, ptr, self.s_exec)
 
     def _derived_slot(self, buf: DeviceBuffer, key, nbytes: int):
         """-> [ptr, nbytes, ready] for ``key`` on ``buf``, allocating (on the
-        exec stream) within the prepared-operand budget; None when over it."""
+        exec stream) within the prepared-operand budget; None when over it or
+        when ``buf`` has not been reused yet."""
         d = buf._derived
         if d is not None:
             hit = d.get(key)
             if hit is not None:
                 return hit
-        if self._prep_bytes + nbytes > self._prep_cap:
+        # promote on reuse: an operand seen once (a cold fetch, or churn under
+        # eviction) keeps using scratch; the first cache hit prepares it
+        if buf._hits == 0 or self._prep_bytes + nbytes > self._prep_cap:
             return None
         slot = [native.malloc_async(self.s_exec, nbytes), nbytes, False]
         self._prep_bytes += nbytes
@@ -345,6 +355,7 @@ class GpuExecutor:
                         f"buffer {arg.name!r}: cached object under {arg.key!r} is"
                         f" {cached.size} bytes, request declares {arg.size}")
                 stats.cache_hits += 1
+                cached._hits += 1
                 cache.pin(cached)
                 cache.touch(cached)
                 cached.is_const = True
