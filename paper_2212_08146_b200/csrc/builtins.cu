@@ -115,26 +115,32 @@ __global__ void k_reduce_sum(uint64_t n, const float *x, float *out) {
 
 // ---- matmul: per cell acc = 0; acc = fl(acc + fl(a*b)), k ascending --------
 // (backend.py:174-189, oracle pkg/tests/oracles.py:25-33).  Bit-exactness
-// forbids split-K, so all parallelism comes from output cells: 256 threads
-// (16 x 16) each own TM x TN cells of a (16*TM) x (16*TN) tile.  The tile
-// shape is picked per launch so small-M / long-K layers (ResNet stage 4:
-// M = 49, K = 4608) still fill the SMs, while big layers get 4x4 blocking.
+// forbids split-K and FMA, so each MAC is an FMUL + FADD (the SIMT roofline
+// is 64 MAC/clk/SM) and all parallelism comes from output cells.  A CTA of
+// TY x TX threads owns a (TY*TM) x (TX*TN) tile, each thread a TM x TN block
+// of cells.  The shape is picked per launch by a small cost model
+// (launch_matmul): big layers get 4x4 blocking, small-M / long-K layers
+// (ResNet stage 4: M = 49, K = 4608) get small CTAs of 1x1 or 2x2 blocks so
+// every scheduler has warps.
 //
 // Operands stream through an S-deep ring of BK = 32 k-chunks filled by
-// cp.async (4-byte copies, zero-filled out of bounds, so any shape and
-// alignment works): S-1 chunks of loads are in flight behind the chunk being
-// computed, which is what long-K layers need -- a 2-deep ring pays the full
-// L2/HBM latency once per chunk.  A tiles are row-major in smem (k
-// contiguous, rows padded to 36 floats) so a thread reads 4 k of a row with
-// one LDS.128; a thread owns TN contiguous columns of B, read as one vector.
-// Padding products are never added (0*Inf would be NaN and +0 would flip
-// the sign of a -0.0 accumulator), so the tail chunk uses the true extent.
-constexpr int MM_BK = 32, MM_LDA = MM_BK + 4;
+// cp.async (zero-filled out of bounds).  Both tiles are stored k-contiguous
+// in smem (A row-major, B transposed, rows padded to 36 floats), so a thread
+// reads 4 k of each of its rows and columns with one LDS.128: per 4 k that
+// is TM + TN loads for 8 TM TN FP instructions.  A is copied 16 bytes at a
+// time when K and the pointer allow it.  Padding products are never added
+// (0*Inf would be NaN and +0 would flip the sign of a -0.0 accumulator), so
+// the tail chunk uses the true extent.
 
 __device__ __forceinline__ void cp_async4(float *dst, const float *src, bool ok) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(src),
                "r"(ok ? 4 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async16(float *dst, const float *src, int bytes) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(bytes)
                : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
@@ -143,54 +149,105 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-template <int TN>
-__device__ __forceinline__ void lds_vec(const float *p, float (&v)[TN]) {
-  if constexpr (TN == 4) {
-    const float4 t = *reinterpret_cast<const float4 *>(p);
-    v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
-  } else if constexpr (TN == 2) {
-    const float2 t = *reinterpret_cast<const float2 *>(p);
-    v[0] = t.x; v[1] = t.y;
-  } else {
-#pragma unroll
-    for (int j = 0; j < TN; ++j) v[j] = p[j];
-  }
-}
 
-template <int TM, int TN, int S>
+template <int TY, int TX, int TM, int TN, int S, int BK>
 constexpr int mm_smem_bytes() {
-  return S * (16 * TM * MM_LDA + MM_BK * 16 * TN) * 4;
+  return S * (TY * TM + TX * TN) * (BK + 4) * 4;
 }
 
-template <int TM, int TN, int S>
-__global__ void __launch_bounds__(256)
+template <int TY, int TX, int TM, int TN, int S, int BK, bool AV>
+__global__ void __launch_bounds__(TY *TX)
 k_matmul(int n, int m, int k, uint64_t cov, const float *__restrict__ a,
          const float *__restrict__ b, float *__restrict__ out) {
-  constexpr int BM = 16 * TM, BN = 16 * TN;
-  constexpr int A_ST = BM * MM_LDA, B_ST = MM_BK * BN;
+  constexpr bool a_vec = AV;  // 16-byte A copies (k % 4 == 0, a 16-byte aligned)
+  constexpr int T = TY * TX, BM = TY * TM, BN = TX * TN, LD = BK + 4;
+  constexpr int A_ST = BM * LD, B_ST = BN * LD;
+  constexpr int NA4 = (BM * (BK / 4) + T - 1) / T;  // 16-byte A copies per thread
+  constexpr int NA1 = (BM * BK + T - 1) / T;        // 4-byte A copies per thread
+  static_assert(BM * BK % T == 0 && BK * BN % T == 0, "copy slots must tile the chunk");
+  constexpr int NB = (BK * BN + T - 1) / T;         // 4-byte B copies per thread
   extern __shared__ __align__(16) float mm_smem[];
   float *As = mm_smem, *Bs = mm_smem + S * A_ST;
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
   const int bm = blockIdx.y * BM, bn = blockIdx.x * BN;
-  const int nk = (k + MM_BK - 1) / MM_BK;
+  const int nk = (k + BK - 1) / BK;
 
+  // Per-thread copy slots, fixed across chunks: a running source pointer
+  // (advanced by one chunk per issue), the smem offset, and the row/column
+  // validity.  Only the tail chunk checks k per element.
+  constexpr int NA = AV ? NA4 : NA1;
+  const float *pa[NA];
+  int sa[NA], ka[NA], ba[NA];  // smem offset, k offset in chunk (-1 unused), copy bytes
+  size_t step_a[NA];
+#pragma unroll
+  for (int u = 0; u < NA; ++u) {
+    const int e = threadIdx.x + T * u;
+    const int r = AV ? e / (BK / 4) : e / BK;
+    const int kk = AV ? 4 * (e % (BK / 4)) : e % BK;
+    const bool used = r < BM;
+    const bool ok = used && bm + r < n;
+    ka[u] = used ? kk : -1;
+    sa[u] = used ? r * LD + kk : 0;
+    ba[u] = ok ? (AV ? 16 : 4) : 0;
+    pa[u] = ok ? a + (size_t)(bm + r) * k + kk : a;
+    step_a[u] = ok ? BK : 0;
+  }
+  const float *pb[NB];
+  int sb[NB], kb[NB], bb[NB];
+  size_t step_b[NB];
+#pragma unroll
+  for (int u = 0; u < NB; ++u) {
+    const int e = threadIdx.x + T * u;
+    const int kk = e / BN, c = e % BN;
+    const bool used = kk < BK;
+    const bool ok = used && bn + c < m;
+    kb[u] = used ? kk : -1;
+    sb[u] = used ? c * LD + kk : 0;  // B[k0 + kk][bn + c] -> Bs[c][kk]
+    bb[u] = ok ? 4 : 0;
+    pb[u] = ok ? b + (size_t)kk * m + bn + c : b;
+    step_b[u] = ok ? (size_t)BK * m : 0;
+  }
+  int stage_in = 0;  // stage the next issue() fills
   auto issue = [&](int t) {
-    const int k0 = t * MM_BK;
-    float *as = As + (t % S) * A_ST, *bs = Bs + (t % S) * B_ST;
+    const int k0 = t * BK;
+    float *as = As + stage_in * A_ST, *bs = Bs + stage_in * B_ST;
+    stage_in = stage_in + 1 == S ? 0 : stage_in + 1;
+    if (k0 + BK <= k) {  // full chunk: fixed per-slot sizes
 #pragma unroll
-    for (int u = 0; u < BM * MM_BK / 256; ++u) {
-      const int e = threadIdx.x + 256 * u;
-      const int r = e / MM_BK, kk = e % MM_BK;
-      const bool ok = bm + r < n && k0 + kk < k;
-      cp_async4(as + r * MM_LDA + kk, ok ? a + (size_t)(bm + r) * k + k0 + kk : a, ok);
+      for (int u = 0; u < NA; ++u) {
+        if (BM * (AV ? BK / 4 : BK) % T != 0 && ka[u] < 0) continue;
+        if (AV) cp_async16(as + sa[u], pa[u], ba[u]);
+        else cp_async4(as + sa[u], pa[u], ba[u] != 0);
+      }
+#pragma unroll
+      for (int u = 0; u < NB; ++u) {
+        if (BK * BN % T != 0 && kb[u] < 0) continue;
+        cp_async4(bs + sb[u], pb[u], bb[u] != 0);
+      }
+    } else {  // tail chunk: k bound per element
+#pragma unroll
+      for (int u = 0; u < NA; ++u) {
+        if (ka[u] < 0) continue;
+        const int left = k - (k0 + ka[u]);
+        if (AV) {
+          const int bytes = (ba[u] && left > 0) ? (left >= 4 ? 16 : 4 * left) : 0;
+          cp_async16(as + sa[u], bytes ? pa[u] : a, bytes);
+        } else {
+          const bool ok = ba[u] && left > 0;
+          cp_async4(as + sa[u], ok ? pa[u] : a, ok);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < NB; ++u) {
+        if (kb[u] < 0) continue;
+        const bool ok = bb[u] && k0 + kb[u] < k;
+        cp_async4(bs + sb[u], ok ? pb[u] : b, ok);
+      }
     }
 #pragma unroll
-    for (int u = 0; u < MM_BK * BN / 256; ++u) {
-      const int e = threadIdx.x + 256 * u;
-      const int kk = e / BN, c = e % BN;
-      const bool ok = bn + c < m && k0 + kk < k;
-      cp_async4(bs + kk * BN + c, ok ? b + (size_t)(k0 + kk) * m + bn + c : b, ok);
-    }
+    for (int u = 0; u < NA; ++u) pa[u] += step_a[u];
+#pragma unroll
+    for (int u = 0; u < NB; ++u) pb[u] += step_b[u];
   };
 
   float acc[TM][TN];
@@ -209,36 +266,40 @@ k_matmul(int n, int m, int k, uint64_t cov, const float *__restrict__ a,
     __syncthreads();  // chunk t landed; everyone is done with chunk t-1's stage
     if (t + S - 1 < nk) issue(t + S - 1);
     cp_async_commit();
-    const float *as = As + (t % S) * A_ST + ty * TM * MM_LDA;
-    const float *bs = Bs + (t % S) * B_ST + tx * TN;
-    const int kc = min(MM_BK, k - t * MM_BK);
-    if (kc == MM_BK) {
+    // thread (ty, tx) owns rows ty + TY*i and columns tx + TX*j: each LDS.128
+    // of a warp then hits consecutive rows (4-bank steps), conflict-free
+    const float *as = As + (t % S) * A_ST + ty * LD;
+    const float *bs = Bs + (t % S) * B_ST + tx * LD;
+    const int kc = min(BK, k - t * BK);
+    if (kc == BK) {
 #pragma unroll
-      for (int k4 = 0; k4 < MM_BK; k4 += 4) {
-        float4 av[TM];
+      for (int k4 = 0; k4 < BK; k4 += 4) {
+        float4 av[TM], bv[TN];
 #pragma unroll
-        for (int i = 0; i < TM; ++i) av[i] = *reinterpret_cast<const float4 *>(as + i * MM_LDA + k4);
+        for (int i = 0; i < TM; ++i) av[i] = *reinterpret_cast<const float4 *>(as + i * TY * LD + k4);
+#pragma unroll
+        for (int j = 0; j < TN; ++j) bv[j] = *reinterpret_cast<const float4 *>(bs + j * TX * LD + k4);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          float bv[TN];
-          lds_vec<TN>(bs + (k4 + q) * BN, bv);
 #pragma unroll
           for (int i = 0; i < TM; ++i) {
             const float x = q == 0 ? av[i].x : q == 1 ? av[i].y : q == 2 ? av[i].z : av[i].w;
 #pragma unroll
-            for (int j = 0; j < TN; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(x, bv[j]));
+            for (int j = 0; j < TN; ++j) {
+              const float y = q == 0 ? bv[j].x : q == 1 ? bv[j].y : q == 2 ? bv[j].z : bv[j].w;
+              acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(x, y));
+            }
           }
         }
       }
     } else {
       for (int kk = 0; kk < kc; ++kk) {
-        float bv[TN];
-        lds_vec<TN>(bs + kk * BN, bv);
 #pragma unroll
         for (int i = 0; i < TM; ++i) {
-          const float x = as[i * MM_LDA + kk];
+          const float x = as[i * TY * LD + kk];
 #pragma unroll
-          for (int j = 0; j < TN; ++j) acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(x, bv[j]));
+          for (int j = 0; j < TN; ++j)
+            acc[i][j] = __fadd_rn(acc[i][j], __fmul_rn(x, bs[j * TX * LD + kk]));
         }
       }
     }
@@ -246,11 +307,11 @@ k_matmul(int n, int m, int k, uint64_t cov, const float *__restrict__ a,
   cp_async_wait<0>();
 #pragma unroll
   for (int i = 0; i < TM; ++i) {
-    const int r = bm + ty * TM + i;
+    const int r = bm + ty + TY * i;
     if (r >= n) continue;
 #pragma unroll
     for (int j = 0; j < TN; ++j) {
-      const int c = bn + tx * TN + j;
+      const int c = bn + tx + TX * j;
       if (c >= m) continue;
       const uint64_t g = (uint64_t)r * m + c;
       if (g < cov) out[g] = acc[i][j];
@@ -287,42 +348,70 @@ int launch_matmul(cudaStream_t s, int dev, uint64_t n, uint64_t m, uint64_t k, u
   if (n == 0 || m == 0 || cov == 0) return 0;
   if (n > 0x7fffffffu || m > 0x7fffffffu || k > 0x7fffffffu)
     return fail(KAAS_E_INVALID, "matmul extent exceeds i32");
-  // largest register tile that still gives >= 2 CTAs per SM
-  const uint64_t want = 2ull * device_props(dev).sm_count;
-  auto ctas = [&](int tm, int tn) {
-    return ((n + 16 * tm - 1) / (16 * tm)) * ((m + 16 * tn - 1) / (16 * tn));
-  };
-  int tm = 1, tn = 1;
-  const int cand[][2] = {{4, 4}, {2, 4}, {4, 2}, {2, 2}, {1, 2}, {2, 1}};
-  for (auto &c : cand) {
-    if (ctas(c[0], c[1]) >= want) {
-      tm = c[0];
-      tn = c[1];
-      break;
+  // Cost model: a config's rate ~ (warps it can field, up to 2 per
+  // scheduler) x (useful fraction of its tiles) / (instructions per MAC:
+  // 2 FP + (TM + TN) / 4 LDS.128 per k + ~0.5 copy/loop overhead, per cell).
+  struct Cfg { int ty, tx, tm, tn; };
+  static const Cfg cfgs[] = {{16, 16, 4, 4}, {16, 16, 2, 4}, {16, 16, 4, 2}, {16, 16, 2, 2},
+                             {8, 16, 2, 2},  {16, 8, 2, 2},  {8, 8, 2, 2},   {8, 8, 1, 2},
+                             {8, 8, 2, 1},   {8, 8, 1, 1}};
+  const int sms = device_props(dev).sm_count;
+  const double want_warps = 8.0 * sms;
+  int best = 0;
+  double best_score = -1.0;
+  for (int i = 0; i < (int)(sizeof(cfgs) / sizeof(cfgs[0])); ++i) {
+    const Cfg &c = cfgs[i];
+    const uint64_t tbm = (uint64_t)c.ty * c.tm, tbn = (uint64_t)c.tx * c.tn;
+    const uint64_t gy = (n + tbm - 1) / tbm, gx = (m + tbn - 1) / tbn;
+    if (gy > 65535) continue;
+    const double warps = (double)(gy * gx) * (c.ty * c.tx / 32.0);
+    const double useful = (double)(n * m) / (double)(gy * tbm * gx * tbn);
+    const double cells = c.tm * c.tn;
+    const double ipm = (2.0 * cells + (c.tm + c.tn) / 4.0 + 0.5) / cells;
+    const double score = (warps < want_warps ? warps : want_warps) * useful / ipm;
+    if (score > best_score * 1.02) {  // ties -> the larger tile (earlier)
+      best_score = score;
+      best = i;
     }
   }
-  const uint64_t gy = (n + 16 * tm - 1) / (16 * tm), gx = (m + 16 * tn - 1) / (16 * tn);
-  if (gy > 65535) return fail(KAAS_E_INVALID, "matmul: n too large for grid.y");
-  dim3 grid((unsigned)gx, (unsigned)gy);
-#define MM_LAUNCH(TM, TN)                                                               \
-  do {                                                                                  \
-    constexpr int S_ = (TM) * (TN) >= 8 ? 4 : 8;                                        \
-    constexpr int SM_ = mm_smem_bytes<TM, TN, S_>();                                    \
-    static std::atomic<uint64_t> attr_done{0}; /* per device (dev < 64) */               \
-    if (!(attr_done.load(std::memory_order_relaxed) >> (dev & 63) & 1)) {               \
-      KAAS_CUDA(cudaFuncSetAttribute(k_matmul<TM, TN, S_>,                              \
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, SM_)); \
-      attr_done.fetch_or(1ull << (dev & 63));                                           \
-    }                                                                                   \
-    k_matmul<TM, TN, S_><<<grid, 256, SM_, s>>>((int)n, (int)m, (int)k, cov, a, b, out); \
+  if (best_score < 0) return fail(KAAS_E_INVALID, "matmul: n too large for grid.y");
+  const Cfg &c = cfgs[best];
+  const unsigned gy = (unsigned)((n + c.ty * c.tm - 1) / (c.ty * c.tm));
+  const unsigned gx = (unsigned)((m + c.tx * c.tn - 1) / (c.tx * c.tn));
+  dim3 grid(gx, gy);
+  const int a_vec = (k % 4 == 0) && aligned16(a);
+#define MM_LAUNCH(TY, TX, TM, TN)                                                          \
+  do {                                                                                     \
+    constexpr int S_ = (TM) * (TN) >= 8 ? 4 : (TM) * (TN) >= 4 ? 6 : 8;                    \
+    constexpr int BK_ = (TM) * (TN) <= 2 ? 64 : 32;                                        \
+    constexpr int SM_ = mm_smem_bytes<TY, TX, TM, TN, S_, BK_>();                          \
+    static std::atomic<uint64_t> attr_done{0}; /* per device (dev < 64) */                  \
+    if (!(attr_done.load(std::memory_order_relaxed) >> (dev & 63) & 1)) {                  \
+      KAAS_CUDA(cudaFuncSetAttribute(k_matmul<TY, TX, TM, TN, S_, BK_, true>,              \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, SM_));    \
+      KAAS_CUDA(cudaFuncSetAttribute(k_matmul<TY, TX, TM, TN, S_, BK_, false>,             \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, SM_));    \
+      attr_done.fetch_or(1ull << (dev & 63));                                              \
+    }                                                                                      \
+    if (a_vec)                                                                             \
+      k_matmul<TY, TX, TM, TN, S_, BK_, true><<<grid, (TY) * (TX), SM_, s>>>(              \
+          (int)n, (int)m, (int)k, cov, a, b, out);                                         \
+    else                                                                                   \
+      k_matmul<TY, TX, TM, TN, S_, BK_, false><<<grid, (TY) * (TX), SM_, s>>>(             \
+          (int)n, (int)m, (int)k, cov, a, b, out);                                         \
   } while (0)
-  if (tm == 4 && tn == 4) MM_LAUNCH(4, 4);
-  else if (tm == 2 && tn == 4) MM_LAUNCH(2, 4);
-  else if (tm == 4 && tn == 2) MM_LAUNCH(4, 2);
-  else if (tm == 2 && tn == 2) MM_LAUNCH(2, 2);
-  else if (tm == 1 && tn == 2) MM_LAUNCH(1, 2);
-  else if (tm == 2 && tn == 1) MM_LAUNCH(2, 1);
-  else MM_LAUNCH(1, 1);
+  switch (best) {
+    case 0: MM_LAUNCH(16, 16, 4, 4); break;
+    case 1: MM_LAUNCH(16, 16, 2, 4); break;
+    case 2: MM_LAUNCH(16, 16, 4, 2); break;
+    case 3: MM_LAUNCH(16, 16, 2, 2); break;
+    case 4: MM_LAUNCH(8, 16, 2, 2); break;
+    case 5: MM_LAUNCH(16, 8, 2, 2); break;
+    case 6: MM_LAUNCH(8, 8, 2, 2); break;
+    case 7: MM_LAUNCH(8, 8, 1, 2); break;
+    case 8: MM_LAUNCH(8, 8, 2, 1); break;
+    default: MM_LAUNCH(8, 8, 1, 1); break;
+  }
 #undef MM_LAUNCH
   count_launch();
   KAAS_CUDA(cudaGetLastError());
