@@ -194,9 +194,17 @@ def measure_cgemm(n, steps, device, cold_too):
     from paper_2212_08146_b200.pool import KaasService
     store = PinnedStore()
     W.seed_cgemm(store, n, prefix="cg")
+    if cold_too:  # cold = not in the device cache; the host objects exist up front
+        for c in range(2):
+            W.seed_cgemm(store, n, prefix=f"cold{c}", seed=100 + c)
     out = {"workload": f"cgemm {n}x{n}x{n} complex64, A/B const, C flushed, single client"}
     cap = 16 * n * n * 8
-    with KaasService(store, n_executors=1, capacity=cap, policy="rr", devices=[device]) as svc:
+    # the server maps its cache memory at start-up (ledger + prepared operands
+    # of one A/B pair + the cGEMM scratch); cold requests then pay for data
+    # movement and compute, not for growing the device pool
+    reserve = cap + 8 * 8 * n * n
+    with KaasService(store, n_executors=1, capacity=cap, policy="rr", devices=[device],
+                     reserve_bytes=reserve) as svc:
         ex = svc.executors[0]
 
         def req(i, pfx="cg"):
@@ -211,7 +219,6 @@ def measure_cgemm(n, steps, device, cold_too):
         if cold_too:
             colds, cold_dev, h2d_ms = [], [], []
             for c in range(2):
-                W.seed_cgemm(store, n, prefix=f"cold{c}", seed=100 + c)
                 h0 = ex.dev_stats.h2d_ms
                 t = time.perf_counter()
                 r = svc.submit(req(0, pfx=f"cold{c}"))

@@ -36,7 +36,8 @@ class KaasService:
                  policy="affinity:8", timing: TimingModel | None = None,
                  digest_cap: int = 1024, strict_schema: bool = False, debug: bool = False,
                  devices: list[int] | None = None, executor_factory=None,
-                 log_decisions: bool = False, max_inflight: int = 3, peer_fills: bool = True):
+                 log_decisions: bool = False, max_inflight: int = 3, peer_fills: bool = True,
+                 reserve_bytes: int = 0):
         if executor_factory is None:
             devices = devices if devices is not None else visible_devices()
             if not devices:
@@ -53,7 +54,8 @@ class KaasService:
         if executor_factory is None:
             def executor_factory(i):
                 cfg = ExecutorConfig(capacity=capacity, timing=self.timing, executor_id=i,
-                                     debug=debug, device=devices[i % len(devices)])
+                                     debug=debug, device=devices[i % len(devices)],
+                                     reserve_bytes=reserve_bytes)
                 return GpuExecutor(cfg, store, GpuBackend(timing=self.timing))
         self.executors = [executor_factory(i) for i in range(n_executors)]
         # peer fills between this pool's executors (NVLink across GPUs, D2D on one)
