@@ -104,3 +104,26 @@ def test_http_front_end_over_gpu_pool(cuda):
         srv.shutdown()
         srv.server_close()
         svc.close()
+
+
+def test_gpu_report_v2_over_http(cuda):
+    """Report v2 through the HTTP front end over the GPU pool: the v1 fields
+    are the reference's (modulo the over_http flag) and every GPU executor's
+    device measurements are attached."""
+    golden = load_golden("routing.json.gz")["bench_matmul_chain"]
+    spec = WorkloadSpec("matmul_chain", 6, matrix_dim=16, seed=5)
+
+    def factory(store, policy):
+        return KaasService(store, n_executors=2, capacity=default_capacity(spec), policy=policy,
+                           devices=[0])
+
+    rep = run_bench(spec, ["rr"], n_executors=2, warm_repeat=True, over_http="127.0.0.1:0",
+                    version=2, service_factory=factory, store_factory=PinnedStore)
+    rep = json.loads(report_json(rep))
+    meas = rep.pop("measured")
+    assert rep.pop("report_version") == 2 and rep.pop("over_http") is True
+    g = dict(golden)
+    g.pop("report_version"), g.pop("over_http")
+    assert rep == g
+    devs = meas["rr"]["devices"]
+    assert len(devs) == 2 and all(d["kernel_launches"] > 0 for d in devs)

@@ -103,3 +103,34 @@ def test_multi_client_service_completes_and_balances():
     for policy, entry in rep["policies"].items():
         assert entry["requests"] == 800 and entry["errors"] == 0, policy
         assert sum(entry["per_executor_requests"]) == 800
+
+
+def test_report_over_http_and_v2():
+    """The v1 report through the HTTP front end (reference ``--over-http``)
+    equals the golden report except for the ``over_http`` flag; v2 keeps
+    every v1 field and adds the measurements."""
+    golden = load_golden("routing.json.gz")["bench_matmul_chain"]
+    spec = WorkloadSpec("matmul_chain", 6, matrix_dim=16, seed=5)
+    from paper_2212_08146_b200.workloads import default_capacity
+    capacity = default_capacity(spec)
+    rep = run_bench(spec, ["rr"], n_executors=2, warm_repeat=True, over_http="127.0.0.1:0",
+                    service_factory=oracle_service(2, capacity))
+    rep = _strip(rep)
+    assert rep.pop("over_http") is True
+    g = dict(golden)
+    assert g.pop("over_http") is False
+    assert rep == g
+    v2 = run_bench(spec, ["rr"], n_executors=2, warm_repeat=True, version=2,
+                   service_factory=oracle_service(2, capacity))
+    v2 = json.loads(report_json(v2))
+    meas = v2.pop("measured")
+    assert v2.pop("report_version") == 2 and meas["rr"]["req_per_s"] > 0
+    g2 = dict(golden)
+    g2.pop("report_version")
+    assert v2 == g2
+
+
+def test_bench_cli_validates_like_the_reference(capsys):
+    from paper_2212_08146_b200.benchlib import bench_main
+    assert bench_main(["run", "--workload", "mixed", "--requests", "0"]) == 2
+    assert "invalid workload" in capsys.readouterr().err
