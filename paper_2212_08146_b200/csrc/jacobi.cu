@@ -242,6 +242,7 @@ struct ChainParams {
   unsigned tag0;
   int tagged;
   int poll_ns;  // back-off between unsuccessful polls
+  unsigned zero;  // always 0: an opaque value ptxas cannot fold (k_jacobi_tmem)
   unsigned *trace;  // dev: [32 sweeps][148 CTAs][3] globaltimer_lo stamps, or nullptr
 };
 
@@ -1156,6 +1157,302 @@ k_jacobi_cols(const __grid_constant__ ChainParams p, float *partials, unsigned *
   }
 }
 
+// ---- TMEM-tier kernel: the whole band of A on chip (n <= 4096) -----------------
+//
+// Same thread layout, reduction and tagged exchange as k_jacobi_cols, but the
+// band's 28 rows never leave the SM after the first sweep:
+//   rows 0..15   tensor memory (each thread owns 256 of its TMEM lane's 512
+//                columns: warps w and w+4 share lane quadrant w%4), read back
+//                with tcgen05.ld.32x32b.x16 -- one row's 16 floats per load
+//   rows 16..21  registers
+//   rows 22..27  thread-private shared memory (LDS.128, conflict-free)
+// Measured on B200 (tools/tmembw.cu): tcgen05.ld streams ~425 B/clk/SM, 3.3x
+// the 128 B/clk LDS path, and the two overlap, so a sweep's 458 KB per SM
+// costs ~1,000 cycles instead of the L2 tier's ~2 us.  Nothing is re-read
+// from L2 or HBM after the fill.
+constexpr int kTmRT = 16;   // TMEM rows
+constexpr int kTmRR = 6;    // register rows
+constexpr int kTmRS = 6;    // shared-memory rows
+static_assert(kTmRT + kTmRR + kTmRS == kColRows, "row tiers must cover the band");
+constexpr int kTmBatch = 1;  // TMEM rows per tcgen05.ld batch
+constexpr int kTmDep = 3;    // batches in flight (each waits on the dots kTmDep batches back)
+// padded so no other 1-CTA/SM kernel that allocates TMEM can be co-resident
+constexpr size_t kTmTier = (size_t)kTmRS * kColC4 * kColT * sizeof(float4);
+constexpr size_t kTmSmem = kTmTier > 116 * 1024 ? kTmTier : 116 * 1024;
+
+#define KAAS_TMEM_LD16(taddr, v)                                                               \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 "                                      \
+               "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"             \
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),     \
+                 "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),   \
+                 "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])                          \
+               : "r"(taddr))
+#define KAAS_TMEM_ST16(taddr, v)                                                               \
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "                                \
+               "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),    \
+               "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]),  \
+               "r"(v[7]), "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]),          \
+               "r"(v[13]), "r"(v[14]), "r"(v[15])                                           \
+               : "memory")
+
+// volatile so ptxas keeps the smem tier's loads where they are written
+// instead of hoisting the whole tier into registers at the top of the sweep
+__device__ __forceinline__ float4 lds4(const float4 *q) {
+  float4 a;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w)
+               : "r"((uint32_t)__cvta_generic_to_shared(q)));
+  return a;
+}
+
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(kColT, 1)
+k_jacobi_tmem(const __grid_constant__ ChainParams p, float *partials, unsigned *sync) {
+  extern __shared__ __align__(16) float4 acache[];  // [kTmRS][kColC4][kColT]
+  __shared__ float red[kColW][32];
+  __shared__ uint32_t tmem_base;
+  const int n = p.n, n4 = n >> 2;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  int r0, r1;
+  band(p.cov, r0, r1);
+  const int R = r1 - r0;
+  const uint64_t pol = l2_policy(false);  // A is read once per launch
+  const int cbase = warp * 32 * kColC4 + lane;
+  const bool full = cbase + 32 * (kColC4 - 1) < n4;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&tmem_base)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t taddr = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(warp >> 2) * 256u;
+
+  // A[r0 + rl][cbase + 32u] with the diagonal zeroed; rows past the band and
+  // columns past n are 0 (their partials are discarded / contribute nothing)
+  auto lda = [&](int rl, int u) -> float4 {
+    float4 a = zero4();
+    if (rl >= R) return a;
+    const float4 *rp = reinterpret_cast<const float4 *>(p.A) + (size_t)(r0 + rl) * n4 + cbase;
+    if (full || cbase + 32 * u < n4) a = ld_a(reinterpret_cast<const float *>(rp + 32 * u), pol);
+    const int c4 = cbase + 32 * u, i = r0 + rl;
+    if (c4 == (i >> 2)) {
+      const int d = i & 3;
+      a.x = d == 0 ? 0.f : a.x;
+      a.y = d == 1 ? 0.f : a.y;
+      a.z = d == 2 ? 0.f : a.z;
+      a.w = d == 3 ? 0.f : a.w;
+    }
+    return a;
+  };
+  // fill the three tiers once per launch
+#pragma unroll 1
+  for (int r = 0; r < kTmRT; ++r) {
+    uint32_t v[16];
+#pragma unroll
+    for (int u = 0; u < kColC4; ++u) {
+      const float4 a = lda(r, u);
+      v[4 * u + 0] = __float_as_uint(a.x);
+      v[4 * u + 1] = __float_as_uint(a.y);
+      v[4 * u + 2] = __float_as_uint(a.z);
+      v[4 * u + 3] = __float_as_uint(a.w);
+    }
+    KAAS_TMEM_ST16(taddr + 16u * r, v);
+  }
+  float4 areg[kTmRR][kColC4];
+#pragma unroll
+  for (int r = 0; r < kTmRR; ++r)
+#pragma unroll
+    for (int u = 0; u < kColC4; ++u) areg[r][u] = lda(kTmRT + r, u);
+#pragma unroll 1
+  for (int r = 0; r < kTmRS; ++r)
+#pragma unroll
+    for (int u = 0; u < kColC4; ++u) acache[(r * kColC4 + u) * kColT + tid] = lda(kTmRT + kTmRR + r, u);
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+
+  // reduction slot l holds band row l (slots 28..31 empty)
+  const int my_rl = lane;
+  float bi = 0.f, di = 1.f;
+  if (warp == 0 && my_rl < R) {
+    bi = __ldg(p.b + r0 + my_rl);
+    di = __ldg(p.A + (size_t)(r0 + my_rl) * n + r0 + my_rl);
+  }
+
+  float xprev = 0.f;
+  unsigned epoch = 0;
+  for (int s = 0; s < p.sweeps; ++s) {
+    const float *x_in = p.ptrs[p.idx[s][0]];
+    float *x_out = p.ptrs[p.idx[s][1]];
+    const bool want_resid = (p.idx[s][2] & 0x80) != 0;
+    const bool from_tags = p.tagged && s > 0;
+    float4 xr[kColC4];
+    if (!from_tags) {
+#pragma unroll
+      for (int u = 0; u < kColC4; ++u)
+        xr[u] = cbase + 32 * u < n4 ? __ldcg(reinterpret_cast<const float4 *>(x_in) + cbase + 32 * u)
+                                    : zero4();
+    } else {
+      const unsigned want = p.tag0 + (unsigned)s;
+      const unsigned long long *src = p.xt + (size_t)(s & 1) * kJacTaggedMaxN;
+      ulonglong2 q[kColC4][2];
+      unsigned pending = 0;
+#pragma unroll
+      for (int u = 0; u < kColC4; ++u)
+        if (cbase + 32 * u < n4) pending |= 1u << u;
+      unsigned spins = 0;
+      while (pending) {
+        if (++spins > (1u << 22)) __trap();  // a lost producer: fail loudly, never hang
+        if (spins > 1 && p.poll_ns) __nanosleep(p.poll_ns);
+#pragma unroll
+        for (int u = 0; u < kColC4; ++u) {
+          if (pending & (1u << u)) {
+            const int c4 = cbase + 32 * u;
+            q[u][0] = ld_relaxed_u64x2(src + 4 * c4);
+            q[u][1] = ld_relaxed_u64x2(src + 4 * c4 + 2);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kColC4; ++u) {
+          if ((pending & (1u << u)) && (unsigned)(q[u][0].x >> 32) == want &&
+              (unsigned)(q[u][0].y >> 32) == want && (unsigned)(q[u][1].x >> 32) == want &&
+              (unsigned)(q[u][1].y >> 32) == want)
+            pending &= ~(1u << u);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kColC4; ++u)
+        xr[u] = cbase + 32 * u < n4
+                    ? make_float4(__uint_as_float((unsigned)q[u][0].x), __uint_as_float((unsigned)q[u][0].y),
+                                  __uint_as_float((unsigned)q[u][1].x), __uint_as_float((unsigned)q[u][1].y))
+                    : zero4();
+    }
+    const bool tr = p.trace != nullptr && s >= 100 && s < 132 && threadIdx.x == 0;
+    unsigned *trp = tr ? p.trace + ((s - 100) * 148 + (blockIdx.x < 148 ? blockIdx.x : 147)) * 3 : nullptr;
+    if (tr) trp[0] = gtimer_lo();
+    auto dot = [&](const float4 (&a)[kColC4]) {
+      float acc = 0.f;
+#pragma unroll
+      for (int u = 0; u < kColC4; ++u) {
+        acc = fmaf(a[u].x, xr[u].x, acc);
+        acc = fmaf(a[u].y, xr[u].y, acc);
+        acc = fmaf(a[u].z, xr[u].z, acc);
+        acc = fmaf(a[u].w, xr[u].w, acc);
+      }
+      return acc;
+    };
+    auto dot_t = [&](const uint32_t (&t)[16]) {
+      float acc = 0.f;
+#pragma unroll
+      for (int u = 0; u < kColC4; ++u) {
+        acc = fmaf(__uint_as_float(t[4 * u + 0]), xr[u].x, acc);
+        acc = fmaf(__uint_as_float(t[4 * u + 1]), xr[u].y, acc);
+        acc = fmaf(__uint_as_float(t[4 * u + 2]), xr[u].z, acc);
+        acc = fmaf(__uint_as_float(t[4 * u + 3]), xr[u].w, acc);
+      }
+      return acc;
+    };
+    auto reduce16 = [&](float (&v)[16]) {
+#pragma unroll
+      for (int h = 8; h >= 1; h >>= 1) {
+        const bool up = (lane & h) != 0;
+#pragma unroll
+        for (int k = 0; k < h; ++k) {
+          const float send = up ? v[k] : v[k + h];
+          const float keep = up ? v[k + h] : v[k];
+          v[k] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+        }
+      }
+      return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 16);
+    };
+    // set 1 = register rows, smem rows, 4 empty (reduced first, so only one
+    // set of partials is live while TMEM rows stream in); set 0 = TMEM rows
+    float m1;
+    {
+      float w[16];
+#pragma unroll
+      for (int r = 0; r < kTmRR; ++r) w[r] = dot(areg[r]);
+#pragma unroll
+      for (int r = 0; r < kTmRS; ++r) {
+        float4 a[kColC4];
+#pragma unroll
+        for (int u = 0; u < kColC4; ++u) a[u] = lds4(&acache[(r * kColC4 + u) * kColT + tid]);
+        w[kTmRR + r] = dot(a);
+      }
+#pragma unroll
+      for (int k = kTmRR + kTmRS; k < 16; ++k) w[k] = 0.f;
+      m1 = reduce16(w);
+    }
+    float m0;
+    {
+      float v[16];
+#pragma unroll
+      for (int bt = 0; bt < kTmRT / kTmBatch; ++bt) {
+        uint32_t t[kTmBatch][16];
+        // the batch's address depends (by an opaque 0) on the previous batch's
+        // dots, so ptxas cannot hoist every tcgen05.ld of the sweep to the
+        // top and hold all 256 values in registers at once
+        const uint32_t dep =
+            bt < kTmDep ? 0u : (__float_as_uint(v[(bt - kTmDep + 1) * kTmBatch - 1]) & p.zero);
+#pragma unroll
+        for (int j = 0; j < kTmBatch; ++j) KAAS_TMEM_LD16(taddr + dep + 16u * (bt * kTmBatch + j), t[j]);
+        tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < kTmBatch; ++j) v[bt * kTmBatch + j] = dot_t(t[j]);
+      }
+      m0 = reduce16(v);
+    }
+    const float mine = lane < 16 ? m0 : m1;
+    red[warp][lane] = mine;
+    if (tr) trp[1] = gtimer_lo();
+    __syncthreads();
+    float *slot = partials + (s & 1) * kMaxJacobiBlocks;
+    if (warp == 0) {
+      float tot = 0.f;
+#pragma unroll
+      for (int w8 = 0; w8 < kColW; ++w8) tot += red[w8][lane];
+      float res = 0.f;
+      if (my_rl < R) {
+        const float xn = (bi - tot) / di;  // IEEE div.rn
+        const int i = r0 + my_rl;
+        x_out[i] = xn;
+        if (p.tagged)
+          st_relaxed_u64(p.xt + (size_t)((s + 1) & 1) * kJacTaggedMaxN + i,
+                         tagged_word(xn, p.tag0 + (unsigned)s + 1));
+        res = fabsf(xn - (from_tags ? xprev : __ldcg(x_in + i)));
+        xprev = xn;
+      }
+      if (want_resid) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) res += __shfl_xor_sync(0xffffffffu, res, off);
+        if (lane == 0) slot[blockIdx.x] = res;
+      }
+    }
+    if (tr) trp[2] = gtimer_lo();
+    if (want_resid || !p.tagged) {
+      grid_sync_mono(sync + 3, epoch++);
+      if (want_resid && blockIdx.x == 0 && threadIdx.x < 32)
+        finish_resid(slot, gridDim.x, p.ptrs[p.idx[s][2] & 0x7f]);
+    } else {
+      __syncthreads();
+    }
+  }
+
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+}
+
 unsigned *&jacobi_trace_buffer() {
   static unsigned *buf = nullptr;
   return buf;
@@ -1167,6 +1464,12 @@ bool use_cols_kernel(int dev, int n, uint64_t cov, int blocks) {
   return n % 4 == 0 && n >= 2048 && n <= kColW * 32 * kColC4 * 4 &&
          (cov + blocks - 1) / blocks <= (uint64_t)kColRows &&
          device_props(dev).max_smem_optin >= (int)(kColSmem + sizeof(float) * kColW * 32);
+}
+
+// the band in TMEM + registers + smem (default); KAAS_JACOBI_TMEM=0 = L2 tier
+bool use_tmem_kernel() {
+  const char *e = getenv("KAAS_JACOBI_TMEM");  // dev A/B
+  return !(e && e[0] == '0');
 }
 
 // threads for the row kernel: one warp per band row, 4..32 warps
@@ -1442,6 +1745,7 @@ int launch_jacobi_chain(cudaStream_t s, int dev, const JacobiChain &c, StreamScr
     p.xt = sc->jac_xt;
     p.tag0 = 0;
     p.tagged = 0;
+    p.zero = 0;
     p.trace = nullptr;
     if (use_rows && use_cols_kernel(dev, c.n, c.cov, blocks)) {
       // a pure ping-pong run (each sweep reads the previous one's output, no
@@ -1468,12 +1772,13 @@ int launch_jacobi_chain(cudaStream_t s, int dev, const JacobiChain &c, StreamScr
         p.tag0 = sc->jac_tag;
         sc->jac_tag += (unsigned)cnt + 1u;
       }
-      KAAS_CUDA(cudaFuncSetAttribute((const void *)k_jacobi_cols,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kColSmem));
+      const bool tm = use_tmem_kernel();
+      const void *cfn = tm ? (const void *)k_jacobi_tmem : (const void *)k_jacobi_cols;
+      const size_t csmem = tm ? kTmSmem : kColSmem;
+      KAAS_CUDA(cudaFuncSetAttribute(cfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
       KAAS_CUDA(cudaMemsetAsync(sync + 3, 0, sizeof(unsigned), s));  // monotonic barrier counter
       void *cargs[] = {(void *)&p, (void *)&partials, (void *)&sync};
-      KAAS_CUDA(cudaLaunchCooperativeKernel((const void *)k_jacobi_cols, dim3(blocks), dim3(kColT),
-                                            cargs, kColSmem, s));
+      KAAS_CUDA(cudaLaunchCooperativeKernel(cfn, dim3(blocks), dim3(kColT), cargs, csmem, s));
     } else if (use_rows) {
       KAAS_CUDA(cudaMemsetAsync(sync + 3, 0, sizeof(unsigned), s));  // monotonic barrier counter
       void *rargs[] = {(void *)&p, (void *)&partials, (void *)&sync};
