@@ -1311,7 +1311,12 @@ k_jacobi_tmem(const __grid_constant__ ChainParams p, float *partials, unsigned *
       unsigned spins = 0;
       while (pending) {
         if (++spins > (1u << 22)) __trap();  // a lost producer: fail loudly, never hang
-        if (spins > 1 && p.poll_ns) __nanosleep(p.poll_ns);
+        if (p.tagged == 3 && spins > 1) break;  // dev: no waiting (compute-only timing; wrong results)
+        if (spins > 1 && p.poll_ns) {  // dev A/B: busy back-off (cycles) between polls
+          const long long t = clock64();
+          while (clock64() - t < p.poll_ns) {
+          }
+        }
 #pragma unroll
         for (int u = 0; u < kColC4; ++u) {
           if (pending & (1u << u)) {
@@ -1471,6 +1476,7 @@ bool use_tmem_kernel() {
   const char *e = getenv("KAAS_JACOBI_TMEM");  // dev A/B
   return !(e && e[0] == '0');
 }
+
 
 // threads for the row kernel: one warp per band row, 4..32 warps
 int rows_threads(int dev, uint64_t cov) {
@@ -1762,7 +1768,7 @@ int launch_jacobi_chain(cudaStream_t s, int dev, const JacobiChain &c, StreamScr
                                     2 * kJacTaggedMaxN * sizeof(unsigned long long), s));
           sc->jac_tag = 1;
         }
-        p.tagged = 1;
+        p.tagged = getenv("KAAS_JACOBI_NOWAIT") ? 3 : 1;  // dev: 3 = compute-only timing
         static unsigned *trace_buf = nullptr;  // dev: KAAS_JACOBI_TRACE=1 (tools/jtrace.py)
         if (getenv("KAAS_JACOBI_TRACE") && !trace_buf) cudaMalloc((void **)&trace_buf, 32 * 148 * 3 * 4);
         p.trace = getenv("KAAS_JACOBI_TRACE") ? trace_buf : nullptr;

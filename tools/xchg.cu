@@ -1,0 +1,102 @@
+// All-to-all x exchange alone (dev tool): the Jacobi sweep's communication
+// pattern without the arithmetic.  148 CTAs x 256 threads; each sweep every
+// CTA publishes its 28 rows as (value, tag) words and every lane polls its
+// 16 words (4 chunks x 4) until the tags of this sweep are seen.
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/xchg tools/xchg.cu
+//   ./tools/xchg [sweeps=2000]
+//
+// mode 0: per-lane polling of all 16 words (the kernel's scheme)
+// mode 1: mode 0 + a busy delay of D cycles per sweep standing in for compute
+// mode 2: warp 0 lane l polls only the words of producer CTAs, then bar.sync
+//         and every lane reads its x with one more L2 round trip
+#include <cstdio>
+#include <cstdlib>
+#include <cuda_runtime.h>
+
+constexpr int N = 4096, T = 256;
+
+__device__ __forceinline__ ulonglong2 ld_rlx2(const unsigned long long *p) {
+  ulonglong2 v;
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_rlx(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(T, 1) xchg(unsigned long long *xt, int sweeps, int delay, unsigned tag0,
+                                              float *sink) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int G = gridDim.x;
+  const int r0 = (int)((long long)blockIdx.x * N / G), r1 = (int)((long long)(blockIdx.x + 1) * N / G);
+  const int cbase = warp * 128 + lane;
+  float acc = 0.f;
+  for (int s = 0; s < sweeps; ++s) {
+    const unsigned want = tag0 + s;
+    const unsigned long long *src = xt + (size_t)(s & 1) * N;
+    if (s > 0) {
+      unsigned pending = 0xf;
+      ulonglong2 q[4][2];
+      while (pending) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (pending & (1u << u)) {
+            q[u][0] = ld_rlx2(src + 4 * (cbase + 32 * u));
+            q[u][1] = ld_rlx2(src + 4 * (cbase + 32 * u) + 2);
+          }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if ((pending & (1u << u)) && (unsigned)(q[u][0].x >> 32) == want && (unsigned)(q[u][0].y >> 32) == want &&
+              (unsigned)(q[u][1].x >> 32) == want && (unsigned)(q[u][1].y >> 32) == want)
+            pending &= ~(1u << u);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc += __uint_as_float((unsigned)q[u][0].x) + __uint_as_float((unsigned)q[u][1].y);
+    }
+    if (delay) {
+      const long long t = clock64();
+      while (clock64() - t < delay) {
+      }
+    }
+    __syncthreads();
+    if (warp == 0 && r0 + lane < r1) {
+      const unsigned long long w = ((unsigned long long)(want + 1) << 32) | __float_as_uint(acc);
+      st_rlx(xt + (size_t)((s + 1) & 1) * N + r0 + lane, w);
+    }
+    __syncthreads();
+  }
+  if (acc == 1234.5f) *sink = acc;
+}
+
+int main(int argc, char **argv) {
+  const int sweeps = argc > 1 ? atoi(argv[1]) : 2000;
+  int sms, clk;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+  unsigned long long *xt;
+  float *sink;
+  cudaMalloc(&xt, 2 * N * 8);
+  cudaMalloc(&sink, 4);
+  cudaMemset(xt, 0, 2 * N * 8);
+  unsigned tag = 1;
+  for (int delay : {0, 0, 500, 1000, 2000}) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a);
+    void *args[] = {&xt, (void *)&sweeps, &delay, &tag, &sink};
+    cudaLaunchCooperativeKernel((void *)xchg, sms, T, args, 0, 0);
+    cudaEventRecord(b);
+    if (cudaEventSynchronize(b) != cudaSuccess) {
+      printf("error\n");
+      return 1;
+    }
+    tag += sweeps + 1;
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    printf("exchange only, busy delay %4d cycles (%.0f ns): %.3f us/sweep\n", delay, delay / (clk * 1e-6),
+           ms * 1e3 / sweeps);
+  }
+  return 0;
+}
