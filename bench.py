@@ -408,14 +408,16 @@ def ours(args, rank, world, local_rank, dist):
                 "peak": peaks["hbm_gbs"], "peak_kind": peak_kind,
                 "frac": achieved / peaks["hbm_gbs"],
                 "traffic": profile_traffic("jacobi_sweep"),
-                "kernel": "k_jacobi_cols (500 sweeps, one cooperative launch; A on chip, x via tagged words)",
+                "kernel": "k_jacobi_tmem (500 sweeps, one cooperative launch; A on chip, x via tagged words)",
                 "unit_bytes": alg_bytes, "sweep_us": sweep_s * 1e6,
                 "note": "A (64 MiB) is read from HBM once per request (L2 flushed between "
-                        "requests) and then held on chip across the 500 sweeps: 20 of each "
-                        "SM's 28 rows in registers + shared memory, 8 re-read from L2 "
-                        "(evict_last). Achieved = algorithmic bytes / sweep time, so it "
-                        "exceeds the HBM copy peak by design; L2 re-read ceiling for "
-                        "reference (tools/l2bw.cu, profiles/l2bw_r01.txt)",
+                        "requests; ncu: 67.2 MB DRAM per 500-sweep launch) and then held on "
+                        "chip for all 500 sweeps: 16 of each SM's 28 rows in tensor memory, "
+                        "6 in registers, 6 in shared memory. Achieved = algorithmic bytes / "
+                        "sweep time, so it exceeds the HBM copy peak by design. The sweep is "
+                        "bound by the all-to-all x exchange between the 148 CTAs (exchange "
+                        "alone: 1.5 us/sweep, tools/xchg.cu; one SM->SM hop 366 ns, "
+                        "tools/pingpong.cu) plus ~1 us of on-chip arithmetic",
                 "l2_peak_measured_gbs": L2_PEAK_GBS,
                 "frac_of_l2": achieved / L2_PEAK_GBS,
             },
