@@ -405,9 +405,14 @@ k_cgemm_tf32x3(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
 // accumulator, so K is walked once instead of three times: 2/3 of v1's
 // L2->SMEM operand traffic for the same tensor work.
 constexpr int BK2 = 16;
-constexpr int STAGES2 = 4;
-
+// ring depth: stages of (2 BM + 2 BN) x 16 fp32 -- 32 KiB at BN = 128, 48 KiB
+// at BN = 256 -- as many as fit next to the barriers (192 KiB either way); the
+// narrow-tile case needs the depth to cover L2 latency (each stage is only
+// 384 MMA cycles there)
 template <int BN>
+constexpr int stages2() { return BN == 128 ? 6 : 4; }
+
+template <int BN, int STAGES2 = stages2<BN>()>
 struct Smem2 {
   alignas(1024) float a_hi[STAGES2][BM * BK2];
   alignas(1024) float a_lo[STAGES2][BM * BK2];
@@ -438,6 +443,7 @@ k_cgemm_fused4(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
   extern __shared__ uint8_t smem_raw[];
   Smem2<BN> &sm = *reinterpret_cast<Smem2<BN> *>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int STAGES2 = stages2<BN>();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr uint32_t kTmemCols = 2 * BN;
   constexpr uint32_t kStageBytes = (2 * BM + 2 * BN) * BK2 * 4;

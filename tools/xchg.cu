@@ -7,9 +7,9 @@
 //   ./tools/xchg [sweeps=2000]
 //
 // mode 0: per-lane polling of all 16 words (the kernel's scheme)
-// mode 1: mode 0 + a busy delay of D cycles per sweep standing in for compute
-// mode 2: warp 0 lane l polls only the words of producer CTAs, then bar.sync
-//         and every lane reads its x with one more L2 round trip
+// (each mode also runs with a busy delay of D cycles per sweep standing in for compute)
+// mode 1: polls with ld.global.cg (weak, L2) instead of ld.relaxed.gpu
+// mode 2: mode 0 without the second bar.sync per sweep
 #include <cstdio>
 #include <cstdlib>
 #include <cuda_runtime.h>
@@ -21,10 +21,16 @@ __device__ __forceinline__ ulonglong2 ld_rlx2(const unsigned long long *p) {
   asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ ulonglong2 ld_cg2(const unsigned long long *p) {
+  ulonglong2 v;
+  asm volatile("ld.global.cg.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void st_rlx(unsigned long long *p, unsigned long long v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+template <int MODE, int REP = 1>
 __global__ void __launch_bounds__(T, 1) xchg(unsigned long long *xt, int sweeps, int delay, unsigned tag0,
                                               float *sink) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -34,7 +40,9 @@ __global__ void __launch_bounds__(T, 1) xchg(unsigned long long *xt, int sweeps,
   float acc = 0.f;
   for (int s = 0; s < sweeps; ++s) {
     const unsigned want = tag0 + s;
-    const unsigned long long *src = xt + (size_t)(s & 1) * N;
+    // REP replicas of the tagged buffer: CTA b polls replica b % REP, so each
+    // L2 line is polled by ~148 / REP CTAs instead of all of them
+    const unsigned long long *src = xt + ((size_t)(s & 1) * REP + blockIdx.x % REP) * N;
     if (s > 0) {
       unsigned pending = 0xf;
       ulonglong2 q[4][2];
@@ -42,8 +50,13 @@ __global__ void __launch_bounds__(T, 1) xchg(unsigned long long *xt, int sweeps,
 #pragma unroll
         for (int u = 0; u < 4; ++u)
           if (pending & (1u << u)) {
-            q[u][0] = ld_rlx2(src + 4 * (cbase + 32 * u));
-            q[u][1] = ld_rlx2(src + 4 * (cbase + 32 * u) + 2);
+            if (MODE == 1) {
+              q[u][0] = ld_cg2(src + 4 * (cbase + 32 * u));
+              q[u][1] = ld_cg2(src + 4 * (cbase + 32 * u) + 2);
+            } else {
+              q[u][0] = ld_rlx2(src + 4 * (cbase + 32 * u));
+              q[u][1] = ld_rlx2(src + 4 * (cbase + 32 * u) + 2);
+            }
           }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
@@ -62,9 +75,10 @@ __global__ void __launch_bounds__(T, 1) xchg(unsigned long long *xt, int sweeps,
     __syncthreads();
     if (warp == 0 && r0 + lane < r1) {
       const unsigned long long w = ((unsigned long long)(want + 1) << 32) | __float_as_uint(acc);
-      st_rlx(xt + (size_t)((s + 1) & 1) * N + r0 + lane, w);
+#pragma unroll
+      for (int r = 0; r < REP; ++r) st_rlx(xt + ((size_t)((s + 1) & 1) * REP + r) * N + r0 + lane, w);
     }
-    __syncthreads();
+    if (MODE != 2) __syncthreads();
   }
   if (acc == 1234.5f) *sink = acc;
 }
@@ -76,17 +90,21 @@ int main(int argc, char **argv) {
   cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
   unsigned long long *xt;
   float *sink;
-  cudaMalloc(&xt, 2 * N * 8);
+  cudaMalloc(&xt, 2 * 16 * N * 8);
   cudaMalloc(&sink, 4);
-  cudaMemset(xt, 0, 2 * N * 8);
+  cudaMemset(xt, 0, 2 * 16 * N * 8);
   unsigned tag = 1;
-  for (int delay : {0, 0, 500, 1000, 2000}) {
+  void *kern[] = {(void *)xchg<0>, (void *)xchg<1>, (void *)xchg<2>, (void *)xchg<0, 2>, (void *)xchg<0, 4>,
+                  (void *)xchg<0, 8>, (void *)xchg<0, 16>};
+  const char *names[] = {"relaxed", "ld.cg", "1 bar", "2 replicas", "4 replicas", "8 replicas", "16 replicas"};
+  for (int mode = 0; mode < 7; ++mode)
+  for (int delay : {0, 0, 1000}) {
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     cudaEventRecord(a);
     void *args[] = {&xt, (void *)&sweeps, &delay, &tag, &sink};
-    cudaLaunchCooperativeKernel((void *)xchg, sms, T, args, 0, 0);
+    cudaLaunchCooperativeKernel(kern[mode], sms, T, args, 0, 0);
     cudaEventRecord(b);
     if (cudaEventSynchronize(b) != cudaSuccess) {
       printf("error\n");
@@ -95,7 +113,7 @@ int main(int argc, char **argv) {
     tag += sweeps + 1;
     float ms;
     cudaEventElapsedTime(&ms, a, b);
-    printf("exchange only, busy delay %4d cycles (%.0f ns): %.3f us/sweep\n", delay, delay / (clk * 1e-6),
+    printf("%-12s: exchange only, busy delay %4d cycles (%.0f ns): %.3f us/sweep\n", names[mode], delay, delay / (clk * 1e-6),
            ms * 1e3 / sweeps);
   }
   return 0;
