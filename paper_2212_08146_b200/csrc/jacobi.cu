@@ -873,6 +873,20 @@ __device__ __forceinline__ ulonglong2 ld_relaxed_u64x2(const unsigned long long 
   asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p) : "memory");
   return v;
 }
+// one lane's whole chunk (4 tagged words, 32 B) in one 256-bit load: a warp's
+// poll is 1 KB contiguous, every sector fully used (two 128-bit loads would
+// fetch each sector twice -- strong loads bypass L1)
+struct TagWords4 {
+  unsigned long long w[4];
+};
+__device__ __forceinline__ TagWords4 ld_relaxed_u64x4(const unsigned long long *p) {
+  TagWords4 v;
+  asm volatile("ld.relaxed.gpu.global.v4.u64 {%0, %1, %2, %3}, [%4];"
+               : "=l"(v.w[0]), "=l"(v.w[1]), "=l"(v.w[2]), "=l"(v.w[3])
+               : "l"(p)
+               : "memory");
+  return v;
+}
 __device__ __forceinline__ void st_relaxed_u64(unsigned long long *p, unsigned long long v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -1303,7 +1317,7 @@ k_jacobi_tmem(const __grid_constant__ ChainParams p, float *partials, unsigned *
     } else {
       const unsigned want = p.tag0 + (unsigned)s;
       const unsigned long long *src = p.xt + (size_t)(s & 1) * kJacTaggedMaxN;
-      ulonglong2 q[kColC4][2];
+      TagWords4 q[kColC4];
       unsigned pending = 0;
 #pragma unroll
       for (int u = 0; u < kColC4; ++u)
@@ -1318,26 +1332,21 @@ k_jacobi_tmem(const __grid_constant__ ChainParams p, float *partials, unsigned *
           }
         }
 #pragma unroll
-        for (int u = 0; u < kColC4; ++u) {
-          if (pending & (1u << u)) {
-            const int c4 = cbase + 32 * u;
-            q[u][0] = ld_relaxed_u64x2(src + 4 * c4);
-            q[u][1] = ld_relaxed_u64x2(src + 4 * c4 + 2);
-          }
-        }
+        for (int u = 0; u < kColC4; ++u)
+          if (pending & (1u << u)) q[u] = ld_relaxed_u64x4(src + 4 * (cbase + 32 * u));
 #pragma unroll
         for (int u = 0; u < kColC4; ++u) {
-          if ((pending & (1u << u)) && (unsigned)(q[u][0].x >> 32) == want &&
-              (unsigned)(q[u][0].y >> 32) == want && (unsigned)(q[u][1].x >> 32) == want &&
-              (unsigned)(q[u][1].y >> 32) == want)
+          if ((pending & (1u << u)) && (unsigned)(q[u].w[0] >> 32) == want &&
+              (unsigned)(q[u].w[1] >> 32) == want && (unsigned)(q[u].w[2] >> 32) == want &&
+              (unsigned)(q[u].w[3] >> 32) == want)
             pending &= ~(1u << u);
         }
       }
 #pragma unroll
       for (int u = 0; u < kColC4; ++u)
         xr[u] = cbase + 32 * u < n4
-                    ? make_float4(__uint_as_float((unsigned)q[u][0].x), __uint_as_float((unsigned)q[u][0].y),
-                                  __uint_as_float((unsigned)q[u][1].x), __uint_as_float((unsigned)q[u][1].y))
+                    ? make_float4(__uint_as_float((unsigned)q[u].w[0]), __uint_as_float((unsigned)q[u].w[1]),
+                                  __uint_as_float((unsigned)q[u].w[2]), __uint_as_float((unsigned)q[u].w[3]))
                     : zero4();
     }
     const bool tr = p.trace != nullptr && s >= 100 && s < 132 && threadIdx.x == 0;

@@ -1,5 +1,9 @@
-# dev: ncu capture of the Jacobi TMEM kernel
+# dev: Jacobi A/B (kernel-only timings), parity subset first
 mkdir -p gpurun_out
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"jacobi_tmem" -c 1 \
-    -o gpurun_out/jtmem_full -f python tools/kbench.py jacobi 4096 500 1 > gpurun_out/ncu_jtmem.log 2>&1
-tail -5 gpurun_out/ncu_jtmem.log
+out=gpurun_out/jvar.txt; : > $out
+timeout 300 python -m pytest tests -m gpu -q -p no:cacheprovider -x -k "jacobi or Jacobi" 2>&1 | tail -2 >> $out
+for i in 1 2; do echo "== default" >> $out; timeout 60 python tools/kbench.py jacobi 4096 500 5 >> $out 2>&1; done
+echo "== nowait" >> $out; KAAS_JACOBI_NOWAIT=1 timeout 60 python tools/kbench.py jacobi 4096 500 5 >> $out 2>&1
+echo "== trace" >> $out; KAAS_JACOBI_TRACE=1 timeout 60 python tools/jtrace.py 4096 >> $out 2>&1
+for v in $(ls build/var 2>/dev/null); do echo "== $v" >> $out; KAAS_B200_LIB=build/var/$v timeout 60 python tools/kbench.py jacobi 4096 500 5 >> $out 2>&1 || echo FAIL >> $out; done
+cat $out
