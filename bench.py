@@ -257,7 +257,11 @@ def measure_mixed(device, clients=16, count=160, policy="affinity:8", capacity=5
     reqs = W.mixed_requests(uni, count)
     with KaasService(store, n_executors=1, capacity=capacity, policy=policy,
                      devices=[device]) as svc:
-        run_stream(svc, reqs[:8], 1)  # warm the pinned pools / plans
+        # one full pass first: a server maps its pinned output blocks and
+        # device pools once; the first pass pays ~0.5 s of cudaHostAlloc /
+        # pool growth for 1 GiB of distinct outputs (tools/mixed_diag.py).
+        # The measured pass then runs under steady-state LRU pressure.
+        run_stream(svc, reqs, clients)
         ex = svc.executors[0]
         h2d0, h2dms0, dev0 = ex.dev_stats.h2d_bytes, ex.dev_stats.h2d_ms, ex.dev_stats.device_ms
         t0 = time.perf_counter()
@@ -269,7 +273,8 @@ def measure_mixed(device, clients=16, count=160, policy="affinity:8", capacity=5
         h2d_ms = ex.dev_stats.h2d_ms - h2dms0
         evictions = ex.cache.evictions
     return {"workload": "mixed cgemm 2048^3 + jacobi N=4096x100 sweeps, zipf(1.0) over 8+8 const "
-                        f"objects, {clients} clients, {policy}, ledger {capacity >> 20} MiB/GPU",
+                        f"objects, {clients} clients, {policy}, ledger {capacity >> 20} MiB/GPU; "
+                        "measured pass after one warm-up pass of the same stream",
             "requests": len(reqs), "errors": sum(0 if r.status.ok else 1 for r in resps),
             "req_per_s": len(reqs) / wall, "p50_ms": percentile(lat, 0.5) * 1e3,
             "p99_ms": percentile(lat, 0.99) * 1e3, "hit_rate": hits / max(1, hits + misses),
