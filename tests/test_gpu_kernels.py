@@ -289,3 +289,59 @@ def test_resnet_chain_bit_exact(gpu):
     assert o.status.ok and r.per_invocation == o.per_invocation
     assert r.simulated_total_time == o.simulated_total_time
     assert canon(store.get("rn/out")) == canon(ostore.get("rn/out"))
+
+
+@pytest.mark.parametrize("n", [2048, 4096])
+def test_jacobi_every_residual_observable(gpu, n):
+    """Each sweep writes its own keyed residual (every sweep is a last writer,
+    so the on-chip kernel runs a grid barrier + residual finish per sweep)
+    and the chain ping-pongs keyed buffers, all of them flushed."""
+    ex, store = gpu
+    sweeps = 6
+    A, b = W.seed_jacobi(store, n, prefix=f"jr{n}")
+    bufs = [BufferArg("A", 4 * n * n, "input", key=f"jr{n}/A/{n}", is_const=True),
+            BufferArg("b", 4 * n, "input", key=f"jr{n}/b/{n}", is_const=True),
+            BufferArg("x0", 4 * n, "input", key=f"jr{n}/x0/{n}"),
+            BufferArg("p", 4 * n, "inout", key=f"jr{n}/p"),
+            BufferArg("q", 4 * n, "inout", key=f"jr{n}/q")]
+    bufs += [BufferArg(f"r{s}", 4, "output", key=f"jr{n}/r{s}") for s in range(sweeps)]
+    invs = []
+    for s in range(sweeps):
+        src = "x0" if s == 0 else ("p" if s % 2 == 1 else "q")
+        dst = "p" if s % 2 == 0 else "q"
+        invs.append(KernelInvocation("jacobi_sweep", LaunchDims(grid_x=n), (i32(n),), ("A", "b", src, dst, f"r{s}")))
+    store.put(f"jr{n}/p", bytes(4 * n))
+    store.put(f"jr{n}/q", bytes(4 * n))
+    req = KaasRequest(f"jr{n}", tuple(bufs), tuple(invs))
+    _run(ex, req)
+    ostore = DictStore({f"jr{n}/A/{n}": A.tobytes(), f"jr{n}/b/{n}": b.tobytes(),
+                        f"jr{n}/x0/{n}": np.zeros(n, "<f4").tobytes(),
+                        f"jr{n}/p": bytes(4 * n), f"jr{n}/q": bytes(4 * n)})
+    OracleExecutor(1 << 30, ostore).execute(req)
+    for key in ("p", "q"):
+        g = np.frombuffer(store.get(f"jr{n}/{key}"), "<f4").astype(np.float64)
+        o = np.frombuffer(ostore.get(f"jr{n}/{key}"), "<f4").astype(np.float64)
+        assert np.abs(g - o).max() <= 1e-5
+    for s in range(sweeps):
+        gr = np.frombuffer(store.get(f"jr{n}/r{s}"), "<f4")[0]
+        orr = np.frombuffer(ostore.get(f"jr{n}/r{s}"), "<f4")[0]
+        assert abs(gr - orr) <= 1e-4 * abs(orr) + 1e-6, (s, gr, orr)
+
+
+@pytest.mark.parametrize("path", ["tmem", "cols"])
+def test_jacobi_onchip_kernels_agree(gpu, path, monkeypatch):
+    """Both on-chip kernels (TMEM tier default; KAAS_JACOBI_TMEM=0 = L2 tier)
+    meet the tolerance on BASELINE configs[1]'s shape, 50 sweeps."""
+    ex, store = gpu
+    if path == "cols":
+        monkeypatch.setenv("KAAS_JACOBI_TMEM", "0")
+    n, sweeps = 4096, 50
+    A, b = W.seed_jacobi(store, n, prefix="jk")
+    req = W.jacobi_request(f"jk-{path}", n, sweeps, f"jk/A/{n}", f"jk/b/{n}", f"jk/x0/{n}", f"jk/x-{path}", "jk/r")
+    _run(ex, req)
+    ostore = DictStore({f"jk/A/{n}": A.tobytes(), f"jk/b/{n}": b.tobytes(),
+                        f"jk/x0/{n}": np.zeros(n, "<f4").tobytes()})
+    OracleExecutor(1 << 30, ostore).execute(req)
+    g = np.frombuffer(store.get(f"jk/x-{path}"), "<f4").astype(np.float64)
+    o = np.frombuffer(ostore.get(f"jk/x-{path}"), "<f4").astype(np.float64)
+    assert np.abs(g - o).max() <= 1e-5
