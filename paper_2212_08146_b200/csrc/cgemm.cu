@@ -220,6 +220,9 @@ struct GemmShape {
   int num_m, num_n;  // tile grid
   int m_complex;     // m (complex columns) for coverage indexing
   unsigned long long cov;  // covered complex cells
+  int ksplit;        // fused4 only: 1, or 2 = each tile's K in two halves on
+                     // two CTAs, both red.add-ed onto a zeroed C ((0+a)+b ==
+                     // (0+b)+a exactly, so the result is deterministic)
 };
 
 template <int BN>
@@ -471,18 +474,19 @@ k_cgemm_fused4(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = sm.tmem_base;
-  const int total_tiles = s.num_m * s.num_n;
+  const int total_units = s.num_m * s.num_n * s.ksplit;  // unit = (tile, K slice)
   const int kbs = s.kb_per_seg;  // k-blocks of BK2 per tile (one pass)
 
   if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+      for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
         int mb, nb;
-        tile_coords(s, t, mb, nb);
+        tile_coords(s, u / s.ksplit, mb, nb);
         const int arow = mb * BM, brow = nb * BN;
-        for (int kb = 0; kb < kbs; ++kb) {
+        const int ks = u % s.ksplit;
+        for (int kb = ks * kbs / s.ksplit; kb < (ks + 1) * kbs / s.ksplit; ++kb) {
           mbar_wait(&sm.empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&sm.full[stage], kStageBytes);
           tma_load_2d(&map_a, &sm.full[stage], sm.a_hi[stage], kb * BK2, arow);
@@ -502,13 +506,14 @@ k_cgemm_fused4(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++local) {
+      for (int u = blockIdx.x; u < total_units; u += gridDim.x, ++local) {
         const int acc = local & 1;
         const uint32_t acc_phase = (local >> 1) & 1;
         mbar_wait(&sm.tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * BN;
-        for (int kb = 0; kb < kbs; ++kb) {
+        const int ks = u % s.ksplit, kb0 = ks * kbs / s.ksplit, kb1 = (ks + 1) * kbs / s.ksplit;
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&sm.full[stage], phase);
           tc_fence_after();
           const uint32_t ah = smem_u32(sm.a_hi[stage]), al = smem_u32(sm.a_lo[stage]);
@@ -518,7 +523,7 @@ k_cgemm_fused4(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
             const uint32_t off = k * 32;
             // small terms first, then the main product
             tc_mma_tf32(tmem_d, make_sw64_desc(ah + off), make_sw64_desc(bl + off), idesc,
-                        (kb | k) != 0);
+                        kb != kb0 || k != 0);
             tc_mma_tf32(tmem_d, make_sw64_desc(al + off), make_sw64_desc(bh + off), idesc, 1);
             tc_mma_tf32(tmem_d, make_sw64_desc(ah + off), make_sw64_desc(bh + off), idesc, 1);
           }
@@ -534,9 +539,9 @@ k_cgemm_fused4(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
   } else {
     const int quarter = warp & 3;
     int local = 0;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++local) {
+    for (int u = blockIdx.x; u < total_units; u += gridDim.x, ++local) {
       int mb, nb;
-      tile_coords(s, t, mb, nb);
+      tile_coords(s, u / s.ksplit, mb, nb);
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       mbar_wait(&sm.tfull[acc], acc_phase);
@@ -553,7 +558,23 @@ k_cgemm_fused4(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
           const unsigned long long g0 = (unsigned long long)row * s.m_complex + (col >> 1);
           const bool full = (col + 32 <= s.N) && (g0 + 16 <= s.cov) &&
                             ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0);
-          if (full) {
+          if (s.ksplit > 1) {  // K half: add onto the zeroed C
+            if (full) {
+#pragma unroll
+              for (int q = 0; q < 8; ++q)
+                asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4 * q),
+                             "f"(__uint_as_float(v[4 * q])), "f"(__uint_as_float(v[4 * q + 1])),
+                             "f"(__uint_as_float(v[4 * q + 2])), "f"(__uint_as_float(v[4 * q + 3]))
+                             : "memory");
+            } else {
+#pragma unroll
+              for (int q = 0; q < 32; ++q) {
+                const int c = col + q;
+                if (c < s.N && (unsigned long long)row * s.m_complex + (c >> 1) < s.cov)
+                  atomicAdd(dst + q, __uint_as_float(v[q]));
+              }
+            }
+          } else if (full) {
 #pragma unroll
             for (int q = 0; q < 8; ++q)
               reinterpret_cast<float4 *>(dst)[q] =
@@ -650,9 +671,9 @@ int launch_gemm2(cudaStream_t s, int dev, const CUtensorMap &ma, const CUtensorM
   const size_t smem = sizeof(Smem2<BN>) + 1024;
   KAAS_CUDA(cudaFuncSetAttribute(k_cgemm_fused4<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
-  const int tiles = shape.num_m * shape.num_n;
+  const int units = shape.num_m * shape.num_n * shape.ksplit;
   int grid = device_props(dev).sm_count;
-  if (grid > tiles) grid = tiles;
+  if (grid > units) grid = units;
   const int npanels = (shape.num_m + kGroupM - 1) / kGroupM;
   WaitValue32Fn waitv = get_wait_value();
   const bool progressive = po != nullptr && waitv != nullptr && npanels > 1 &&
@@ -678,7 +699,7 @@ int launch_gemm2(cudaStream_t s, int dev, const CUtensorMap &ma, const CUtensorM
     for (int p = 0; p < npanels; ++p) {
       const int mb0 = p * kGroupM, mbs = min(kGroupM, shape.num_m - mb0);
       const int row0 = mb0 * BM, row1 = min(shape.M, (mb0 + mbs) * BM);
-      const unsigned want = (unsigned)(mbs * shape.num_n);
+      const unsigned want = (unsigned)(mbs * shape.num_n * shape.ksplit);
       CUresult r = waitv((CUstream)po->out_stream, (CUdeviceptr)(sc->panel_done + p), want,
                          0 /* CU_STREAM_WAIT_VALUE_GEQ */);
       if (r != CUDA_SUCCESS) return fail(KAAS_E_UNSUPPORTED, "cuStreamWaitValue32 failed");
@@ -770,10 +791,15 @@ int launch_cgemm(cudaStream_t s, int dev, int n, int m, int k, uint64_t cov, con
   }
   KAAS_CUDA(cudaGetLastError());
 
-  // Small problems: narrower N tiles so the grid covers the SMs.
+  // Small problems: narrower N tiles, or (full coverage only: C is zeroed
+  // first) each tile's K split over two CTAs, so the grid covers the SMs.
   const int N = 2 * m;
   const int tiles256 = ((n + BM - 1) / BM) * ((N + 255) / 256);
-  const bool narrow = tiles256 < sms;
+  const bool full_cov = cov >= (uint64_t)n * m;
+  const char *ke = getenv("KAAS_CGEMM_KSPLIT");  // dev A/B: 0 = never split K
+  const bool ksplit2 = !(ke && ke[0] == '0') && !cgemm_v1() && full_cov && tiles256 < sms &&
+                       2 * tiles256 <= sms && ldk / BK2 >= 16;
+  const bool narrow = tiles256 < sms && !ksplit2;
   const int BNv = narrow ? 128 : 256;
 
   CUtensorMap ma, mbm;
@@ -795,6 +821,8 @@ int launch_cgemm(cudaStream_t s, int dev, int n, int m, int k, uint64_t cov, con
   shape.num_n = (N + BNv - 1) / BNv;
   shape.m_complex = m;
   shape.cov = cov;
+  shape.ksplit = ksplit2 ? 2 : 1;
+  if (ksplit2) KAAS_CUDA(cudaMemsetAsync(C, 0, (size_t)n * m * 8, s));
   if (!v1) {
     shape.kb_per_seg = ldk / BK2;
     return narrow ? launch_gemm2<128>(s, dev, ma, mbm, shape, C, sc, po)
