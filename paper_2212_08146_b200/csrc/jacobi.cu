@@ -4,21 +4,27 @@
 //   x_out[i] = (b[i] - sum_{j != i} A[i,j] * x_in[j]) / A[i,i]   for i < cov
 //   resid[0] = sum_{i < cov} |x_out[i] - x_in[i]|
 //
-// HBM-bound GEMV: 4*n*n bytes of A per sweep against 2*n*n flops.  Layout in
-// HBM is the request's row-major f32 A.  One CTA per SM, each owning a
-// contiguous band of ~n/148 rows.  Columns are cut into 128-float chunks (one
-// float4 per lane); chunk c belongs to warp c % 16, which keeps its x chunks
-// in registers for the whole sweep.  Rows are processed 8 at a time, so each
-// lane has 8 x (chunks per warp) independent 128-bit loads of A in flight
-// (16 for n = 4096).  The diagonal is masked in-register; per-row partials are
-// reduced with warp shuffles, then across warps through smem in fixed order.
-// Residual partials are reduced deterministically (rows -> CTA -> grid, fixed
-// order, grid level in double).
+// A sweep is a GEMV (4*n*n bytes of A, 2*n*n flops) with no reuse of A
+// inside it -- but a request's sweeps all read the same A, so the kernels
+// that run a request's sweeps keep A close to the SMs.  Kernel family:
+//
+//   k_jacobi_tmem   (default, 2048 <= n <= 4096, n % 4 == 0): each SM's band
+//                   of A lives in TMEM + registers + smem for all sweeps; x
+//                   moves between SMs as (value, tag) words, no grid barrier
+//   k_jacobi_cols   same layout with an L2 tier instead of TMEM
+//                   (KAAS_JACOBI_TMEM=0; the A/B reference)
+//   k_jacobi_rows   n % 4 == 0 up to 40960: one warp per row, A re-read from
+//                   L2 (evict_last), x staged in smem, grid barrier per sweep
+//   k_jacobi_sweep / k_jacobi_chain   any n (scalar path when n % 4 != 0)
+//
+// One CTA per SM, each owning a contiguous band of ~n/148 rows; the diagonal
+// is dropped in-register; per-row partials are reduced with warp shuffles and
+// across warps in fixed order.  Residual partials are reduced
+// deterministically (rows -> CTA -> grid, fixed order, grid level in double).
 //
 // A request's 500 sweeps are 500 invocations ping-ponging two ephemerals;
-// kaas_launch_batch hands such runs to launch_jacobi_chain, a cooperative
-// persistent kernel that runs every sweep with a grid barrier in between, so
-// there is one launch per request instead of 500.
+// kaas_launch_batch hands such runs to launch_jacobi_chain: one cooperative
+// persistent launch per request instead of 500.
 #include <cooperative_groups.h>
 
 #include <cstdlib>
@@ -304,392 +310,6 @@ k_jacobi_chain(const __grid_constant__ ChainParams p, float *partials, unsigned 
   }
 }
 
-
-// ---- TMA-staged sweep kernel (preferred path) -------------------------------
-//
-// Warp 0 (one lane) is a bulk-copy producer: it streams this CTA's rows of A,
-// one row per smem stage, with cp.async.bulk (TMA engine, no register
-// staging) into an S-deep ring guarded by full/empty mbarriers.  Because A is
-// the same for every sweep, the producer runs straight on into the next sweep
-// while the consumers sit in the grid barrier, so the memory pipe never
-// drains.  Warps 1..8 are consumers: x_in is staged once per sweep into smem;
-// each consumer takes every 8th row of the band, reads it from its stage with
-// conflict-free 128-bit smem loads, masks the diagonal, shuffle-reduces, and
-// releases the stage.
-
-constexpr int kTmaConsumers = 8;
-constexpr int kTmaThreads = 32 * (kTmaConsumers + 1);
-constexpr int kTmaMaxStages = 12;
-
-__device__ __forceinline__ uint32_t smem_addr(const void *p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "JWAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra JWAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
-               "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
-                                         uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_addr(dst)),
-      "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
-      : "memory");
-}
-
-__device__ __forceinline__ void consumers_sync() {
-  asm volatile("bar.sync 1, %0;" ::"n"(kTmaConsumers * 32) : "memory");
-}
-
-// consumer-only grid barrier (the producer warp never joins it)
-__device__ __forceinline__ void consumer_grid_barrier(unsigned *count, unsigned *gen, int ctid) {
-  consumers_sync();
-  if (ctid == 0) {
-    const unsigned g = ld_acquire(gen);
-    __threadfence();
-    if (atomicAdd(count, 1u) == gridDim.x - 1) {
-      *count = 0u;
-      __threadfence();
-      atomicAdd(gen, 1u);
-    } else {
-      while (ld_acquire(gen) == g) __nanosleep(20);
-    }
-    __threadfence();
-  }
-  consumers_sync();
-}
-
-// Row dot product against x held in registers: xr[it] = x[128*it + 4*lane ..].
-// Only chunk it_d = i/128 contains the diagonal; that iteration (warp-uniform
-// branch) masks it on the owning lane, every other iteration is 4 plain FMAs.
-template <int XR>
-__device__ __forceinline__ float row_dot_regs(const float4 *row4, const float4 (&xr)[XR], int n4,
-                                              int i, int lane) {
-  float a0 = 0.f, a1 = 0.f;
-  const int it_d = i >> 7;
-#pragma unroll
-  for (int it = 0; it < XR; ++it) {
-    const int j4 = it * 32 + lane;
-    if (j4 < n4) {
-      const float4 a = row4[j4];
-      float4 x = xr[it];
-      if (it == it_d) {
-        const int d = i - 4 * j4;
-        x.x = d == 0 ? 0.f : x.x;
-        x.y = d == 1 ? 0.f : x.y;
-        x.z = d == 2 ? 0.f : x.z;
-        x.w = d == 3 ? 0.f : x.w;
-      }
-      float &acc = (it & 1) ? a1 : a0;
-      acc = fmaf(a.x, x.x, acc);
-      acc = fmaf(a.y, x.y, acc);
-      acc = fmaf(a.z, x.z, acc);
-      acc = fmaf(a.w, x.w, acc);
-    }
-  }
-  return a0 + a1;
-}
-
-// XR > 0: x in registers (n <= 128*XR); XR == 0: x read from smem.
-template <bool kChain, int XR>
-__global__ void __launch_bounds__(kTmaThreads, 1)
-k_jacobi_tma(const __grid_constant__ ChainParams p, int stages, float *partials, unsigned *sync) {
-  extern __shared__ __align__(128) uint8_t jsm[];
-  const int n = p.n;
-  float *x_s = reinterpret_cast<float *>(jsm);
-  float *ring = x_s + ((n + 31) & ~31);
-  uint64_t *full = reinterpret_cast<uint64_t *>(ring + (size_t)stages * n);
-  uint64_t *empty = full + kTmaMaxStages;
-  float *red = reinterpret_cast<float *>(empty + kTmaMaxStages);
-  __shared__ bool last;
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int r0, r1;
-  band(p.cov, r0, r1);
-  const int R = r1 - r0;
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < stages; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  const uint32_t row_bytes = (uint32_t)n * 4u;
-
-  if (warp == 0) {
-    // ===== producer: streams rows, running ahead across sweeps (A is constant)
-    if (lane == 0) {
-      const uint64_t pol = l2_policy(p.keep_l2 != 0);
-      for (int s = 0; s < p.sweeps; ++s)
-        for (int t = 0; t < R; ++t) {
-          const int q = s * R + t, st = q % stages;
-          mbar_wait(&empty[st], ((q / stages) & 1) ^ 1);
-          mbar_expect_tx(&full[st], row_bytes);
-          bulk_g2s(ring + (size_t)st * n, p.A + (size_t)(r0 + t) * n, row_bytes, &full[st], pol);
-        }
-    }
-    return;
-  }
-
-  // ===== consumers =====
-  const int cw = warp - 1, ctid = threadIdx.x - 32;
-  const int n4 = n >> 2;
-  for (int s = 0; s < p.sweeps; ++s) {
-    const float *x_in = p.ptrs[p.idx[s][0]];
-    float *x_out = p.ptrs[p.idx[s][1]];
-    for (int e = ctid; e < n4; e += kTmaConsumers * 32)
-      reinterpret_cast<float4 *>(x_s)[e] = kChain ? __ldcg(reinterpret_cast<const float4 *>(x_in) + e)
-                                                  : __ldg(reinterpret_cast<const float4 *>(x_in) + e);
-    consumers_sync();
-    const float4 *x4 = reinterpret_cast<const float4 *>(x_s);
-    float4 xr[XR > 0 ? XR : 1];
-    if (XR > 0) {
-#pragma unroll
-      for (int it = 0; it < (XR > 0 ? XR : 1); ++it) {
-        const int j4 = it * 32 + lane;
-        xr[it] = j4 < n4 ? x4[j4] : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-    }
-    float res = 0.f;
-    for (int t = cw; t < R; t += kTmaConsumers) {
-      const int q = s * R + t, st = q % stages;
-      const int i = r0 + t;
-      mbar_wait(&full[st], (q / stages) & 1);
-      const float4 *row4 = reinterpret_cast<const float4 *>(ring + (size_t)st * n);
-      float v;
-      if (XR > 0) {
-        v = row_dot_regs<(XR > 0 ? XR : 1)>(row4, xr, n4, i, lane);
-      } else {
-        float a0 = 0.f, a1 = 0.f;
-        int j4 = lane;
-        for (; j4 + 32 < n4; j4 += 64) {
-          a0 += dot_masked(row4[j4], x4[j4], i - 4 * j4);
-          a1 += dot_masked(row4[j4 + 32], x4[j4 + 32], i - 4 * (j4 + 32));
-        }
-        if (j4 < n4) a0 += dot_masked(row4[j4], x4[j4], i - 4 * j4);
-        v = a0 + a1;
-      }
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-      float aii = 0.f;
-      if (lane == 0) aii = ring[(size_t)st * n + i];
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&empty[st]);  // row consumed: release the stage early
-        const float xn = (p.b[i] - v) / aii;  // IEEE div.rn
-        x_out[i] = xn;
-        res += fabsf(xn - x_s[i]);
-      }
-    }
-    if (lane == 0) red[cw] = res;
-    consumers_sync();
-    float part = 0.f;
-    if (ctid == 0)
-      for (int w = 0; w < kTmaConsumers; ++w) part += red[w];
-    if (kChain) {
-      float *slot = partials + (s & 1) * kMaxJacobiBlocks;
-      if (ctid == 0) slot[blockIdx.x] = part;
-      consumer_grid_barrier(sync + 1, sync + 2, ctid);
-      if (blockIdx.x == 0 && cw == 0) finish_resid(slot, gridDim.x, p.ptrs[p.idx[s][2] & 0x7f]);
-    } else {
-      if (ctid == 0) {
-        partials[blockIdx.x] = part;
-        __threadfence();
-        last = atomicAdd(sync, 1u) == gridDim.x - 1;
-      }
-      consumers_sync();
-      if (last && cw == 0) {
-        __threadfence();
-        finish_resid(partials, gridDim.x, p.ptrs[p.idx[s][2] & 0x7f]);
-        if (lane == 0) *sync = 0u;
-      }
-    }
-  }
-}
-
-// ---- direct-load sweep kernel (default path) ---------------------------------
-//
-// A row of the GEMV is used exactly once per sweep, so staging it through
-// shared memory only adds smem-pipe traffic (TMA write + LDS read of every
-// byte).  Measured on B200: an L2-resident 64 MiB buffer re-reads at ~19 TB/s
-// with 128-bit LDG from all SMs, while the smem-staged kernel above tops out
-// near 7 TB/s on the smem pipe.  This kernel loads A straight into registers:
-//   * 8 warps per CTA, one CTA per SM, band of ~n/148 rows per CTA;
-//   * warp w owns columns [w*CW, (w+1)*CW) (CW = KC*128): its x slice lives in
-//     KC float4 registers per lane for the whole sweep;
-//   * rows are processed G at a time with the next group's KC*G 128-bit loads
-//     issued before the current group's FMAs (software pipelined);
-//   * per-lane row partials are combined with a 31-shuffle reduce-scatter
-//     (lane l ends up owning row l of the 32-row block), then across the 8
-//     warps through smem in fixed order.
-constexpr int kLdgWarps = 8;
-constexpr int kLdgThreads = kLdgWarps * 32;
-constexpr int kRowBlock = 32;
-
-// reduce-scatter of v[0..31] across the warp: afterwards lane l holds the
-// warp-wide sum of row l (each step keeps the half selected by one lane bit).
-__device__ __forceinline__ float reduce_scatter32(float (&v)[kRowBlock], int lane) {
-#pragma unroll
-  for (int step = 0; step < 5; ++step) {
-    const int off = 16 >> step;
-    const int half = 16 >> step;  // number of live values halves each step
-    const bool upper = (lane & off) != 0;
-#pragma unroll
-    for (int i = 0; i < half; ++i) {
-      const float send = upper ? v[i] : v[i + half];
-      const float keep = upper ? v[i + half] : v[i];
-      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, off);
-    }
-  }
-  return v[0];
-}
-
-
-template <int KC, int G, bool kChain>
-__device__ __forceinline__ float sweep_ldg(int n, int r0, int r1, const float *__restrict__ A,
-                                           const float *__restrict__ b, const float *x_in,
-                                           float *x_out, float (*red)[kRowBlock], float *part,
-                                           uint64_t pol) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n4 = n >> 2;
-  // this lane's columns: c4[k] = warp*KC*32 + k*32 + lane (float4 index)
-  float4 xr[KC];
-  int c4[KC];
-#pragma unroll
-  for (int k = 0; k < KC; ++k) {
-    c4[k] = (warp * KC + k) * 32 + lane;
-    xr[k] = c4[k] < n4 ? (kChain ? __ldcg(reinterpret_cast<const float4 *>(x_in) + c4[k])
-                                 : __ldg(reinterpret_cast<const float4 *>(x_in) + c4[k]))
-                       : make_float4(0.f, 0.f, 0.f, 0.f);
-  }
-  const int wlo = warp * KC * 128, whi = wlo + KC * 128;  // this warp's column range
-  float res = 0.f;
-  for (int rb = r0; rb < r1; rb += kRowBlock) {
-    const int R = min(kRowBlock, r1 - rb);
-    float acc[kRowBlock];
-#pragma unroll
-    for (int r = 0; r < kRowBlock; ++r) acc[r] = 0.f;
-    float4 cur[G][KC], nxt[G][KC];
-    auto load = [&](float4 (&dst)[G][KC], int g0) {
-#pragma unroll
-      for (int g = 0; g < G; ++g)
-#pragma unroll
-        for (int k = 0; k < KC; ++k) {
-          const int r = g0 + g;
-          dst[g][k] = (r < R && c4[k] < n4)
-                          ? ld_a(A + (size_t)(rb + r) * n + 4 * c4[k], pol)
-                          : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-    };
-    load(cur, 0);
-#pragma unroll
-    for (int g0 = 0; g0 < kRowBlock; g0 += G) {
-      if (g0 + G < kRowBlock && g0 + G < R) load(nxt, g0 + G);
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        const int i = rb + g0 + g;
-        if (i >= wlo && i < whi) {  // warp-uniform: this warp holds the diagonal of row i
-#pragma unroll
-          for (int k = 0; k < KC; ++k) acc[g0 + g] += dot_masked(cur[g][k], xr[k], i - 4 * c4[k]);
-        } else {
-#pragma unroll
-          for (int k = 0; k < KC; ++k) {
-            float a = acc[g0 + g];
-            a = fmaf(cur[g][k].x, xr[k].x, a);
-            a = fmaf(cur[g][k].y, xr[k].y, a);
-            a = fmaf(cur[g][k].z, xr[k].z, a);
-            a = fmaf(cur[g][k].w, xr[k].w, a);
-            acc[g0 + g] = a;
-          }
-        }
-      }
-      if (g0 + G < kRowBlock) {
-#pragma unroll
-        for (int g = 0; g < G; ++g)
-#pragma unroll
-          for (int k = 0; k < KC; ++k) cur[g][k] = nxt[g][k];
-      }
-    }
-    const float mine = reduce_scatter32(acc, lane);
-    red[warp][lane] = mine;
-    __syncthreads();
-    if (threadIdx.x < R) {
-      const int r = threadIdx.x, i = rb + r;
-      float s = 0.f;
-#pragma unroll
-      for (int w = 0; w < kLdgWarps; ++w) s += red[w][r];
-      const float xi = kChain ? __ldcg(x_in + i) : __ldg(x_in + i);
-      const float xn = (b[i] - s) / __ldg(A + (size_t)i * n + i);  // IEEE div.rn
-      x_out[i] = xn;
-      res += fabsf(xn - xi);
-    }
-    __syncthreads();
-  }
-  // CTA residual partial (threads 0..31 hold row residuals), fixed order
-  if (warp == 0) {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) res += __shfl_xor_sync(0xffffffffu, res, off);
-    if (lane == 0) *part = res;
-  }
-  __syncthreads();
-  return *part;
-}
-
-template <int KC, int G, bool kChain>
-__global__ void __launch_bounds__(kLdgThreads, 1)
-k_jacobi_ldg(const __grid_constant__ ChainParams p, float *partials, unsigned *sync) {
-  __shared__ float red[kLdgWarps][kRowBlock];
-  __shared__ float part;
-  __shared__ bool last;
-  int r0, r1;
-  band(p.cov, r0, r1);
-  const uint64_t pol = l2_policy(p.keep_l2 != 0);
-  for (int s = 0; s < p.sweeps; ++s) {
-    const float *x_in = p.ptrs[p.idx[s][0]];
-    float *x_out = p.ptrs[p.idx[s][1]];
-    const float cta = sweep_ldg<KC, G, kChain>(p.n, r0, r1, p.A, p.b, x_in, x_out, red, &part, pol);
-    if (kChain) {
-      float *slot = partials + (s & 1) * kMaxJacobiBlocks;
-      if (threadIdx.x == 0) slot[blockIdx.x] = cta;
-      grid_barrier(sync + 1, sync + 2);
-      if (blockIdx.x == 0 && threadIdx.x < 32) finish_resid(slot, gridDim.x, p.ptrs[p.idx[s][2] & 0x7f]);
-    } else {
-      if (threadIdx.x == 0) {
-        partials[blockIdx.x] = cta;
-        __threadfence();
-        last = atomicAdd(sync, 1u) == gridDim.x - 1;
-      }
-      __syncthreads();
-      if (last && threadIdx.x < 32) {
-        __threadfence();
-        finish_resid(partials, gridDim.x, p.ptrs[p.idx[s][2] & 0x7f]);
-        if (threadIdx.x == 0) *sync = 0u;
-      }
-    }
-  }
-}
 
 // ---- row-per-warp direct kernel ----------------------------------------------
 //
@@ -1504,76 +1124,11 @@ bool rows_prefetch() {
 }
 
 bool use_rows_kernel(int n) {
-  const char *e = getenv("KAAS_JACOBI_PATH");  // dev A/B: rows (default) | ldg | tma
-  if (e && (e[0] == 'l' || e[0] == 't')) return false;
+  const char *e = getenv("KAAS_JACOBI_PATH");  // dev A/B: rows (default) | generic
+  if (e && e[0] == 'g') return false;
   return n % 4 == 0 && (size_t)n * 4 <= 160 * 1024;
 }
 
-// KC = float4 chunks per lane (x registers), 0 = direct path not applicable
-int ldg_kc(int n) {
-  if (const char *e = getenv("KAAS_JACOBI_PATH"))  // dev A/B: "tma" forces the staged kernel
-    if (e[0] == 't' || e[0] == 'r') return 0;
-  if (n % 4 != 0) return 0;
-  const int chunks = (n + 127) / 128;
-  const int per = (chunks + kLdgWarps - 1) / kLdgWarps;
-  if (per <= 1) return 1;
-  if (per <= 2) return 2;
-  if (per <= 4) return 4;
-  if (per <= 8) return 8;
-  return 0;
-}
-
-template <bool kChain>
-const void *ldg_kernel(int kc) {
-  switch (kc) {
-    case 1: return (const void *)k_jacobi_ldg<1, 8, kChain>;
-    case 2: return (const void *)k_jacobi_ldg<2, 8, kChain>;
-    case 4: return (const void *)k_jacobi_ldg<4, 4, kChain>;
-    default: return (const void *)k_jacobi_ldg<8, 2, kChain>;
-  }
-}
-
-// stages that fit in smem (0 = TMA path not applicable)
-int tma_stages(int n, int max_smem) {
-  if (n % 4 != 0 || n <= 0) return 0;
-  const size_t row = (size_t)n * 4, xbytes = (size_t)((n + 31) & ~31) * 4;
-  const size_t fixed = xbytes + 2 * kTmaMaxStages * 8 + kTmaConsumers * 4 + 256;
-  if (fixed + 2 * row > (size_t)max_smem) return 0;
-  int s = (int)(((size_t)max_smem - fixed) / row);
-  int cap = kTmaMaxStages;
-  if (const char *e = getenv("KAAS_JACOBI_STAGES")) cap = atoi(e) > 1 ? atoi(e) : cap;  // dev A/B
-  if (cap > kTmaMaxStages) cap = kTmaMaxStages;
-  return s > cap ? cap : s;
-}
-
-// x-register chunks: 32 for n <= 4096, 16 for n <= 2048, ... 0 (smem x) above 4096
-// (KAAS_JACOBI_XREG=0 forces x from smem; dev A/B switch)
-int tma_xr(int n) {
-  const char *e = getenv("KAAS_JACOBI_XREG");
-  if (e && e[0] == '0') return 0;
-  const int c = (n + 127) / 128;
-  if (c <= 8) return 8;
-  if (c <= 16) return 16;
-  if (c <= 32) return 32;
-  return 0;
-}
-
-template <bool kChain>
-const void *tma_kernel(int xr) {
-  switch (xr) {
-    case 8: return (const void *)k_jacobi_tma<kChain, 8>;
-    case 16: return (const void *)k_jacobi_tma<kChain, 16>;
-    case 32: return (const void *)k_jacobi_tma<kChain, 32>;
-    default: return (const void *)k_jacobi_tma<kChain, 0>;
-  }
-}
-
-size_t tma_smem(int n, int stages) {
-  return (size_t)((n + 31) & ~31) * 4 + (size_t)stages * n * 4 + 2 * kTmaMaxStages * 8 +
-         kTmaConsumers * 4 + 128;
-}
-
-// chunks-per-warp template selector: 0 = scalar path
 int pick_kc(int n) {
   if (n % 4 != 0) return 0;
   const int chunks = (n + kChunk - 1) / kChunk;
@@ -1618,55 +1173,6 @@ int launch_jacobi(cudaStream_t s, int dev, int n, uint64_t cov, const float *A, 
     count_launch();
     return 0;
   }
-  const int kcl = ldg_kc(n);
-  if (kcl > 0 && aligned16(A) && aligned16(x_in)) {
-    static thread_local ChainParams p;
-    p.A = A;
-    p.b = b;
-    p.n = n;
-    p.cov = (int)cov;
-    p.sweeps = 1;
-    p.keep_l2 = 0;
-    p.ptrs[0] = const_cast<float *>(x_in);
-    p.ptrs[1] = x_out;
-    p.ptrs[2] = resid;
-    p.idx[0][0] = 0;
-    p.idx[0][1] = 1;
-    p.idx[0][2] = 2;
-    float *partials = sc->jac_partials;
-    unsigned *sync = sc->jac_sync;
-    void *args[] = {(void *)&p, (void *)&partials, (void *)&sync};
-    KAAS_CUDA(cudaLaunchKernel(ldg_kernel<false>(kcl), dim3(blocks), dim3(kLdgThreads), args, 0, s));
-    count_launch();
-    return 0;
-  }
-  const int stages = tma_stages(n, device_props(dev).max_smem_optin);
-  if (stages >= 2 && aligned16(A) && aligned16(x_in)) {
-    static thread_local ChainParams p;
-    p.A = A;
-    p.b = b;
-    p.n = n;
-    p.cov = (int)cov;
-    p.sweeps = 1;
-    p.keep_l2 = 0;
-    p.ptrs[0] = const_cast<float *>(x_in);
-    p.ptrs[1] = x_out;
-    p.ptrs[2] = resid;
-    p.idx[0][0] = 0;
-    p.idx[0][1] = 1;
-    p.idx[0][2] = 2;
-    const size_t smem = tma_smem(n, stages);
-    const void *fn = tma_kernel<false>(tma_xr(n));
-    KAAS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int st = stages;
-    float *partials = sc->jac_partials;
-    unsigned *sync = sc->jac_sync;
-    void *args[] = {(void *)&p, (void *)&st, (void *)&partials, (void *)&sync};
-    KAAS_CUDA(cudaLaunchKernel(fn, dim3(blocks), dim3(kTmaThreads), args, smem, s));
-    count_launch();
-    KAAS_CUDA(cudaGetLastError());
-    return 0;
-  }
   int kc = pick_kc(n);
   if (!aligned16(A) || !aligned16(x_in)) kc = 0;
   if (kc < 0) kc = 0;
@@ -1703,18 +1209,6 @@ int launch_jacobi_chain(cudaStream_t s, int dev, const JacobiChain &c, StreamScr
                                   : (const void *)k_jacobi_rows<true, false>);
   if (use_rows)
     KAAS_CUDA(cudaFuncSetAttribute(rfn, cudaFuncAttributeMaxDynamicSharedMemorySize, c.n * 4));
-  const int kcl = use_rows ? 0 : ldg_kc(c.n);
-  bool use_ldg = kcl > 0 && aligned16(c.A);
-  for (int t = 0; t < c.sweeps && use_ldg; ++t)
-    if (!aligned16(c.x_in[t])) use_ldg = false;
-  const int stages = tma_stages(c.n, device_props(dev).max_smem_optin);
-  bool use_tma = !use_ldg && stages >= 2 && aligned16(c.A);
-  for (int t = 0; t < c.sweeps && use_tma; ++t)
-    if (!aligned16(c.x_in[t])) use_tma = false;
-  const size_t tsmem = use_tma ? tma_smem(c.n, stages) : 0;
-  const void *tfn = tma_kernel<true>(tma_xr(c.n));
-  if (use_tma)
-    KAAS_CUDA(cudaFuncSetAttribute(tfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem));
   const void *fn = kc == 1 ? (const void *)k_jacobi_chain<1>
                  : kc == 2 ? (const void *)k_jacobi_chain<2>
                  : kc == 4 ? (const void *)k_jacobi_chain<4>
@@ -1799,14 +1293,6 @@ int launch_jacobi_chain(cudaStream_t s, int dev, const JacobiChain &c, StreamScr
       void *rargs[] = {(void *)&p, (void *)&partials, (void *)&sync};
       KAAS_CUDA(cudaLaunchCooperativeKernel(rfn, dim3(blocks),
                                             dim3(rows_threads(dev, c.cov)), rargs, (size_t)c.n * 4, s));
-    } else if (use_ldg) {
-      void *largs[] = {(void *)&p, (void *)&partials, (void *)&sync};
-      KAAS_CUDA(cudaLaunchCooperativeKernel(ldg_kernel<true>(kcl), dim3(blocks), dim3(kLdgThreads),
-                                            largs, 0, s));
-    } else if (use_tma) {
-      int st = stages;
-      void *targs[] = {(void *)&p, (void *)&st, (void *)&partials, (void *)&sync};
-      KAAS_CUDA(cudaLaunchCooperativeKernel(tfn, dim3(blocks), dim3(kTmaThreads), targs, tsmem, s));
     } else {
       void *args[] = {(void *)&p, (void *)&partials, (void *)&sync};
       KAAS_CUDA(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(kJacThreads), args, 0, s));

@@ -57,7 +57,7 @@ int main(void) {
 
 
 def test_sass_contains_blackwell_instructions():
-    """tcgen05 MMA, TMEM loads and TMA bulk/tensor copies are in the cubin."""
+    """tcgen05 MMA, TMEM loads/stores and TMA tensor copies are in the cubin."""
     try:
         out = subprocess.run(["cuobjdump", "-sass", native.LIB_PATH], capture_output=True,
                              text=True, timeout=120).stdout
@@ -66,7 +66,8 @@ def test_sass_contains_blackwell_instructions():
     assert "UTCHMMA" in out        # tcgen05.mma kind::tf32
     assert "LDTM" in out           # tcgen05.ld
     assert "UTMALDG" in out        # cp.async.bulk.tensor (cGEMM operands)
-    assert "UBLKCP" in out         # cp.async.bulk (Jacobi rows)
+    assert "STTM" in out           # tcgen05.st (Jacobi band of A into TMEM)
+    assert "LDG.E.ENL2.256" in out  # 256-bit tagged-x polls (Jacobi exchange)
     assert "sm_100a" in subprocess.run(["cuobjdump", "-lelf", native.LIB_PATH], capture_output=True,
                                        text=True).stdout
 
