@@ -282,6 +282,52 @@ def measure_mixed(device, clients=16, count=160, policy="affinity:8", capacity=5
             "evictions": evictions, "device_busy_frac": (ex.dev_stats.device_ms - dev0) / (wall * 1e3)}
 
 
+def measure_peer_fill(device, n=8192, reps=2):
+    """Cache fills from a peer executor: executor 0 fetches the
+    const A, B of a cGEMM 8192^3 request over PCIe (cold H2D); executor 1 then
+    serves the same request and fills both from executor 0's copies with
+    cudaMemcpyPeerAsync -- NVLink when a second GPU is visible, an HBM D2D
+    copy between two executors sharing this GPU otherwise.  Decisions and
+    statistics are the reference's either way (both are store fetches)."""
+    from paper_2212_08146_b200 import native
+    from paper_2212_08146_b200 import workloads as W
+    from paper_2212_08146_b200.hoststore import PinnedStore
+    from paper_2212_08146_b200.pool import KaasService
+    ngpu = native.device_count()
+    devs = [device, (device + 1) % ngpu] if ngpu > 1 else [device, device]
+    store = PinnedStore()
+    for r in range(reps):
+        W.seed_cgemm(store, n, prefix=f"pf{r}", seed=300 + r)
+    cap = 16 * n * n * 8
+    h2d, p2p = [], []
+    with KaasService(store, n_executors=2, capacity=cap, policy="rr", devices=devs,
+                     reserve_bytes=cap + 8 * 8 * n * n) as svc:
+        e0, e1 = svc.executors
+        for r in range(reps):
+            def req(tag):
+                return W.cgemm_request(f"pf{r}/{tag}", n, f"pf{r}/A/{n}", f"pf{r}/B/{n}", f"pf{r}/C")
+            got = {}
+            for tag in ("a", "b"):  # rr: one request per executor
+                before = {id(e): (e.dev_stats.h2d_ms, e.dev_stats.h2d_bytes, e.dev_stats.p2p_bytes)
+                          for e in (e0, e1)}
+                resp = svc.submit(req(tag))
+                assert resp.status.ok and resp.io_stats.store_gets == 2, resp
+                for e in (e0, e1):
+                    ms0, hb0, pb0 = before[id(e)]
+                    if e.dev_stats.h2d_ms != ms0:
+                        got[tag] = (e.dev_stats.h2d_ms - ms0, e.dev_stats.h2d_bytes - hb0,
+                                    e.dev_stats.p2p_bytes - pb0)
+            (ms_a, hb_a, _), (ms_b, _, pb_b) = got["a"], got["b"]
+            h2d.append(hb_a / (ms_a * 1e6))
+            p2p.append(pb_b / (ms_b * 1e6))
+    return {"workload": f"cgemm {n}^3 request served by executor 0 (cold: A, B over PCIe) then by "
+                        f"executor 1 (A, B filled from executor 0's cached copies)",
+            "peer_path": "NVLink P2P" if devs[0] != devs[1] else "same-GPU D2D (one GPU visible)",
+            "fill_bytes": 2 * 8 * n * n,
+            "h2d_gbs": statistics.median(h2d), "p2p_gbs": statistics.median(p2p),
+            "p2p_over_h2d": statistics.median(p2p) / statistics.median(h2d)}
+
+
 def measure_resnet(device, steps=5):
     """BASELINE configs[4]: ResNet-50-shaped chain (53 bit-exact conv-as-GEMM
     matmuls + residual adds, batch 1), const weights, ephemeral activations."""
@@ -363,6 +409,7 @@ def ours(args, rank, world, local_rank, dist):
             extras["cgemm8192"] = measure_cgemm(8192, 5, local_rank, True)
             extras["mixed"] = measure_mixed(local_rank)
             extras["resnet50_chain"] = measure_resnet(local_rank)
+            extras["peer_fill"] = measure_peer_fill(local_rank)
             for key in ("cgemm1024", "cgemm8192"):
                 e = extras[key]
                 e["roofline"] = {
