@@ -441,8 +441,8 @@ def ours(args, rank, world, local_rank, dist):
                 "global_batch": world, "seq_len": None,
                 "parallelism": f"request-sharded x{world} (no collective)",
                 "l2": "256 MiB memset flushes L2 before every timed request (outside the timed spans); "
-                      "within a request A (64 MiB) is re-read by all 500 sweeps and stays L2-resident "
-                      "(evict_last) -- that reuse is the kernel's design",
+                      "within a request A (64 MiB) is read from HBM once and held in TMEM, registers "
+                      "and shared memory for all 500 sweeps -- that reuse is the kernel's design",
             },
             "p50_ms": percentile(lat, 0.5) * 1e3,
             "p99_ms": percentile(lat, 0.99) * 1e3,

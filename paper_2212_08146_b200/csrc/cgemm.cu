@@ -26,6 +26,7 @@
 //      overlaps the main loop of tile t+1.
 #include <cuda.h>
 
+#include <atomic>
 #include <cstdlib>
 
 #include "kaas_internal.cuh"
@@ -669,8 +670,12 @@ template <int BN>
 int launch_gemm2(cudaStream_t s, int dev, const CUtensorMap &ma, const CUtensorMap &mb,
                  const GemmShape &shape, float *C, StreamScratch *sc, const ProgressiveOut *po) {
   const size_t smem = sizeof(Smem2<BN>) + 1024;
-  KAAS_CUDA(cudaFuncSetAttribute(k_cgemm_fused4<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
+  static std::atomic<uint64_t> attr_done{0};  // bit per device (dev < 64)
+  if (!(attr_done.load(std::memory_order_relaxed) >> (dev & 63) & 1)) {
+    KAAS_CUDA(cudaFuncSetAttribute(k_cgemm_fused4<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
+    attr_done.fetch_or(1ull << (dev & 63));
+  }
   const int units = shape.num_m * shape.num_n * shape.ksplit;
   int grid = device_props(dev).sm_count;
   if (grid > units) grid = units;
@@ -678,11 +683,11 @@ int launch_gemm2(cudaStream_t s, int dev, const CUtensorMap &ma, const CUtensorM
   WaitValue32Fn waitv = get_wait_value();
   const bool progressive = po != nullptr && waitv != nullptr && npanels > 1 &&
                            npanels <= kMaxPanels && sc->panel_done != nullptr;
-  cudaEvent_t ev_ready = nullptr, ev_done = nullptr;
-  if (po) {
-    KAAS_CUDA(cudaEventCreateWithFlags(&ev_ready, cudaEventDisableTiming));
-    KAAS_CUDA(cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming));
+  if (po && !sc->cg_ev_ready) {
+    KAAS_CUDA(cudaEventCreateWithFlags(&sc->cg_ev_ready, cudaEventDisableTiming));
+    KAAS_CUDA(cudaEventCreateWithFlags(&sc->cg_ev_done, cudaEventDisableTiming));
   }
+  cudaEvent_t ev_ready = sc->cg_ev_ready, ev_done = sc->cg_ev_done;
   if (progressive) {
     KAAS_CUDA(cudaMemsetAsync(sc->panel_done, 0, npanels * sizeof(unsigned), s));
     KAAS_CUDA(cudaEventRecord(ev_ready, s));
@@ -715,8 +720,6 @@ int launch_gemm2(cudaStream_t s, int dev, const CUtensorMap &ma, const CUtensorM
   if (copied < po->bytes)
     KAAS_CUDA(cudaMemcpyAsync((char *)po->host + copied, (const char *)C + copied,
                               po->bytes - copied, cudaMemcpyDeviceToHost, po->out_stream));
-  cudaEventDestroy(ev_ready);
-  cudaEventDestroy(ev_done);
   return 0;
 }
 

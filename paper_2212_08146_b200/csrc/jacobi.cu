@@ -27,6 +27,7 @@
 // persistent launch per request instead of 500.
 #include <cooperative_groups.h>
 
+#include <atomic>
 #include <cstdlib>
 
 #include "kaas_internal.cuh"
@@ -1284,7 +1285,11 @@ int launch_jacobi_chain(cudaStream_t s, int dev, const JacobiChain &c, StreamScr
       const bool tm = use_tmem_kernel();
       const void *cfn = tm ? (const void *)k_jacobi_tmem : (const void *)k_jacobi_cols;
       const size_t csmem = tm ? kTmSmem : kColSmem;
-      KAAS_CUDA(cudaFuncSetAttribute(cfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
+      static std::atomic<uint64_t> attr_done[2];  // per kernel, bit per device (dev < 64)
+      if (!(attr_done[tm].load(std::memory_order_relaxed) >> (dev & 63) & 1)) {
+        KAAS_CUDA(cudaFuncSetAttribute(cfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
+        attr_done[tm].fetch_or(1ull << (dev & 63));
+      }
       KAAS_CUDA(cudaMemsetAsync(sync + 3, 0, sizeof(unsigned), s));  // monotonic barrier counter
       void *cargs[] = {(void *)&p, (void *)&partials, (void *)&sync};
       KAAS_CUDA(cudaLaunchCooperativeKernel(cfn, dim3(blocks), dim3(kColT), cargs, csmem, s));

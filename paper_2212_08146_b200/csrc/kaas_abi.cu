@@ -327,15 +327,32 @@ static int jacobi_run_length(const kaas_launch_desc *d, const Plan *plans, int i
     const uint64_t A = e.ptrs[0], b = e.ptrs[1], xi = e.ptrs[2], xo = e.ptrs[3], r = e.ptrs[4];
     if (xo == xi || xo == A || xo == b || r == A || r == b || r == xi || r == xo) break;
   }
+  // residual slots must not be read (as x_in) or written (as x_out) by any
+  // sweep of the run: the run ends before the first sweep that conflicts
+  // with itself or an earlier one.  A run touches only a handful of distinct
+  // buffers, so the seen-sets are short vectors (linear in the run length;
+  // the all-pairs check cost ~140 us of host time per 500-sweep request).
+  std::vector<uint64_t> xs, rs;
+  auto has = [](const std::vector<uint64_t> &v, uint64_t q) {
+    for (uint64_t e : v)
+      if (e == q) return true;
+    return false;
+  };
+  auto add = [&](std::vector<uint64_t> &v, uint64_t q) {
+    if (!has(v, q)) v.push_back(q);
+  };
   int len = j - i;
-  // residual slots must not be read (as x_in) or written (as x_out) by any sweep of the run
-  for (int a = i; a < i + len; ++a)
-    for (int c = i; c < i + len; ++c)
-      if (d[a].ptrs[4] == d[c].ptrs[2] || d[a].ptrs[4] == d[c].ptrs[3]) {
-        len = (a > c ? a : c) - i;  // cut before the conflict
-        if (len < 1) len = 1;
-      }
-  return len;
+  for (int t = i; t < i + len; ++t) {
+    const uint64_t xi = d[t].ptrs[2], xo = d[t].ptrs[3], r = d[t].ptrs[4];
+    add(xs, xi);
+    add(xs, xo);
+    if (has(xs, r) || has(rs, xi) || has(rs, xo)) {
+      len = t - i;
+      break;
+    }
+    add(rs, r);
+  }
+  return len < 1 ? 1 : len;
 }
 
 static int coop_serialise_begin(int dev, cudaStream_t s) {
@@ -481,6 +498,8 @@ int kaas_stream_destroy(uint64_t stream) {
     if (sc->cg_buf) cudaFreeAsync(sc->cg_buf, s);
     cudaStreamSynchronize(s);
     if (sc->panel_done) cudaFree(sc->panel_done);
+    if (sc->cg_ev_ready) cudaEventDestroy(sc->cg_ev_ready);
+    if (sc->cg_ev_done) cudaEventDestroy(sc->cg_ev_done);
     delete sc;
   }
   KAAS_CUDA(cudaStreamDestroy(s));

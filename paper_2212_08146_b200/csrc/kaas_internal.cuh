@@ -38,6 +38,8 @@ struct StreamScratch {
   // Jacobi column kernel: x published as (value, tag) words, ping-pong
   unsigned long long *jac_xt = nullptr;  // [2][kJacTaggedMaxN], zeroed at creation
   unsigned jac_tag = 1;                  // next launch's tag base (host side, stream-ordered)
+  // cGEMM write-back ordering events, created on first use, reused per launch
+  cudaEvent_t cg_ev_ready = nullptr, cg_ev_done = nullptr;
 };
 constexpr int kJacTaggedMaxN = 4096;
 constexpr int kMaxPanels = 1024;
