@@ -1208,16 +1208,12 @@ int launch_jacobi_chain(cudaStream_t s, int dev, const JacobiChain &c, StreamScr
                                   : (const void *)k_jacobi_rows<true, false, true>)
                             : (pf ? (const void *)k_jacobi_rows<true, true>
                                   : (const void *)k_jacobi_rows<true, false>);
-  if (use_rows)
-    KAAS_CUDA(cudaFuncSetAttribute(rfn, cudaFuncAttributeMaxDynamicSharedMemorySize, c.n * 4));
   const void *fn = kc == 1 ? (const void *)k_jacobi_chain<1>
                  : kc == 2 ? (const void *)k_jacobi_chain<2>
                  : kc == 4 ? (const void *)k_jacobi_chain<4>
                            : (const void *)k_jacobi_chain<0>;
   // Keep A resident in L2 across sweeps when it fits comfortably.
-  int l2 = 0;
-  cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
-  const bool keep = (double)c.n * c.n * 4.0 <= 0.75 * (double)l2;
+  const bool keep = (double)c.n * c.n * 4.0 <= 0.75 * (double)device_props(dev).l2_bytes;
   int done = 0;
   while (done < c.sweeps) {
     static thread_local ChainParams p;  // ~6 KB: keep it off the stack
@@ -1294,6 +1290,7 @@ int launch_jacobi_chain(cudaStream_t s, int dev, const JacobiChain &c, StreamScr
       void *cargs[] = {(void *)&p, (void *)&partials, (void *)&sync};
       KAAS_CUDA(cudaLaunchCooperativeKernel(cfn, dim3(blocks), dim3(kColT), cargs, csmem, s));
     } else if (use_rows) {
+      KAAS_CUDA(cudaFuncSetAttribute(rfn, cudaFuncAttributeMaxDynamicSharedMemorySize, c.n * 4));
       KAAS_CUDA(cudaMemsetAsync(sync + 3, 0, sizeof(unsigned), s));  // monotonic barrier counter
       void *rargs[] = {(void *)&p, (void *)&partials, (void *)&sync};
       KAAS_CUDA(cudaLaunchCooperativeKernel(rfn, dim3(blocks),

@@ -52,6 +52,7 @@ const DeviceProps &device_props(int dev) {
   cudaDeviceGetAttribute(&p.max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   cudaDeviceGetAttribute(&p.cc_major, cudaDevAttrComputeCapabilityMajor, dev);
   cudaDeviceGetAttribute(&p.cc_minor, cudaDevAttrComputeCapabilityMinor, dev);
+  cudaDeviceGetAttribute(&p.l2_bytes, cudaDevAttrL2CacheSize, dev);
   return g_props.emplace(dev, p).first->second;
 }
 
@@ -673,6 +674,13 @@ int kaas_launch_batch_ex(int dev, uint64_t stream, const kaas_launch_desc *descs
   KAAS_CUDA(cudaSetDevice(dev));
   std::vector<Plan> plans((size_t)n);
   for (int i = 0; i < n; ++i) {
+    // a plan depends on everything but the pointers: a run of identical
+    // invocations (a Jacobi chain's 500 sweeps) is validated once
+    if (i > 0 && std::memcmp(&descs[i], &descs[i - 1], offsetof(kaas_launch_desc, ptrs)) == 0 &&
+        std::memcmp(descs[i].sizes, descs[i - 1].sizes, sizeof(descs[i].sizes)) == 0) {
+      plans[i] = plans[i - 1];
+      continue;
+    }
     int rc = plan_launch(&descs[i], &plans[i]);
     if (rc) {
       set_error("invocation " + std::to_string(i) + ": " + t_last_error);

@@ -59,6 +59,7 @@ struct DeviceProps {
   int sm_count = 148;
   int max_smem_optin = 227 * 1024;
   int cc_major = 10, cc_minor = 0;
+  int l2_bytes = 126 << 20;
 };
 const DeviceProps &device_props(int dev);
 
