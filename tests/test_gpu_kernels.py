@@ -345,3 +345,15 @@ def test_jacobi_onchip_kernels_agree(gpu, path, monkeypatch):
     g = np.frombuffer(store.get(f"jk/x-{path}"), "<f4").astype(np.float64)
     o = np.frombuffer(ostore.get(f"jk/x-{path}"), "<f4").astype(np.float64)
     assert np.abs(g - o).max() <= 1e-5
+
+
+def test_cgemm_split_k_deterministic(gpu):
+    """Small fully-covered problems split K over two CTAs that red.add onto a
+    zeroed C; with exactly two partials the sum is order-independent, so
+    repeated runs are bit-identical (and within tolerance)."""
+    ex, store = gpu
+    outs = []
+    for rep in range(3):
+        _cgemm_check(ex, store, 512, 512, 512, seed=5)
+        outs.append(bytes(store.get("cg/C")))
+    assert outs[0] == outs[1] == outs[2]
