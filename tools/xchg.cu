@@ -46,7 +46,9 @@ __global__ void __launch_bounds__(T, 1) xchg(unsigned long long *xt, int sweeps,
     if (s > 0) {
       unsigned pending = 0xf;
       ulonglong2 q[4][2];
+      unsigned spins = 0;
       while (pending) {
+        if (++spins > (1u << 24)) __trap();  // never hang the box
 #pragma unroll
         for (int u = 0; u < 4; ++u)
           if (pending & (1u << u)) {
@@ -73,10 +75,11 @@ __global__ void __launch_bounds__(T, 1) xchg(unsigned long long *xt, int sweeps,
       }
     }
     __syncthreads();
-    if (warp == 0 && r0 + lane < r1) {
+    if (warp == 0) {
       const unsigned long long w = ((unsigned long long)(want + 1) << 32) | __float_as_uint(acc);
+      for (int row = r0 + lane; row < r1; row += 32)
 #pragma unroll
-      for (int r = 0; r < REP; ++r) st_rlx(xt + ((size_t)((s + 1) & 1) * REP + r) * N + r0 + lane, w);
+        for (int r = 0; r < REP; ++r) st_rlx(xt + ((size_t)((s + 1) & 1) * REP + r) * N + row, w);
     }
     if (MODE != 2) __syncthreads();
   }
@@ -97,6 +100,25 @@ int main(int argc, char **argv) {
   void *kern[] = {(void *)xchg<0>, (void *)xchg<1>, (void *)xchg<2>, (void *)xchg<0, 2>, (void *)xchg<0, 4>,
                   (void *)xchg<0, 8>, (void *)xchg<0, 16>};
   const char *names[] = {"relaxed", "ld.cg", "1 bar", "2 replicas", "4 replicas", "8 replicas", "16 replicas"};
+  const int grids[] = {sms, sms / 2, sms / 4, 16, 2};
+  for (int gi = 0; gi < 5; ++gi) {
+    const int g = grids[gi];
+    int delay = 0;
+    void *args[] = {&xt, (void *)&sweeps, &delay, &tag, &sink};
+    cudaLaunchCooperativeKernel(kern[0], g, T, args, 0, 0);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    tag += sweeps + 1;
+    cudaEventRecord(a);
+    cudaLaunchCooperativeKernel(kern[0], g, T, args, 0, 0);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    tag += sweeps + 1;
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    printf("relaxed, %3d CTAs (all 4096 words each): %.3f us/sweep\n", g, ms * 1e3 / sweeps);
+  }
   for (int mode = 0; mode < 7; ++mode)
   for (int delay : {0, 0, 1000}) {
     cudaEvent_t a, b;
