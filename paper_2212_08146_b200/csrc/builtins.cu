@@ -31,11 +31,38 @@ inline int elt_blocks(int dev, uint64_t work) {
 
 inline bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
 
+// Programmatic dependent launch: a request's builtin kernels run back to back
+// on one stream (ResNet chain: ~100 of them), so each is launched with
+// programmatic stream serialization and may be scheduled while its
+// predecessor drains.  Every such kernel waits (griddepcontrol.wait: the
+// previous grid has completed and its writes are visible) before touching
+// memory, and lets its own dependents launch once its main work is issued.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_release() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, (KArgs)args...);
+}
+
 // Exact aliasing (out == x or out == y) is safe: each element is read and
 // then written by the same thread, so no __restrict__ on these pointers.
 template <int kOp>  // 0 = add, 1 = saxpy, 2 = fill
 __global__ void __launch_bounds__(kEltThreads)
 k_elementwise_v4(uint64_t n4, float a, const float4 *x, const float4 *y, float4 *out) {
+  pdl_wait();
+  pdl_release();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
     float4 r;
@@ -60,6 +87,8 @@ template <int kOp>
 __global__ void __launch_bounds__(kEltThreads)
 k_elementwise_scalar(uint64_t begin, uint64_t end, float a, const float *x, const float *y,
                      float *out) {
+  pdl_wait();
+  pdl_release();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = begin + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < end; i += stride) {
     float r;
@@ -78,14 +107,14 @@ int launch_elementwise(cudaStream_t s, int dev, uint64_t cov, float a, const flo
   uint64_t done = 0;
   if (vec && cov >= 4) {
     const uint64_t n4 = cov / 4;
-    k_elementwise_v4<kOp><<<elt_blocks(dev, n4), kEltThreads, 0, s>>>(
-        n4, a, (const float4 *)x, (const float4 *)y, (float4 *)out);
+    KAAS_CUDA(launch_pdl(k_elementwise_v4<kOp>, dim3(elt_blocks(dev, n4)), dim3(kEltThreads), 0, s,
+                         n4, a, (const float4 *)x, (const float4 *)y, (float4 *)out));
     count_launch();
     done = n4 * 4;
   }
   if (done < cov) {
-    k_elementwise_scalar<kOp><<<elt_blocks(dev, cov - done), kEltThreads, 0, s>>>(
-        done, cov, a, x, y, out);
+    KAAS_CUDA(launch_pdl(k_elementwise_scalar<kOp>, dim3(elt_blocks(dev, cov - done)), dim3(kEltThreads), 0,
+                         s, done, cov, a, x, y, out));
     count_launch();
   }
   KAAS_CUDA(cudaGetLastError());
@@ -256,6 +285,7 @@ k_matmul(int n, int m, int k, uint64_t cov, const float *__restrict__ a,
 #pragma unroll
     for (int j = 0; j < TN; ++j) acc[i][j] = 0.0f;
 
+  pdl_wait();  // the operands may be the previous kernel's output
 #pragma unroll
   for (int t = 0; t < S - 1; ++t) {
     if (t < nk) issue(t);
@@ -305,6 +335,7 @@ k_matmul(int n, int m, int k, uint64_t cov, const float *__restrict__ a,
     }
   }
   cp_async_wait<0>();
+  pdl_release();
 #pragma unroll
   for (int i = 0; i < TM; ++i) {
     const int r = bm + ty + TY * i;
@@ -393,12 +424,10 @@ int launch_matmul(cudaStream_t s, int dev, uint64_t n, uint64_t m, uint64_t k, u
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, SM_));    \
       attr_done.fetch_or(1ull << (dev & 63));                                              \
     }                                                                                      \
-    if (a_vec)                                                                             \
-      k_matmul<TY, TX, TM, TN, S_, BK_, true><<<grid, (TY) * (TX), SM_, s>>>(              \
-          (int)n, (int)m, (int)k, cov, a, b, out);                                         \
-    else                                                                                   \
-      k_matmul<TY, TX, TM, TN, S_, BK_, false><<<grid, (TY) * (TX), SM_, s>>>(             \
-          (int)n, (int)m, (int)k, cov, a, b, out);                                         \
+    KAAS_CUDA(launch_pdl(a_vec ? k_matmul<TY, TX, TM, TN, S_, BK_, true>                   \
+                               : k_matmul<TY, TX, TM, TN, S_, BK_, false>,                   \
+                         grid, dim3((TY) * (TX)), SM_, s, (int)n, (int)m, (int)k, cov, a, b, \
+                         out));                                                            \
   } while (0)
   switch (best) {
     case 0: MM_LAUNCH(16, 16, 4, 4); break;
