@@ -30,7 +30,7 @@ __device__ __forceinline__ void st_rlx(unsigned long long *p, unsigned long long
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-template <int MODE, int REP = 1>
+template <int MODE, int REP = 1, int NCH = 4>
 __global__ void __launch_bounds__(T, 1) xchg(unsigned long long *xt, int sweeps, int delay, unsigned tag0,
                                               float *sink) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(T, 1) xchg(unsigned long long *xt, int sweeps,
     // L2 line is polled by ~148 / REP CTAs instead of all of them
     const unsigned long long *src = xt + ((size_t)(s & 1) * REP + blockIdx.x % REP) * N;
     if (s > 0) {
-      unsigned pending = 0xf;
+      unsigned pending = (1u << NCH) - 1u;
       ulonglong2 q[4][2];
       unsigned spins = 0;
       while (pending) {
@@ -100,6 +100,24 @@ int main(int argc, char **argv) {
   void *kern[] = {(void *)xchg<0>, (void *)xchg<1>, (void *)xchg<2>, (void *)xchg<0, 2>, (void *)xchg<0, 4>,
                   (void *)xchg<0, 8>, (void *)xchg<0, 16>};
   const char *names[] = {"relaxed", "ld.cg", "1 bar", "2 replicas", "4 replicas", "8 replicas", "16 replicas"};
+  {
+    void *half = (void *)xchg<0, 1, 2>;
+    int delay = 0;
+    void *args[] = {&xt, (void *)&sweeps, &delay, &tag, &sink};
+    cudaLaunchCooperativeKernel(half, sms, T, args, 0, 0);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    tag += sweeps + 1;
+    cudaEventRecord(a);
+    cudaLaunchCooperativeKernel(half, sms, T, args, 0, 0);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    tag += sweeps + 1;
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    printf("relaxed, %3d CTAs, each polling HALF of x (2048 words): %.3f us/sweep\n", sms, ms * 1e3 / sweeps);
+  }
   const int grids[] = {sms, sms / 2, sms / 4, 16, 2};
   for (int gi = 0; gi < 5; ++gi) {
     const int g = grids[gi];
