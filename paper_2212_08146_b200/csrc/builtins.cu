@@ -413,8 +413,11 @@ int launch_matmul(cudaStream_t s, int dev, uint64_t n, uint64_t m, uint64_t k, u
   const int a_vec = (k % 4 == 0) && aligned16(a);
 #define MM_LAUNCH(TY, TX, TM, TN)                                                          \
   do {                                                                                     \
-    constexpr int S_ = (TM) * (TN) >= 8 ? 4 : (TM) * (TN) >= 4 ? 6 : 8;                    \
-    constexpr int BK_ = (TM) * (TN) <= 2 ? 64 : 32;                                        \
+    /* ring: 4 x 32-k chunks for the big tiles; 3 x 64-k for the small ones, whose   \
+       CTAs are small and many -- a shallower ring keeps more of them resident      \
+       (measured over the ResNet-50 layers: 1364 -> 1207 us vs 6-8 stages) */       \
+    constexpr int S_ = (TM) * (TN) >= 8 ? 4 : 3;                                           \
+    constexpr int BK_ = (TM) * (TN) >= 8 ? 32 : 64;                                        \
     constexpr int SM_ = mm_smem_bytes<TY, TX, TM, TN, S_, BK_>();                          \
     static std::atomic<uint64_t> attr_done{0}; /* per device (dev < 64) */                  \
     if (!(attr_done.load(std::memory_order_relaxed) >> (dev & 63) & 1)) {                  \
