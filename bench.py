@@ -433,8 +433,11 @@ def ours(args, rank, world, local_rank, dist):
                     "bound": "tensor", "unit": "TFLOP/s",
                     "achieved": e["tf32_issued_tflops"],
                     "peak": peaks["bf16_tflops"] / 2,
-                    "peak_note": "TF32 dense = 1/2 of measured BF16 burst (MEASURED_PEAKS.json)",
+                    "peak_kind": peak_kind,
+                    "peak_note": "TF32 dense = 1/2 of the BF16 dense peak (MEASURED_PEAKS.json when "
+                                 "present, else the profiling recipe's fallback)",
                     "frac": e["tf32_issued_tflops"] / (peaks["bf16_tflops"] / 2),
+                    "traffic": profile_traffic(key),  # dram bytes per launch (ncu, cold L2)
                     "useful_tflops": e["useful_tflops"],
                 }
         cpu = cpu_baseline(seconds=args.cpu_seconds)
