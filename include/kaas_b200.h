@@ -55,6 +55,11 @@ extern "C" {
 #define KAAS_F_CG_B_USE 2
 #define KAAS_F_CG_A_FILL 4
 #define KAAS_F_CG_B_FILL 8
+/* kaas_launch_desc.flags for KAAS_K_MATMUL: ptrs[3] / sizes[3] hold an
+ * executor-owned buffer for B transposed ([m][k] f32, 4*m*k bytes) -- the
+ * prepared form of a const weight.  USE: it holds Bt; FILL: build it first. */
+#define KAAS_F_MM_BT_USE 16
+#define KAAS_F_MM_BT_FILL 32
 
 /* literal tags, protocol.py:27 LITERAL_TYPES order */
 #define KAAS_LIT_I32 0

@@ -184,17 +184,21 @@ constexpr int mm_smem_bytes() {
   return S * (TY * TM + TX * TN) * (BK + 4) * 4;
 }
 
-template <int TY, int TX, int TM, int TN, int S, int BK, bool AV>
+// BT: b is given transposed ([m][k], k-contiguous, 16-byte aligned rows --
+// the executor keeps that form of a const weight beside its cache entry), so
+// B is copied 16 bytes at a time like A instead of one 4-byte cp.async per
+// element (a third of the small-tile kernels' instructions went to those).
+template <int TY, int TX, int TM, int TN, int S, int BK, bool AV, bool BT>
 __global__ void __launch_bounds__(TY *TX)
 k_matmul(int n, int m, int k, uint64_t cov, const float *__restrict__ a,
          const float *__restrict__ b, float *__restrict__ out) {
-  constexpr bool a_vec = AV;  // 16-byte A copies (k % 4 == 0, a 16-byte aligned)
   constexpr int T = TY * TX, BM = TY * TM, BN = TX * TN, LD = BK + 4;
   constexpr int A_ST = BM * LD, B_ST = BN * LD;
   constexpr int NA4 = (BM * (BK / 4) + T - 1) / T;  // 16-byte A copies per thread
   constexpr int NA1 = (BM * BK + T - 1) / T;        // 4-byte A copies per thread
   static_assert(BM * BK % T == 0 && BK * BN % T == 0, "copy slots must tile the chunk");
-  constexpr int NB = (BK * BN + T - 1) / T;         // 4-byte B copies per thread
+  constexpr int NB = BT ? (BN * (BK / 4) + T - 1) / T  // 16-byte Bt copies per thread
+                        : (BK * BN + T - 1) / T;       // 4-byte B copies per thread
   extern __shared__ __align__(16) float mm_smem[];
   float *As = mm_smem, *Bs = mm_smem + S * A_ST;
   const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
@@ -227,14 +231,25 @@ k_matmul(int n, int m, int k, uint64_t cov, const float *__restrict__ a,
 #pragma unroll
   for (int u = 0; u < NB; ++u) {
     const int e = threadIdx.x + T * u;
-    const int kk = e / BN, c = e % BN;
-    const bool used = kk < BK;
-    const bool ok = used && bn + c < m;
-    kb[u] = used ? kk : -1;
-    sb[u] = used ? c * LD + kk : 0;  // B[k0 + kk][bn + c] -> Bs[c][kk]
-    bb[u] = ok ? 4 : 0;
-    pb[u] = ok ? b + (size_t)kk * m + bn + c : b;
-    step_b[u] = ok ? (size_t)BK * m : 0;
+    if (BT) {  // Bt[bn + c][k0 + kk .. +3] -> Bs[c][kk .. +3]
+      const int c = e / (BK / 4), kk = 4 * (e % (BK / 4));
+      const bool used = c < BN;
+      const bool ok = used && bn + c < m;
+      kb[u] = used ? kk : -1;
+      sb[u] = used ? c * LD + kk : 0;
+      bb[u] = ok ? 16 : 0;
+      pb[u] = ok ? b + (size_t)(bn + c) * k + kk : b;
+      step_b[u] = ok ? BK : 0;
+    } else {
+      const int kk = e / BN, c = e % BN;
+      const bool used = kk < BK;
+      const bool ok = used && bn + c < m;
+      kb[u] = used ? kk : -1;
+      sb[u] = used ? c * LD + kk : 0;  // B[k0 + kk][bn + c] -> Bs[c][kk]
+      bb[u] = ok ? 4 : 0;
+      pb[u] = ok ? b + (size_t)kk * m + bn + c : b;
+      step_b[u] = ok ? (size_t)BK * m : 0;
+    }
   }
   int stage_in = 0;  // stage the next issue() fills
   auto issue = [&](int t) {
@@ -250,8 +265,9 @@ k_matmul(int n, int m, int k, uint64_t cov, const float *__restrict__ a,
       }
 #pragma unroll
       for (int u = 0; u < NB; ++u) {
-        if (BK * BN % T != 0 && kb[u] < 0) continue;
-        cp_async4(bs + sb[u], pb[u], bb[u] != 0);
+        if ((BT ? BN * (BK / 4) : BK * BN) % T != 0 && kb[u] < 0) continue;
+        if (BT) cp_async16(bs + sb[u], pb[u], bb[u]);
+        else cp_async4(bs + sb[u], pb[u], bb[u] != 0);
       }
     } else {  // tail chunk: k bound per element
 #pragma unroll
@@ -269,8 +285,14 @@ k_matmul(int n, int m, int k, uint64_t cov, const float *__restrict__ a,
 #pragma unroll
       for (int u = 0; u < NB; ++u) {
         if (kb[u] < 0) continue;
-        const bool ok = bb[u] && k0 + kb[u] < k;
-        cp_async4(bs + sb[u], ok ? pb[u] : b, ok);
+        if (BT) {
+          const int left = k - (k0 + kb[u]);
+          const int bytes = (bb[u] && left > 0) ? (left >= 4 ? 16 : 4 * left) : 0;
+          cp_async16(bs + sb[u], bytes ? pb[u] : b, bytes);
+        } else {
+          const bool ok = bb[u] && k0 + kb[u] < k;
+          cp_async4(bs + sb[u], ok ? pb[u] : b, ok);
+        }
       }
     }
 #pragma unroll
@@ -374,11 +396,56 @@ int launch_reduce_sum(cudaStream_t s, int dev, uint64_t n, const float *x, float
   return 0;
 }
 
+// B [k][m] -> Bt [m][k] (32 x 32 smem tiles)
+__global__ void k_transpose_b(int k, int m, const float *__restrict__ b, float *__restrict__ bt) {
+  __shared__ float t[32][33];
+  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int r = r0 + i, c = c0 + threadIdx.x;
+    if (r < k && c < m) t[i][threadIdx.x] = b[(size_t)r * m + c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int c = c0 + i, r = r0 + threadIdx.x;
+    if (r < k && c < m) bt[(size_t)c * k + r] = t[threadIdx.x][i];
+  }
+}
+
 int launch_matmul(cudaStream_t s, int dev, uint64_t n, uint64_t m, uint64_t k, uint64_t cov,
-                  const float *a, const float *b, float *out) {
+                  const float *a, const float *b, float *out, StreamScratch *sc, const float *bt_prep,
+                  bool bt_ready) {
   if (n == 0 || m == 0 || cov == 0) return 0;
   if (n > 0x7fffffffu || m > 0x7fffffffu || k > 0x7fffffffu)
     return fail(KAAS_E_INVALID, "matmul extent exceeds i32");
+  // B transposed (16-byte B copies): from the executor's prepared-operand
+  // cache when it has one for this weight, else built into per-stream
+  // scratch for this launch (one extra pass over B)
+  const char *be = getenv("KAAS_MATMUL_BT");  // dev A/B: 0 = B as given
+  const bool use_bt = !(be && be[0] == '0') && k > 0 && k % 4 == 0 && aligned16(a);
+  auto transpose_into = [&](float *dst) -> int {
+    KAAS_CUDA(launch_pdl(k_transpose_b, dim3((unsigned)((m + 31) / 32), (unsigned)((k + 31) / 32)),
+                         dim3(32, 8), 0, s, (int)k, (int)m, b, dst));
+    count_launch();
+    return 0;
+  };
+  // a prepared buffer the executor asked to fill is always filled (it will
+  // be trusted as Bt by later launches), whether or not this one uses it
+  if (bt_prep && !bt_ready && k > 0) {
+    int rc = transpose_into(const_cast<float *>(bt_prep));
+    if (rc) return rc;
+    bt_ready = true;
+  }
+  const float *bt = nullptr;
+  if (use_bt) {
+    if (bt_prep) {
+      bt = bt_prep;
+    } else {
+      int rc = ensure_matmul_scratch(sc, s, (size_t)m * k * 4);
+      if (!rc) rc = transpose_into((float *)sc->mm_buf);
+      if (rc) return rc;
+      bt = (const float *)sc->mm_buf;
+    }
+  }
   // Cost model: a config's rate ~ (warps it can field, up to 2 per
   // scheduler) x (useful fraction of its tiles) / (instructions per MAC:
   // 2 FP + (TM + TN) / 4 LDS.128 per k + ~0.5 copy/loop overhead, per cell).
@@ -421,16 +488,19 @@ int launch_matmul(cudaStream_t s, int dev, uint64_t n, uint64_t m, uint64_t k, u
     constexpr int SM_ = mm_smem_bytes<TY, TX, TM, TN, S_, BK_>();                          \
     static std::atomic<uint64_t> attr_done{0}; /* per device (dev < 64) */                  \
     if (!(attr_done.load(std::memory_order_relaxed) >> (dev & 63) & 1)) {                  \
-      KAAS_CUDA(cudaFuncSetAttribute(k_matmul<TY, TX, TM, TN, S_, BK_, true>,              \
+      KAAS_CUDA(cudaFuncSetAttribute(k_matmul<TY, TX, TM, TN, S_, BK_, true, true>,        \
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, SM_));    \
-      KAAS_CUDA(cudaFuncSetAttribute(k_matmul<TY, TX, TM, TN, S_, BK_, false>,             \
+      KAAS_CUDA(cudaFuncSetAttribute(k_matmul<TY, TX, TM, TN, S_, BK_, true, false>,       \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, SM_));    \
+      KAAS_CUDA(cudaFuncSetAttribute(k_matmul<TY, TX, TM, TN, S_, BK_, false, false>,      \
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, SM_));    \
       attr_done.fetch_or(1ull << (dev & 63));                                              \
     }                                                                                      \
-    KAAS_CUDA(launch_pdl(a_vec ? k_matmul<TY, TX, TM, TN, S_, BK_, true>                   \
-                               : k_matmul<TY, TX, TM, TN, S_, BK_, false>,                   \
-                         grid, dim3((TY) * (TX)), SM_, s, (int)n, (int)m, (int)k, cov, a, b, \
-                         out));                                                            \
+    KAAS_CUDA(launch_pdl(bt ? k_matmul<TY, TX, TM, TN, S_, BK_, true, true>                \
+                            : a_vec ? k_matmul<TY, TX, TM, TN, S_, BK_, true, false>        \
+                                    : k_matmul<TY, TX, TM, TN, S_, BK_, false, false>,      \
+                         grid, dim3((TY) * (TX)), SM_, s, (int)n, (int)m, (int)k, cov, a,    \
+                         bt ? bt : b, out));                                               \
   } while (0)
   switch (best) {
     case 0: MM_LAUNCH(16, 16, 4, 4); break;

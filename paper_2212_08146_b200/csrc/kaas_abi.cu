@@ -62,6 +62,16 @@ StreamScratch *scratch_for(cudaStream_t s) {
   return it == g_scratch.end() ? nullptr : it->second;
 }
 
+int ensure_matmul_scratch(StreamScratch *sc, cudaStream_t s, size_t bytes) {
+  if (sc->mm_bytes >= bytes) return 0;
+  if (sc->mm_buf) KAAS_CUDA(cudaFreeAsync(sc->mm_buf, s));
+  sc->mm_buf = nullptr;
+  sc->mm_bytes = 0;
+  KAAS_CUDA(cudaMallocAsync(&sc->mm_buf, bytes, s));
+  sc->mm_bytes = bytes;
+  return 0;
+}
+
 int ensure_cgemm_scratch(StreamScratch *sc, cudaStream_t s, size_t bytes) {
   if (sc->cg_bytes >= bytes) return 0;
   if (sc->cg_buf) KAAS_CUDA(cudaFreeAsync(sc->cg_buf, s));
@@ -261,10 +271,18 @@ static int run_plan(int dev, cudaStream_t s, const kaas_launch_desc *d, const Pl
     case KAAS_K_REDUCE_SUM:
       rc = launch_reduce_sum(s, dev, n, (const float *)ptr[0], (float *)ptr[1]);
       break;
-    case KAAS_K_MATMUL:
+    case KAAS_K_MATMUL: {
+      const float *bt = nullptr;
+      bool bt_ready = false;
+      if (d->flags & (KAAS_F_MM_BT_USE | KAAS_F_MM_BT_FILL)) {
+        if (d->sizes[3] < p.ext[1] * p.ext[2] * 4) return fail(KAAS_E_BOUNDS, "matmul: prepared B buffer too small");
+        bt = (const float *)d->ptrs[3];
+        bt_ready = (d->flags & KAAS_F_MM_BT_USE) != 0;
+      }
       rc = launch_matmul(s, dev, n, p.ext[1], p.ext[2], p.cov, (const float *)ptr[0],
-                         (const float *)ptr[1], (float *)ptr[2]);
+                         (const float *)ptr[1], (float *)ptr[2], sc, bt, bt_ready);
       break;
+    }
     case KAAS_K_CGEMM: {
       if (n > 0x7fffffff || p.ext[1] > 0x7fffffff || p.ext[2] > 0x7fffffff)
         return fail(KAAS_E_BOUNDS, "cgemm: extent exceeds i32");
@@ -497,6 +515,7 @@ int kaas_stream_destroy(uint64_t stream) {
     if (sc->jac_sync) cudaFreeAsync(sc->jac_sync, s);
     if (sc->jac_xt) cudaFreeAsync(sc->jac_xt, s);
     if (sc->cg_buf) cudaFreeAsync(sc->cg_buf, s);
+    if (sc->mm_buf) cudaFreeAsync(sc->mm_buf, s);
     cudaStreamSynchronize(s);
     if (sc->panel_done) cudaFree(sc->panel_done);
     if (sc->cg_ev_ready) cudaEventDestroy(sc->cg_ev_ready);

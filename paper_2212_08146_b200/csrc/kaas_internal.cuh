@@ -38,6 +38,9 @@ struct StreamScratch {
   // Jacobi column kernel: x published as (value, tag) words, ping-pong
   unsigned long long *jac_xt = nullptr;  // [2][kJacTaggedMaxN], zeroed at creation
   unsigned jac_tag = 1;                  // next launch's tag base (host side, stream-ordered)
+  // bit-exact matmul: B transposed for one launch when no prepared copy exists
+  void *mm_buf = nullptr;
+  size_t mm_bytes = 0;
   // cGEMM write-back ordering events, created on first use, reused per launch
   cudaEvent_t cg_ev_ready = nullptr, cg_ev_done = nullptr;
 };
@@ -54,6 +57,7 @@ constexpr int kMaxJacobiBlocks = 4096;
 
 StreamScratch *scratch_for(cudaStream_t s);
 int ensure_cgemm_scratch(StreamScratch *sc, cudaStream_t s, size_t bytes);
+int ensure_matmul_scratch(StreamScratch *sc, cudaStream_t s, size_t bytes);
 
 struct DeviceProps {
   int sm_count = 148;
@@ -73,8 +77,11 @@ int launch_saxpy(cudaStream_t s, int dev, uint64_t cov, float a, const float *x,
                  const float *y, float *out);
 int launch_fill(cudaStream_t s, int dev, uint64_t cov, float v, float *out);
 int launch_reduce_sum(cudaStream_t s, int dev, uint64_t n, const float *x, float *out);
-int launch_matmul(cudaStream_t s, int dev, uint64_t n, uint64_t m, uint64_t k,
-                  uint64_t cov, const float *a, const float *b, float *out);
+// bt_prep: executor-owned buffer for B transposed ([m][k] f32) or nullptr;
+// bt_ready: it already holds that (else it is filled first)
+int launch_matmul(cudaStream_t s, int dev, uint64_t n, uint64_t m, uint64_t k, uint64_t cov,
+                  const float *a, const float *b, float *out, StreamScratch *sc,
+                  const float *bt_prep = nullptr, bool bt_ready = false);
 int launch_jacobi(cudaStream_t s, int dev, int n, uint64_t cov, const float *A,
                   const float *b, const float *x_in, float *x_out, float *resid,
                   StreamScratch *sc);

@@ -555,11 +555,19 @@ class GpuExecutor:
                 if not later and all(o[2] != nm for o in outs):
                     outs = [o for o in outs if o[2] != nm] + [(i, 2, nm)]
         p.stream_outs = tuple(outs)
-        # cgemm operands whose prepared forms may be cached: const inputs the
-        # request does not rewrite
+        # operands whose prepared forms may be cached: const inputs the request
+        # does not rewrite -- cgemm's split A / expanded B, matmul's Bt
         prep = []
         if p.fail_at is None:
             for i, (inv, kernel) in enumerate(zip(req.invocations, kernels)):
+                if kernel.kernel_id == "matmul":
+                    n_, m_, k_ = (lit.value for lit in inv.literals)
+                    if n_ * m_ * k_ == 0 or k_ % 4 or inv.dims.total_threads == 0:
+                        continue
+                    arg = by_name[inv.args[1]]
+                    if arg.is_const and not arg.is_ephemeral and arg.name not in dirty:
+                        prep.append((i, None, (arg.name, ("mm", k_, m_), 4 * m_ * k_)))
+                    continue
                 if kernel.kernel_id != "cgemm":
                     continue
                 n_, m_, k_ = (lit.value for lit in inv.literals)
@@ -752,6 +760,13 @@ class GpuExecutor:
                 name, key, nbytes = side
                 slot = self._derived_slot(resolved[name], key, nbytes)
                 if slot is None:
+                    continue
+                if key[0] == "mm":  # matmul: Bt in ptrs[3]
+                    descs["ptrs"][i, 3] = slot[0]
+                    descs["sizes"][i, 3] = nbytes
+                    flags |= native.F_MM_BT_USE if slot[2] else native.F_MM_BT_FILL
+                    if not slot[2]:
+                        filled.append(slot)
                     continue
                 descs["ptrs"][i, 3 + j] = slot[0]
                 descs["sizes"][i, 3 + j] = nbytes

@@ -95,6 +95,7 @@ _vp = C.c_void_p
 # name -> (argtypes) ; every function returns int
 # kaas_launch_desc.flags for cgemm (include/kaas_b200.h)
 F_CG_A_USE, F_CG_B_USE, F_CG_A_FILL, F_CG_B_FILL = 1, 2, 4, 8
+F_MM_BT_USE, F_MM_BT_FILL = 16, 32
 
 EXPORTS = {
     "kaas_last_error": [C.c_char_p, C.c_size_t],

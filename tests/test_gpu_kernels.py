@@ -357,3 +357,32 @@ def test_cgemm_split_k_deterministic(gpu):
         _cgemm_check(ex, store, 512, 512, 512, seed=5)
         outs.append(bytes(store.get("cg/C")))
     assert outs[0] == outs[1] == outs[2]
+
+
+@pytest.mark.parametrize("shape", [(49, 512, 256), (130, 70, 36), (7, 9, 4)])
+def test_matmul_const_weight_prepared_transpose(gpu, shape):
+    """A const B (a weight) is kept transposed beside its cache entry after
+    its first reuse: run 1 uses scratch, run 2 fills the prepared Bt, run 3
+    reads it -- all bit-exact, with and without full coverage."""
+    ex, store = gpu
+    n, m, k = shape
+    rng = np.random.default_rng(k)
+    a = (rng.standard_normal(n * k) * 3).astype("<f4")
+    b = (rng.standard_normal(k * m) * 3).astype("<f4")
+    tag = f"{n}_{m}_{k}"
+    store.put(f"mw/a{tag}", a.tobytes())
+    store.put(f"mw/w{tag}", b.tobytes())
+    ostore = DictStore({"a": a.tobytes(), "b": b.tobytes()})
+    for rep, cov in enumerate((n * m, n * m, max(1, n * m - 5), n * m)):
+        req = KaasRequest(f"mw{rep}", (BufferArg("a", a.nbytes, "input", key=f"mw/a{tag}"),
+                                       BufferArg("b", b.nbytes, "input", key=f"mw/w{tag}", is_const=True),
+                                       BufferArg("o", 4 * n * m, "output", key=f"mw/o{tag}")),
+                          (KernelInvocation("matmul", LaunchDims(grid_x=cov), (i32(n), i32(m), i32(k)),
+                                            ("a", "b", "o")),))
+        _run(ex, req)
+        oreq = KaasRequest("mw", (BufferArg("a", a.nbytes, "input", key="a"),
+                                  BufferArg("b", b.nbytes, "input", key="b", is_const=True),
+                                  BufferArg("o", 4 * n * m, "output", key="o")), req.invocations)
+        ostore.put("o", bytes(4 * n * m))
+        OracleExecutor(1 << 30, ostore).execute(oreq)
+        assert canon(store.get(f"mw/o{tag}")) == canon(ostore.get("o")), rep
