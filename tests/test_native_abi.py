@@ -76,3 +76,13 @@ def test_no_device_reports_zero_or_loads():
     # on the CPU build box there is no driver/device: count is 0, not an error
     n = native.device_count()
     assert n >= 0
+
+
+def test_flag_constants_match_header():
+    """native.py's descriptor flags are the header's #defines."""
+    import re
+    hdr = open(os.path.join(os.path.dirname(__file__), "..", "include", "kaas_b200.h")).read()
+    defs = {m.group(1): int(m.group(2)) for m in re.finditer(r"#define KAAS_(F_\w+) (\d+)", hdr)}
+    assert defs, "no flag defines found"
+    for name, value in defs.items():
+        assert getattr(native, name) == value, name
