@@ -14,7 +14,7 @@ from helpers import load_golden, replay, canon
 from oracle.executor import DictStore, OracleExecutor
 from oracle.kernels import KERNELS, OracleFault, k_cgemm, k_jacobi_sweep
 from oracle.router import OracleRouter
-from paper_2212_08146_b200.api import LaunchDims, ScalarLiteral, request_from_doc, i32
+from paper_2212_08146_b200.api import LaunchDims, ScalarLiteral, i32
 
 STREAMS = ["executor_fuzz31337.json.gz", "executor_fuzz77.json.gz",
            "executor_tight.json.gz", "executor_fuzzfa22.json.gz"]
