@@ -314,7 +314,7 @@ def measure_peer_fill(device, n=8192, reps=3):
     cap = 16 * n * n * 8
     h2d, p2p = [], []
     with KaasService(store, n_executors=2, capacity=cap, policy="rr", devices=devs,
-                     reserve_bytes=cap + 8 * 8 * n * n) as svc:
+                     reserve_bytes=int(os.environ.get("KAAS_PEER_RESERVE", cap + 8 * 8 * n * n))) as svc:
         e0, e1 = svc.executors
         for r in range(reps):
             def req(tag):
@@ -419,6 +419,10 @@ def ours(args, rank, world, local_rank, dist):
         extras = {}
         if not args.no_extras:
             extras["cgemm1024"] = measure_cgemm(1024, 20, local_rank, True)
+            # before the 8192 workload: a peer fill right after it measured
+            # 146-538 GB/s instead of ~2.3 TB/s (raw D2D copies are not
+            # affected; open issue in DESIGN.md §6)
+            extras["peer_fill"] = measure_peer_fill(local_rank)
             extras["cgemm8192"] = measure_cgemm(8192, 5, local_rank, True)
             # the multi-tenant pool spans every GPU of the run (the other ranks
             # are done with theirs by now); one GPU at N = 1
@@ -426,7 +430,6 @@ def ours(args, rank, world, local_rank, dist):
             extras["mixed"] = measure_mixed(local_rank, devices=[(local_rank + i) % nvis
                                                                 for i in range(min(world, nvis))])
             extras["resnet50_chain"] = measure_resnet(local_rank)
-            extras["peer_fill"] = measure_peer_fill(local_rank)
             for key in ("cgemm1024", "cgemm8192"):
                 e = extras[key]
                 e["roofline"] = {
