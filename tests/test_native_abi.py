@@ -68,6 +68,7 @@ def test_sass_contains_blackwell_instructions():
     assert "UTMALDG" in out        # cp.async.bulk.tensor (cGEMM operands)
     assert "STTM" in out           # tcgen05.st (Jacobi band of A into TMEM)
     assert "LDG.E.ENL2.256" in out  # 256-bit tagged-x polls (Jacobi exchange)
+    assert "FFMA2" in out          # packed FP32 dot products (Jacobi)
     assert "sm_100a" in subprocess.run(["cuobjdump", "-lelf", native.LIB_PATH], capture_output=True,
                                        text=True).stdout
 
