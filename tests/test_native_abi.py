@@ -87,3 +87,21 @@ def test_flag_constants_match_header():
     assert defs, "no flag defines found"
     for name, value in defs.items():
         assert getattr(native, name) == value, name
+
+
+def test_bit_exact_builtins_have_no_fused_multiply_add():
+    """matmul / saxpy must round the product and the sum separately (the
+    reference's numpy semantics): no FFMA/FFMA2 may appear in their SASS."""
+    try:
+        out = subprocess.run(["cuobjdump", "-sass", native.LIB_PATH], capture_output=True,
+                             text=True, timeout=120).stdout
+    except (OSError, subprocess.TimeoutExpired):
+        pytest.skip("cuobjdump unavailable")
+    funcs = re.split(r"\n\s*Function : ", out)
+    checked = 0
+    for f in funcs:
+        name = f.split("\n", 1)[0]
+        if "k_matmul" in name or "k_elementwise" in name:
+            checked += 1
+            assert not re.search(r"\bFFMA2?\b", f), name
+    assert checked >= 10
