@@ -1083,10 +1083,10 @@ k_jacobi_tmem(const __grid_constant__ ChainParams p, float *partials, unsigned *
       if (my_rl < R) {
         const float xn = (bi - tot) * rdi;
         const int i = r0 + my_rl;
-        x_out[i] = xn;
-        if (p.tagged)
+        if (p.tagged)  // the word the other CTAs wait for goes out first
           st_relaxed_u64(p.xt + (size_t)((s + 1) & 1) * kJacTaggedMaxN + i,
                          tagged_word(xn, p.tag0 + (unsigned)s + 1));
+        x_out[i] = xn;
         res = fabsf(xn - (from_tags ? xprev : __ldcg(x_in + i)));
         xprev = xn;
       }
