@@ -584,7 +584,7 @@ def reference_arm(args, rank, world):
         return None
     # warmup steps are untimed; each timed step is one request
     base = cpu_baseline(steps=args.steps, warmup=args.warmup, seconds=1e9)
-    threads, _ = cpu_threads()
+    threads = base["cores"]  # BLAS threads in effect during the run
     return {
         "impl": "reference",
         "metric": METRIC, "value": base["value"], "unit": "req/s", "n_gpus": world,
