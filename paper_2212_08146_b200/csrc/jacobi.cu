@@ -830,8 +830,9 @@ constexpr size_t kTmSmem = kTmTier > 116 * 1024 ? kTmTier : 116 * 1024;
                "r"(v[13]), "r"(v[14]), "r"(v[15])                                           \
                : "memory")
 
-// volatile so ptxas keeps the smem tier's loads where they are written
-// instead of hoisting the whole tier into registers at the top of the sweep
+// volatile so the compiler keeps the smem tier's loads where they are
+// written instead of hoisting the whole tier into registers at the top of
+// the sweep
 __device__ __forceinline__ float4 lds4(const float4 *q) {
   float4 a;
   asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
