@@ -473,6 +473,11 @@ int launch_matmul(cudaStream_t s, int dev, uint64_t n, uint64_t m, uint64_t k, u
     }
   }
   if (best_score < 0) return fail(KAAS_E_INVALID, "matmul: n too large for grid.y");
+  if (const char *fe = getenv("KAAS_MATMUL_CFG")) {  // dev: force a config (tools/mm_cfg_sweep.py)
+    const int f = atoi(fe);
+    const Cfg &c = cfgs[f < 0 ? 0 : f % (int)(sizeof(cfgs) / sizeof(cfgs[0]))];
+    if ((n + (uint64_t)c.ty * c.tm - 1) / ((uint64_t)c.ty * c.tm) <= 65535) best = f % (int)(sizeof(cfgs) / sizeof(cfgs[0]));
+  }
   const Cfg &c = cfgs[best];
   const unsigned gy = (unsigned)((n + c.ty * c.tm - 1) / (c.ty * c.tm));
   const unsigned gx = (unsigned)((m + c.tx * c.tn - 1) / (c.tx * c.tn));
