@@ -75,6 +75,13 @@ class KaasService:
         self.router = Router([e.executor_id for e in self.executors], policy,
                              digest_cap=digest_cap, log_decisions=log_decisions)
         self._queues = {e.executor_id: queue.Queue() for e in self.executors}
+        self._by_id = {e.executor_id: e for e in self.executors}
+        # a GPU executor is driven either by its worker thread or, when it is
+        # idle (nothing queued, nothing in flight), inline by a synchronous
+        # submit() -- saving two thread hand-offs (~40 us) per request; this
+        # lock says who owns it
+        self._owners = {e.executor_id: threading.Lock() for e in self.executors
+                        if hasattr(e, "begin")}
         self._threads = [threading.Thread(target=self._worker, args=(e,), daemon=True,
                                           name=f"kaas-executor-{e.executor_id}")
                          for e in self.executors]
@@ -108,14 +115,19 @@ class KaasService:
         order inside ``begin`` (bit-exact), puts and responses in ``complete``."""
         eid = executor.executor_id
         q = self._queues[eid]
+        owner = self._owners[eid]
         futs: dict[int, tuple] = {}
 
         def on_complete(rec, resp):
-            req, fut = futs.pop(rec.seq)
+            entry = futs.pop(rec.seq, None)
+            if entry is None:  # an inline submit(): the caller finishes it
+                return
+            req, fut = entry
             self.router.update_digest(eid, resp, req)
             fut.set_result(resp)
 
         executor.on_complete = on_complete
+        held = False
         while True:
             if executor.inflight:
                 executor.complete(block=False)
@@ -126,9 +138,15 @@ class KaasService:
                     executor.complete(through=next(iter(futs)))  # block on the oldest
                     continue
             else:
+                if held:  # idle: inline submits may drive the executor meanwhile
+                    owner.release()
+                    held = False
                 item = q.get()
+                owner.acquire()
+                held = True
             if item is None:
                 executor.complete()
+                owner.release()
                 return
             req, fut = item
             try:
@@ -160,7 +178,31 @@ class KaasService:
         return fut
 
     def submit(self, req: KaasRequest) -> KaasResponse:
-        return self.submit_async(req).result()
+        if self._closed:
+            raise RuntimeError("service is closed")
+        eid = self.router.route(req)
+        owner = self._owners.get(eid)
+        q = self._queues[eid]
+        if owner is not None and q.empty() and owner.acquire(blocking=False):
+            try:
+                ex = self._by_id[eid]
+                # idle and nobody queued ahead: this request is next in
+                # arrival order either way, so run it on this thread
+                if not ex.inflight and q.empty():
+                    try:
+                        resp = ex.execute(req)
+                    except BaseException as exc:
+                        failed = KaasResponse(req.request_id, Status.make_error("Internal", str(exc)))
+                        self.router.update_digest(eid, failed, req)
+                        raise
+                    self.router.update_digest(eid, resp, req)
+                    return resp
+            finally:
+                owner.release()
+        fut: Future = Future()
+        fut.executor_id = eid
+        q.put((req, fut))
+        return fut.result()
 
     def stats(self) -> dict:
         out = {"executors": [e.stats() for e in self.executors],
