@@ -124,6 +124,8 @@ int kaas_stream_wait_event(uint64_t stream, uint64_t event);
 int kaas_event_sync(uint64_t event);
 int kaas_event_query(uint64_t event, int *done);
 int kaas_event_elapsed_ms(uint64_t start, uint64_t end, float *ms);
+/* n (start, end) pairs in one crossing (a request's device-timing spans) */
+int kaas_event_elapsed_many(int n, const uint64_t *starts, const uint64_t *ends, float *ms);
 
 /* ---- device memory: DeviceBuffer.__init__ (executor.py:63-72) ---------- */
 int kaas_malloc_async(uint64_t stream, uint64_t bytes, uint64_t *dptr);

@@ -578,6 +578,13 @@ int kaas_event_elapsed_ms(uint64_t start, uint64_t end, float *ms) {
   return 0;
 }
 
+int kaas_event_elapsed_many(int n, const uint64_t *starts, const uint64_t *ends, float *ms) {
+  if (n < 0 || (n > 0 && (!starts || !ends || !ms))) return KAAS_E_INVALID;
+  for (int i = 0; i < n; ++i)
+    KAAS_CUDA(cudaEventElapsedTime(&ms[i], (cudaEvent_t)starts[i], (cudaEvent_t)ends[i]));
+  return 0;
+}
+
 // ---- memory ----------------------------------------------------------------
 
 int kaas_malloc_async(uint64_t stream, uint64_t bytes, uint64_t *dptr) {

@@ -687,15 +687,21 @@ class GpuExecutor:
             for ptr in rec.graveyard:
                 native.free_async(self.s_exec, ptr)
             if self.time_requests:
-                ms = ev[0].elapsed_ms(ev[1])
+                pairs = [(ev[0], ev[1])]
+                if rec.has_kernels:
+                    pairs.append((ev[2], ev[3]))
+                if rec.has_fills:
+                    pairs.append((ev[4], ev[5]))
+                spans = native.elapsed_many(pairs)  # one crossing for the request's spans
+                ms = spans[0]
                 self.dev_stats.last_device_ms = ms
                 self.dev_stats.device_ms += ms
                 if rec.has_kernels:
-                    kms = ev[2].elapsed_ms(ev[3])
+                    kms = spans[1]
                     self.dev_stats.last_kernel_ms = kms
                     self.dev_stats.kernel_ms += kms
                 if rec.has_fills:
-                    self.dev_stats.h2d_ms += ev[4].elapsed_ms(ev[5])
+                    self.dev_stats.h2d_ms += spans[-1]
             self.dev_stats.requests += 1
             del self._inflight[seq]
             self._ev_pool.append(ev)

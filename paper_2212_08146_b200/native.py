@@ -114,6 +114,7 @@ EXPORTS = {
     "kaas_event_sync": [_u64],
     "kaas_event_query": [_u64, C.POINTER(C.c_int)],
     "kaas_event_elapsed_ms": [_u64, _u64, C.POINTER(C.c_float)],
+    "kaas_event_elapsed_many": [C.c_int, _pu64, _pu64, C.POINTER(C.c_float)],
     "kaas_malloc_async": [_u64, _u64, _pu64],
     "kaas_free_async": [_u64, _u64],
     "kaas_memset_async": [_u64, C.c_int, _u64, _u64],
@@ -275,6 +276,16 @@ class Event:
                 _lib.kaas_event_destroy(h)
             except Exception:
                 pass
+
+
+def elapsed_many(pairs) -> list[float]:
+    """cudaEventElapsedTime over (start, end) Event pairs in one crossing."""
+    n = len(pairs)
+    starts = (C.c_uint64 * n)(*(a.handle for a, _ in pairs))
+    ends = (C.c_uint64 * n)(*(b.handle for _, b in pairs))
+    out = (C.c_float * n)()
+    call("kaas_event_elapsed_many", n, starts, ends, out)
+    return list(out)
 
 
 def malloc_async(stream: Stream, nbytes: int) -> int:
