@@ -133,6 +133,30 @@ class DeviceStats:
         return {k: getattr(self, k) for k in self.__slots__}
 
 
+def _written_prefix(kernel_id: str, inv, w: int) -> int:
+    """Bytes [0, n) that invocation ``inv`` of ``kernel_id`` writes into its
+    argument ``w`` (coverage rules of backend.py:137-211 / kernels.py); 0 when
+    not known to be a full prefix."""
+    total = inv.dims.total_threads
+    lits = [lit.value for lit in inv.literals]
+    if kernel_id in ("vector_add", "saxpy") and w == 2:
+        return 4 * max(0, min(total, lits[0]))
+    if kernel_id == "fill" and w == 0:
+        return 4 * max(0, min(total, lits[0]))
+    if kernel_id == "reduce_sum" and w == 1:
+        return 4
+    if kernel_id == "matmul" and w == 2:
+        return 4 * max(0, min(total, lits[0] * lits[1]))
+    if kernel_id == "cgemm" and w == 2:
+        return 8 * max(0, min(total, lits[0] * lits[1]))
+    if kernel_id == "jacobi_sweep":
+        if w == 3:
+            return 4 * max(0, min(total, lits[0]))
+        if w == 4:
+            return 4
+    return 0
+
+
 class _Plan:
     """Everything about a request that does not depend on cache state.
 
@@ -144,7 +168,7 @@ class _Plan:
 
     __slots__ = ("error", "kernels", "fail_at", "fail_exc", "advance_ns", "per_inv",
                  "template", "slots", "names", "dirty_names", "n", "stream_outs", "prepared",
-                 "last_ptrs", "last_descs")
+                 "last_ptrs", "last_descs", "skip_zero")
 
 
 class _LRU(OrderedDict):
@@ -234,6 +258,7 @@ class GpuExecutor:
         self._pinned_store = isinstance(store, PinnedStore)
         self._req_seq = 0
         self._cur: _Req | None = None             # request being begun
+        self._skip_zero: frozenset = frozenset()  # names whose zero-fill the plan proved dead
         self._inflight: OrderedDict[int, _Req] = OrderedDict()  # seq -> begun, not completed
         self._pending_puts: dict[str, int] = {}   # key -> seq of the request that will put it
         self.on_complete = None                   # callback(req_record, response) (pool)
@@ -259,9 +284,10 @@ class GpuExecutor:
         buf.ptr = native.malloc_async(stream, buf.size)
         buf.dev = self.device
 
-    def _alloc_zeroed(self, buf: DeviceBuffer) -> None:
+    def _alloc_zeroed(self, buf: DeviceBuffer, name: str | None = None) -> None:
         self._alloc(buf, self.s_exec)
-        native.memset_async(buf.ptr, 0, buf.size, self.s_exec)
+        if name is None or name not in self._skip_zero:
+            native.memset_async(buf.ptr, 0, buf.size, self.s_exec)
 
     def _drop(self, buf: DeviceBuffer) -> None:
         """on_drop hook: an entry left the table or an ephemeral was freed.
@@ -353,7 +379,7 @@ class GpuExecutor:
             cache.evict_until(arg.size)
             buf = cache.alloc_ephemeral(arg.size)
             self._mark(buf)
-            self._alloc_zeroed(buf)
+            self._alloc_zeroed(buf, arg.name)
             return buf
 
         cached = cache.entries.get(arg.key)
@@ -387,7 +413,7 @@ class GpuExecutor:
             cache.evict_until(arg.size)
             buf = DeviceBuffer(arg.key, arg.size, is_const=False)
             self._mark(buf)
-            self._alloc_zeroed(buf)
+            self._alloc_zeroed(buf, arg.name)
             stats.cache_misses += 1
             cache.insert(buf)
             cache.pin(buf)
@@ -495,6 +521,7 @@ class GpuExecutor:
         p = _Plan()
         p.error = None
         p.last_ptrs = p.last_descs = None
+        p.skip_zero = frozenset()
         violations = validate_request(req)
         if violations:
             p.error = Status.make_error("InvalidRequest", "; ".join(violations))
@@ -584,6 +611,26 @@ class GpuExecutor:
                 if any(sides):
                     prep.append((i, sides[0], sides[1]))
         p.prepared = tuple(prep)
+        # new outputs / ephemerals whose zero-fill no one can observe: the
+        # first invocation touching them overwrites every byte without
+        # reading them first (a planned BackendFault keeps every zero-fill:
+        # never-written outputs stay cached as zeros)
+        skip = set()
+        if p.fail_at is None:
+            seen = set()
+            for inv, kernel in zip(req.invocations, kernels):
+                written = {inv.args[w]: _written_prefix(kernel.kernel_id, inv, w) for w in kernel.writes}
+                for j, nm in enumerate(inv.args):
+                    if nm in seen:
+                        continue
+                    seen.add(nm)
+                    arg = by_name[nm]
+                    if arg.is_const or not (arg.is_ephemeral or arg.direction == "output"):
+                        continue
+                    reads = any(nm == a for jj, a in enumerate(inv.args) if jj not in kernel.writes)
+                    if not reads and written.get(nm, 0) >= arg.size:
+                        skip.add(nm)
+        p.skip_zero = frozenset(skip)
         p.advance_ns = advance
         p.per_inv = tuple(per_inv)
         p.dirty_names = tuple(dirty)
@@ -619,6 +666,7 @@ class GpuExecutor:
             return self._finish(req, stats, t0, plan.error)
 
         self._req_seq += 1
+        self._skip_zero = plan.skip_zero
         rec = _Req(self._req_seq, req)
         rec.events = self._events()
         self._cur = rec
@@ -637,9 +685,11 @@ class GpuExecutor:
                 resolved[nm] = buf
                 if arg.is_ephemeral:
                     ephemerals.append(buf)
+            self._skip_zero = frozenset()
             self._launch(rec, plan, resolved)
             self._enqueue_flush(rec, plan.names, resolved, stats)
         except KaasError as exc:
+            self._skip_zero = frozenset()
             # a host-detected failure enqueued no kernels; drain so the
             # request's fills/zero-fills finish before its buffers are freed
             self._cur = None
