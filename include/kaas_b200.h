@@ -176,6 +176,12 @@ typedef struct kaas_stream_out {
 } kaas_stream_out;
 int kaas_launch_batch_ex(int dev, uint64_t stream, const kaas_launch_desc *descs, int n,
                          const kaas_stream_out *outs, int n_outs);
+/* kaas_launch_batch with a caller-chosen memo key: a nonzero key promises
+ * that `descs` has exactly the content of the last call on this stream that
+ * used the same key, so a fused Jacobi chain is relaunched from its cached
+ * parameters without re-parsing the descriptors (key 0 = no memo). */
+int kaas_launch_batch_memo(int dev, uint64_t stream, const kaas_launch_desc *descs, int n,
+                           uint64_t memo_key);
 
 #ifdef __cplusplus
 }

@@ -515,6 +515,7 @@ int kaas_stream_destroy(uint64_t stream) {
     if (sc->jac_sync) cudaFreeAsync(sc->jac_sync, s);
     if (sc->jac_xt) cudaFreeAsync(sc->jac_xt, s);
     if (sc->cg_buf) cudaFreeAsync(sc->cg_buf, s);
+    free_jacobi_memo(sc);
     if (sc->mm_buf) cudaFreeAsync(sc->mm_buf, s);
     cudaStreamSynchronize(s);
     if (sc->panel_done) cudaFree(sc->panel_done);
@@ -689,8 +690,33 @@ int kaas_launch_batch(int dev, uint64_t stream, const kaas_launch_desc *descs, i
   return kaas_launch_batch_ex(dev, stream, descs, n, nullptr, 0);
 }
 
+static int launch_batch_impl(int dev, uint64_t stream, const kaas_launch_desc *descs, int n,
+                             const kaas_stream_out *outs, int n_outs, uint64_t memo_key);
+
 int kaas_launch_batch_ex(int dev, uint64_t stream, const kaas_launch_desc *descs, int n,
                          const kaas_stream_out *outs, int n_outs) {
+  return launch_batch_impl(dev, stream, descs, n, outs, n_outs, 0);
+}
+
+int kaas_launch_batch_memo(int dev, uint64_t stream, const kaas_launch_desc *descs, int n,
+                           uint64_t memo_key) {
+  if (memo_key) {
+    StreamScratch *sc = scratch_for((cudaStream_t)stream);
+    if (sc && sc->dev == dev && sc->jac_memo_key == memo_key && n > 0 && descs) {
+      KAAS_CUDA(cudaSetDevice(dev));
+      cudaStream_t s = (cudaStream_t)stream;
+      int rc;
+      if ((rc = coop_serialise_begin(dev, s))) return rc;
+      rc = launch_jacobi_memo(s, dev, sc);
+      if (rc == 0) return coop_serialise_end(dev, s);
+      if (rc != 1) return rc;  // 1: nothing memoised after all -- take the full path
+    }
+  }
+  return launch_batch_impl(dev, stream, descs, n, nullptr, 0, memo_key);
+}
+
+static int launch_batch_impl(int dev, uint64_t stream, const kaas_launch_desc *descs, int n,
+                             const kaas_stream_out *outs, int n_outs, uint64_t memo_key) {
   if (n < 0 || (n > 0 && !descs)) return fail(KAAS_E_INVALID, "null launch descriptors");
   if (n_outs < 0 || (n_outs > 0 && !outs)) return fail(KAAS_E_INVALID, "null stream-out specs");
   cudaStream_t s = (cudaStream_t)stream;
@@ -749,7 +775,8 @@ int kaas_launch_batch_ex(int dev, uint64_t stream, const kaas_launch_desc *descs
                     (float *const *)xout.data(), (float *const *)res.data()};
       int rc;
       if ((rc = coop_serialise_begin(dev, s))) return rc;
-      if ((rc = launch_jacobi_chain(s, dev, c, sc))) return rc;
+      // the whole batch is this one run: the caller's memo key may name it
+      if ((rc = launch_jacobi_chain(s, dev, c, sc, (i == 0 && run == n) ? memo_key : 0))) return rc;
       if ((rc = coop_serialise_end(dev, s))) return rc;
       i += run;
       continue;

@@ -41,6 +41,10 @@ struct StreamScratch {
   // bit-exact matmul: B transposed for one launch when no prepared copy exists
   void *mm_buf = nullptr;
   size_t mm_bytes = 0;
+  // memoised fused Jacobi chain (kaas_launch_batch_memo): the built launch
+  // parameters of the last single-launch chain, keyed by the caller's key
+  uint64_t jac_memo_key = 0;
+  void *jac_memo = nullptr;  // owned; freed by free_jacobi_memo
   // cGEMM write-back ordering events, created on first use, reused per launch
   cudaEvent_t cg_ev_ready = nullptr, cg_ev_done = nullptr;
 };
@@ -96,7 +100,11 @@ struct JacobiChain {
   float *const *x_out;       // [sweeps]
   float *const *resid;       // [sweeps]
 };
-int launch_jacobi_chain(cudaStream_t s, int dev, const JacobiChain &c, StreamScratch *sc);
+int launch_jacobi_chain(cudaStream_t s, int dev, const JacobiChain &c, StreamScratch *sc,
+                        uint64_t memo_key = 0);
+// relaunch the memoised chain of sc (returns 1 when there is none to relaunch)
+int launch_jacobi_memo(cudaStream_t s, int dev, StreamScratch *sc);
+void free_jacobi_memo(StreamScratch *sc);
 // Prepared-operand buffers for cGEMM (nullptr = use per-stream scratch).
 struct CgemmPrepared {
   float *a = nullptr;  // [A_hi; A_lo]

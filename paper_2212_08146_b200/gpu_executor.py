@@ -34,6 +34,7 @@ touch it is freed only after the request's streams drain.
 
 from __future__ import annotations
 
+import itertools
 import os
 
 from collections import OrderedDict
@@ -133,6 +134,10 @@ class DeviceStats:
         return {k: getattr(self, k) for k in self.__slots__}
 
 
+# keys naming one immutable descriptor table (kaas_launch_batch_memo); never reused
+_DESC_KEYS = itertools.count(1)
+
+
 def _written_prefix(kernel_id: str, inv, w: int) -> int:
     """Bytes [0, n) that invocation ``inv`` of ``kernel_id`` writes into its
     argument ``w`` (coverage rules of backend.py:137-211 / kernels.py); 0 when
@@ -168,7 +173,7 @@ class _Plan:
 
     __slots__ = ("error", "kernels", "fail_at", "fail_exc", "advance_ns", "per_inv",
                  "template", "slots", "names", "dirty_names", "n", "stream_outs", "prepared",
-                 "last_ptrs", "last_descs", "skip_zero")
+                 "last_ptrs", "last_descs", "last_key", "skip_zero")
 
 
 class _LRU(OrderedDict):
@@ -521,6 +526,7 @@ class GpuExecutor:
         p = _Plan()
         p.error = None
         p.last_ptrs = p.last_descs = None
+        p.last_key = 0
         p.skip_zero = frozenset()
         violations = validate_request(req)
         if violations:
@@ -784,11 +790,14 @@ class GpuExecutor:
             ev[5].record(self.s_in)
         if plan.n:
             ptrs = tuple(resolved[nm].ptr for nm in plan.names)
+            memo_key = 0
             if not plan.prepared and ptrs == plan.last_ptrs:
                 # the pool handed back the same blocks as last time (the usual
                 # steady state): the 500-descriptor table is already built --
-                # kaas_launch_batch copies what it needs before returning
+                # kaas_launch_batch copies what it needs before returning --
+                # and its key lets the C side relaunch a fused chain as is
                 descs = plan.last_descs
+                memo_key = plan.last_key
             else:
                 table = np.fromiter(ptrs, dtype=np.uint64, count=len(ptrs))
                 table = np.append(table, np.uint64(0))
@@ -796,6 +805,7 @@ class GpuExecutor:
                 descs["ptrs"] = table[plan.slots]
                 if not plan.prepared:
                     plan.last_ptrs, plan.last_descs = ptrs, descs
+                    plan.last_key = memo_key = next(_DESC_KEYS)
             filled = self._attach_prepared(plan, descs, resolved) if plan.prepared else ()
             self._ev_fill.record(self.s_in)
             self.s_exec.wait(self._ev_fill)
@@ -808,7 +818,7 @@ class GpuExecutor:
                 outs.append((di, ai, self.s_out, blob.addr, buf.size))
             if self.time_requests:
                 ev[2].record(self.s_exec)
-            native.launch_batch(self.device, self.s_exec, descs, outs)
+            native.launch_batch(self.device, self.s_exec, descs, outs, memo_key)
             for slot in filled:
                 slot[2] = True  # later launches on s_exec are ordered after the fill
             if self.time_requests:

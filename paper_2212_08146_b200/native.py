@@ -130,6 +130,7 @@ EXPORTS = {
     "kaas_memcpy_p2p_async": [_u64, C.c_int, _u64, C.c_int, _u64, _u64],
     "kaas_launch": [C.c_int, _u64, C.POINTER(LaunchDesc)],
     "kaas_launch_batch": [C.c_int, _u64, C.POINTER(LaunchDesc), C.c_int],
+    "kaas_launch_batch_memo": [C.c_int, _u64, C.POINTER(LaunchDesc), C.c_int, _u64],
     "kaas_launch_batch_ex": [C.c_int, _u64, C.POINTER(LaunchDesc), C.c_int,
                              C.POINTER(StreamOut), C.c_int],
 }
@@ -338,11 +339,13 @@ def host_free(addr: int) -> None:
     call("kaas_host_free", C.c_void_p(addr))
 
 
-def launch_batch(dev: int, stream: Stream, descs, outs=None) -> None:
+def launch_batch(dev: int, stream: Stream, descs, outs=None, memo_key: int = 0) -> None:
     """Enqueue LaunchDescs in order (ctypes array or DESC_DTYPE numpy array).
 
     ``outs``: optional list of (desc_index, arg_index, out_stream, host_addr,
-    nbytes) progressive write-backs (kaas_launch_batch_ex)."""
+    nbytes) progressive write-backs (kaas_launch_batch_ex).  ``memo_key``:
+    nonzero promises ``descs`` has the content of the last call on this
+    stream with the same key (kaas_launch_batch_memo)."""
     n = len(descs)
     if n == 0:
         return
@@ -351,7 +354,11 @@ def launch_batch(dev: int, stream: Stream, descs, outs=None) -> None:
     else:
         ptr = descs
     if not outs:
-        check(load().kaas_launch_batch(dev, stream.handle, ptr, n), "kaas_launch_batch")
+        if memo_key:
+            check(load().kaas_launch_batch_memo(dev, stream.handle, ptr, n, memo_key),
+                  "kaas_launch_batch_memo")
+        else:
+            check(load().kaas_launch_batch(dev, stream.handle, ptr, n), "kaas_launch_batch")
         return
     arr = (StreamOut * len(outs))()
     for i, (di, ai, st, addr, nb) in enumerate(outs):
