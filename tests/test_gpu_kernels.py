@@ -386,3 +386,27 @@ def test_matmul_const_weight_prepared_transpose(gpu, shape):
         ostore.put("o", bytes(4 * n * m))
         OracleExecutor(1 << 30, ostore).execute(oreq)
         assert canon(store.get(f"mw/o{tag}")) == canon(ostore.get("o")), rep
+
+
+def test_jacobi_repeated_requests_reuse_the_memoised_launch(gpu):
+    """The executor reuses one descriptor table for a repeated request and the
+    C side relaunches the fused chain from cached parameters (fresh tags):
+    every run must still match the oracle, also after unrelated work in
+    between and after x0 changes in the store."""
+    ex, store = gpu
+    n, sweeps = 2048, 40
+    A, b = W.seed_jacobi(store, n, prefix="jm")
+    req = W.jacobi_request("jm", n, sweeps, f"jm/A/{n}", f"jm/b/{n}", f"jm/x0/{n}", "jm/x", "jm/r")
+    ostore = DictStore({f"jm/A/{n}": A.tobytes(), f"jm/b/{n}": b.tobytes()})
+    rng = np.random.default_rng(3)
+    for rep in range(5):
+        x0 = (rng.standard_normal(n) if rep >= 3 else np.zeros(n)).astype("<f4")
+        store.put(f"jm/x0/{n}", x0.tobytes())
+        ostore.put(f"jm/x0/{n}", x0.tobytes())
+        if rep == 2:
+            _cgemm_check(ex, store, 64, 64, 32, seed=9)  # unrelated work in between
+        _run(ex, req)
+        OracleExecutor(1 << 30, ostore).execute(req)
+        g = np.frombuffer(store.get("jm/x"), "<f4").astype(np.float64)
+        o = np.frombuffer(ostore.get("jm/x"), "<f4").astype(np.float64)
+        assert np.abs(g - o).max() <= 1e-5, rep
