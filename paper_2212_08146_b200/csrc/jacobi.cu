@@ -810,7 +810,7 @@ constexpr int kTmRR = 6;    // register rows
 constexpr int kTmRS = 6;    // shared-memory rows
 static_assert(kTmRT + kTmRR + kTmRS == kColRows, "row tiers must cover the band");
 constexpr int kTmBatch = 1;  // TMEM rows per tcgen05.ld batch
-constexpr int kTmDep = 3;    // batches in flight (each waits on the dots kTmDep batches back)
+constexpr int kTmDep = 4;    // batches in flight (each waits on the dots kTmDep batches back)
 // padded so no other 1-CTA/SM kernel that allocates TMEM can be co-resident
 constexpr size_t kTmTier = (size_t)kTmRS * kColC4 * kColT * sizeof(float4);
 constexpr size_t kTmSmem = kTmTier > 116 * 1024 ? kTmTier : 116 * 1024;
