@@ -439,6 +439,45 @@ __global__ void k_transpose_b(int k, int m, const float *__restrict__ b, float *
   }
 }
 
+template <int TY, int TX, int TM, int TN, int S, int BK>
+int mm_launch_sb(int dev, cudaStream_t s, dim3 grid, const float *bt, bool a_vec, uint64_t n, uint64_t m,
+                 uint64_t k, uint64_t cov, const float *a, const float *b, float *out) {
+  constexpr int SM = mm_smem_bytes<TY, TX, TM, TN, S, BK>();
+  static_assert(SM <= 227 * 1024, "matmul ring exceeds shared memory");
+  static std::atomic<uint64_t> attr_done{0};  // per device (dev < 64)
+  if (!(attr_done.load(std::memory_order_relaxed) >> (dev & 63) & 1)) {
+    KAAS_CUDA(cudaFuncSetAttribute(k_matmul<TY, TX, TM, TN, S, BK, true, true>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, SM));
+    KAAS_CUDA(cudaFuncSetAttribute(k_matmul<TY, TX, TM, TN, S, BK, true, false>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, SM));
+    KAAS_CUDA(cudaFuncSetAttribute(k_matmul<TY, TX, TM, TN, S, BK, false, false>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, SM));
+    attr_done.fetch_or(1ull << (dev & 63));
+  }
+  KAAS_CUDA(launch_pdl(bt ? k_matmul<TY, TX, TM, TN, S, BK, true, true>
+                          : a_vec ? k_matmul<TY, TX, TM, TN, S, BK, true, false>
+                                  : k_matmul<TY, TX, TM, TN, S, BK, false, false>,
+                       grid, dim3(TY * TX), SM, s, (int)n, (int)m, (int)k, cov, a, bt ? bt : b, out));
+  return 0;
+}
+
+// Ring depth: 4 x 32-k chunks for the big tiles; 3 x 64-k for the small ones,
+// whose CTAs are small and many -- a shallower ring keeps more of them
+// resident (measured over the ResNet-50 layers: 1364 -> 1207 us vs 6-8 stages
+// for every layer).  For the long-K layers alone, a deeper ring (4, 6 or 8
+// stages) and 128-k chunks both measured flat or slower: ~1.5 warps per
+// scheduler stall on shared-memory latency and the FADD chain (ncu: short
+// scoreboard 1.14 + wait 1.24 cycles per issue), not on L2 or chunk overhead.
+template <int TY, int TX, int TM, int TN>
+int mm_launch(int dev, cudaStream_t s, dim3 grid, const float *bt, bool a_vec, uint64_t n, uint64_t m,
+              uint64_t k, uint64_t cov, const float *a, const float *b, float *out) {
+  if constexpr (TM * TN >= 8) {
+    return mm_launch_sb<TY, TX, TM, TN, 4, 32>(dev, s, grid, bt, a_vec, n, m, k, cov, a, b, out);
+  } else {
+    return mm_launch_sb<TY, TX, TM, TN, 3, 64>(dev, s, grid, bt, a_vec, n, m, k, cov, a, b, out);
+  }
+}
+
 int launch_matmul(cudaStream_t s, int dev, uint64_t n, uint64_t m, uint64_t k, uint64_t cov,
                   const float *a, const float *b, float *out, StreamScratch *sc, const float *bt_prep,
                   bool bt_ready) {
@@ -511,43 +550,20 @@ int launch_matmul(cudaStream_t s, int dev, uint64_t n, uint64_t m, uint64_t k, u
   const unsigned gx = (unsigned)((m + c.tx * c.tn - 1) / (c.tx * c.tn));
   dim3 grid(gx, gy);
   const int a_vec = (k % 4 == 0) && aligned16(a);
-#define MM_LAUNCH(TY, TX, TM, TN)                                                          \
-  do {                                                                                     \
-    /* ring: 4 x 32-k chunks for the big tiles; 3 x 64-k for the small ones, whose   \
-       CTAs are small and many -- a shallower ring keeps more of them resident      \
-       (measured over the ResNet-50 layers: 1364 -> 1207 us vs 6-8 stages) */       \
-    constexpr int S_ = (TM) * (TN) >= 8 ? 4 : 3;                                           \
-    constexpr int BK_ = (TM) * (TN) >= 8 ? 32 : 64;                                        \
-    constexpr int SM_ = mm_smem_bytes<TY, TX, TM, TN, S_, BK_>();                          \
-    static std::atomic<uint64_t> attr_done{0}; /* per device (dev < 64) */                  \
-    if (!(attr_done.load(std::memory_order_relaxed) >> (dev & 63) & 1)) {                  \
-      KAAS_CUDA(cudaFuncSetAttribute(k_matmul<TY, TX, TM, TN, S_, BK_, true, true>,        \
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, SM_));    \
-      KAAS_CUDA(cudaFuncSetAttribute(k_matmul<TY, TX, TM, TN, S_, BK_, true, false>,       \
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, SM_));    \
-      KAAS_CUDA(cudaFuncSetAttribute(k_matmul<TY, TX, TM, TN, S_, BK_, false, false>,      \
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, SM_));    \
-      attr_done.fetch_or(1ull << (dev & 63));                                              \
-    }                                                                                      \
-    KAAS_CUDA(launch_pdl(bt ? k_matmul<TY, TX, TM, TN, S_, BK_, true, true>                \
-                            : a_vec ? k_matmul<TY, TX, TM, TN, S_, BK_, true, false>        \
-                                    : k_matmul<TY, TX, TM, TN, S_, BK_, false, false>,      \
-                         grid, dim3((TY) * (TX)), SM_, s, (int)n, (int)m, (int)k, cov, a,    \
-                         bt ? bt : b, out));                                               \
-  } while (0)
+  int rc = 0;
   switch (best) {
-    case 0: MM_LAUNCH(16, 16, 4, 4); break;
-    case 1: MM_LAUNCH(16, 16, 2, 4); break;
-    case 2: MM_LAUNCH(16, 16, 4, 2); break;
-    case 3: MM_LAUNCH(16, 16, 2, 2); break;
-    case 4: MM_LAUNCH(8, 16, 2, 2); break;
-    case 5: MM_LAUNCH(16, 8, 2, 2); break;
-    case 6: MM_LAUNCH(8, 8, 2, 2); break;
-    case 7: MM_LAUNCH(8, 8, 1, 2); break;
-    case 8: MM_LAUNCH(8, 8, 2, 1); break;
-    default: MM_LAUNCH(8, 8, 1, 1); break;
+    case 0: rc = mm_launch<16, 16, 4, 4>(dev, s, grid, bt, a_vec, n, m, k, cov, a, b, out); break;
+    case 1: rc = mm_launch<16, 16, 2, 4>(dev, s, grid, bt, a_vec, n, m, k, cov, a, b, out); break;
+    case 2: rc = mm_launch<16, 16, 4, 2>(dev, s, grid, bt, a_vec, n, m, k, cov, a, b, out); break;
+    case 3: rc = mm_launch<16, 16, 2, 2>(dev, s, grid, bt, a_vec, n, m, k, cov, a, b, out); break;
+    case 4: rc = mm_launch<8, 16, 2, 2>(dev, s, grid, bt, a_vec, n, m, k, cov, a, b, out); break;
+    case 5: rc = mm_launch<16, 8, 2, 2>(dev, s, grid, bt, a_vec, n, m, k, cov, a, b, out); break;
+    case 6: rc = mm_launch<8, 8, 2, 2>(dev, s, grid, bt, a_vec, n, m, k, cov, a, b, out); break;
+    case 7: rc = mm_launch<8, 8, 1, 2>(dev, s, grid, bt, a_vec, n, m, k, cov, a, b, out); break;
+    case 8: rc = mm_launch<8, 8, 2, 1>(dev, s, grid, bt, a_vec, n, m, k, cov, a, b, out); break;
+    default: rc = mm_launch<8, 8, 1, 1>(dev, s, grid, bt, a_vec, n, m, k, cov, a, b, out); break;
   }
-#undef MM_LAUNCH
+  if (rc) return rc;
   count_launch();
   KAAS_CUDA(cudaGetLastError());
   return 0;
