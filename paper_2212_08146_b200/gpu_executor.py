@@ -36,6 +36,7 @@ from __future__ import annotations
 
 import itertools
 import os
+import threading
 
 from collections import OrderedDict
 from dataclasses import dataclass, field
@@ -113,25 +114,90 @@ class _ReqStats:
 
 
 class DeviceStats:
-    """Measured (not virtual) device activity of one executor."""
+    """Measured (not virtual) device activity of one executor.
 
-    __slots__ = ("requests", "device_ms", "last_device_ms", "kernel_ms", "last_kernel_ms",
-                 "h2d_bytes", "h2d_ms", "d2h_bytes", "p2p_bytes", "kernel_launches")
+    A request's event spans are read lazily: ``complete()`` queues the
+    request's events and the elapsed-time query (one C-ABI crossing, ~10 us)
+    runs when a timing field is read or while the next request's kernels run
+    -- not between a request's last event and its response."""
 
-    def __init__(self):
+    __slots__ = ("requests", "_device_ms", "_last_device_ms", "_kernel_ms", "_last_kernel_ms",
+                 "h2d_bytes", "_h2d_ms", "d2h_bytes", "p2p_bytes", "kernel_launches", "_pending",
+                 "_release", "_lock")
+    FIELDS = ("requests", "device_ms", "last_device_ms", "kernel_ms", "last_kernel_ms",
+              "h2d_bytes", "h2d_ms", "d2h_bytes", "p2p_bytes", "kernel_launches")
+
+    def __init__(self, release=None):
         self.requests = 0
-        self.device_ms = 0.0
-        self.last_device_ms = 0.0
-        self.kernel_ms = 0.0       # time inside the batched invocation list
-        self.last_kernel_ms = 0.0
+        self._device_ms = 0.0
+        self._last_device_ms = 0.0
+        self._kernel_ms = 0.0      # time inside the batched invocation list
+        self._last_kernel_ms = 0.0
         self.h2d_bytes = 0
-        self.h2d_ms = 0.0          # time the H2D fill stream was busy (first fill -> last fill done)
+        self._h2d_ms = 0.0         # time the H2D fill stream was busy (first fill -> last fill done)
         self.d2h_bytes = 0
         self.p2p_bytes = 0
         self.kernel_launches = 0
+        self._pending: list = []   # (events, has_kernels, has_fills), all complete on the device
+        self._release = release    # events -> the executor's pool once read
+        self._lock = threading.Lock()  # the worker resolves while a reader may too
+
+    def defer(self, events, has_kernels: bool, has_fills: bool) -> None:
+        with self._lock:
+            self._pending.append((events, has_kernels, has_fills))
+            full = len(self._pending) >= 16
+        if full:
+            self.resolve()
+
+    def resolve(self) -> None:
+        if not self._pending:
+            return
+        with self._lock:
+            self._resolve_locked()
+
+    def _resolve_locked(self) -> None:
+        pend = self._pending
+        if not pend:
+            return
+        pairs = []
+        for ev, hk, hf in pend:
+            pairs.append((ev[0], ev[1]))
+            if hk:
+                pairs.append((ev[2], ev[3]))
+            if hf:
+                pairs.append((ev[4], ev[5]))
+        spans = native.elapsed_many(pairs)  # one crossing for all queued requests
+        self._pending = []
+        i = 0
+        for ev, hk, hf in pend:
+            self._last_device_ms = spans[i]
+            self._device_ms += spans[i]
+            i += 1
+            if hk:
+                self._last_kernel_ms = spans[i]
+                self._kernel_ms += spans[i]
+                i += 1
+            if hf:
+                self._h2d_ms += spans[i]
+                i += 1
+            if self._release is not None:
+                self._release(ev)
+
+    def _get(name):
+        def get(self):
+            self.resolve()
+            return getattr(self, name)
+        return property(get)
+
+    device_ms = _get("_device_ms")
+    last_device_ms = _get("_last_device_ms")
+    kernel_ms = _get("_kernel_ms")
+    last_kernel_ms = _get("_last_kernel_ms")
+    h2d_ms = _get("_h2d_ms")
+    del _get
 
     def as_dict(self) -> dict:
-        return {k: getattr(self, k) for k in self.__slots__}
+        return {k: getattr(self, k) for k in self.FIELDS}
 
 
 # keys naming one immutable descriptor table (kaas_launch_batch_memo); never reused
@@ -259,7 +325,7 @@ class GpuExecutor:
         self.total_hits = 0
         self.total_misses = 0
         self.requests_served = 0
-        self.dev_stats = DeviceStats()
+        self.dev_stats = DeviceStats(release=self._ev_pool.append)
         self._pinned_store = isinstance(store, PinnedStore)
         self._req_seq = 0
         self._cur: _Req | None = None             # request being begun
@@ -742,25 +808,12 @@ class GpuExecutor:
                     self.peers.publish(self.executor_id, buf, version, None)
             for ptr in rec.graveyard:
                 native.free_async(self.s_exec, ptr)
-            if self.time_requests:
-                pairs = [(ev[0], ev[1])]
-                if rec.has_kernels:
-                    pairs.append((ev[2], ev[3]))
-                if rec.has_fills:
-                    pairs.append((ev[4], ev[5]))
-                spans = native.elapsed_many(pairs)  # one crossing for the request's spans
-                ms = spans[0]
-                self.dev_stats.last_device_ms = ms
-                self.dev_stats.device_ms += ms
-                if rec.has_kernels:
-                    kms = spans[1]
-                    self.dev_stats.last_kernel_ms = kms
-                    self.dev_stats.kernel_ms += kms
-                if rec.has_fills:
-                    self.dev_stats.h2d_ms += spans[-1]
             self.dev_stats.requests += 1
             del self._inflight[seq]
-            self._ev_pool.append(ev)
+            if self.time_requests:  # spans read later (DeviceStats.resolve), events pooled then
+                self.dev_stats.defer(ev, rec.has_kernels, rec.has_fills)
+            else:
+                self._ev_pool.append(ev)
             rec.keepalive.clear()
             done += 1
             if self.on_complete is not None:
@@ -819,6 +872,7 @@ class GpuExecutor:
             if self.time_requests:
                 ev[2].record(self.s_exec)
             native.launch_batch(self.device, self.s_exec, descs, outs, memo_key)
+            self.dev_stats.resolve()  # earlier requests' spans, while this one runs
             for slot in filled:
                 slot[2] = True  # later launches on s_exec are ordered after the fill
             if self.time_requests:
@@ -951,6 +1005,11 @@ class GpuExecutor:
             s.destroy()
         for e in (self._ev_fill, self._ev_exec):
             e.destroy()
+        try:
+            self.dev_stats.resolve()  # returns the queued requests' events to the pool
+        except Exception:  # noqa: BLE001 -- a faulted context: the events are destroyed below anyway
+            self._ev_pool.extend(ev for ev, _, _ in self.dev_stats._pending)
+            self.dev_stats._pending = []
         for evs in self._ev_pool:
             for e in evs:
                 e.destroy()
