@@ -860,8 +860,11 @@ class GpuExecutor:
                     plan.last_ptrs, plan.last_descs = ptrs, descs
                     plan.last_key = memo_key = next(_DESC_KEYS)
             filled = self._attach_prepared(plan, descs, resolved) if plan.prepared else ()
-            self._ev_fill.record(self.s_in)
-            self.s_exec.wait(self._ev_fill)
+            if self.time_requests and rec.has_fills:
+                self.s_exec.wait(ev[5])  # recorded on s_in just above: the fills' end
+            else:
+                self._ev_fill.record(self.s_in)
+                self.s_exec.wait(self._ev_fill)
             outs = []
             for di, ai, nm in plan.stream_outs:
                 buf = resolved[nm]
@@ -913,8 +916,11 @@ class GpuExecutor:
         (executor.py:371-380): the D2H copies are enqueued now, the puts
         happen in ``complete``; virtual time, IoStats and the clean marks are
         final now, as the next request's decisions depend on them."""
-        self._ev_exec.record(self.s_exec)
-        self.s_out.wait(self._ev_exec)
+        if self.time_requests and rec.has_kernels:
+            self.s_out.wait(rec.events[3])  # _launch recorded it on s_exec after the batch, just now
+        else:
+            self._ev_exec.record(self.s_exec)
+            self.s_out.wait(self._ev_exec)
         for nm in names:
             buf = resolved[nm]
             # only non-const keyed buffers get dirty, and validation forbids
