@@ -112,6 +112,13 @@ int kaas_init_device(int dev);
 int kaas_device_info_get(int dev, kaas_device_info *out);
 /* Total kernels this library has launched (all devices) -- bench evidence. */
 int kaas_launch_counter(uint64_t *out);
+/* Device health after a failed call: 0, or the sticky CUDA error (the
+ * executor is then poisoned and the router stops placing requests on it;
+ * replaces the worker's exception path, service.py:71-78). */
+int kaas_device_check(int dev);
+/* Fault injection for tests (genreq.py:190-243 injects request faults; this
+ * injects a device fault): enqueues a kernel that traps on `stream`. */
+int kaas_inject_fault(uint64_t stream);
 
 /* ---- streams / events (executor request lifecycle, executor.py:320-387) */
 int kaas_stream_create(int dev, int priority, uint64_t *stream);
@@ -143,7 +150,9 @@ int kaas_host_unregister(void *ptr);
 int kaas_memcpy_h2d_async(uint64_t dst, const void *src, uint64_t bytes, uint64_t stream);
 int kaas_memcpy_d2h_async(void *dst, uint64_t src, uint64_t bytes, uint64_t stream);
 int kaas_memcpy_d2d_async(uint64_t dst, uint64_t src, uint64_t bytes, uint64_t stream);
-/* NVLink peer fill of a cache entry another GPU already holds (new). */
+/* NVLink peer fill of a cache entry another GPU already holds (new).
+ * kaas_enable_peer(dev, peer): `dev` may read `peer`'s memory, including
+ * allocations from `peer`'s stream-ordered pool (cudaMemPoolSetAccess). */
 int kaas_enable_peer(int dev, int peer);
 int kaas_can_access_peer(int dev, int peer, int *can);
 int kaas_memcpy_p2p_async(uint64_t dst, int dst_dev, uint64_t src, int src_dev,

@@ -49,11 +49,16 @@ class OracleRouter:
                 best = min(ids, key=lambda e: (self.depth[e], e))
             return best
         if s == "static":
-            consts = sorted({b.key for b in req.buffers if b.is_const and b.key is not None})
-            if not consts:
-                return ids[zlib.crc32(req.request_id.encode()) % len(ids)]
-            return ids[zlib.crc32("\x00".join(consts).encode()) % len(ids)]
+            consts = {b.key for b in req.buffers if b.is_const and b.key is not None}
+            if any(not isinstance(k, str) for k in consts):
+                return ids[0]  # malformed request: routed anywhere fixed, rejected in band
+            token = "\x00".join(sorted(consts)) if consts else req.request_id
+            if not isinstance(token, str):
+                return ids[0]
+            return ids[zlib.crc32(token.encode("utf-8", "surrogatepass")) % len(ids)]
         if s == "exclusive":
+            if not isinstance(req.request_id, str):
+                return ids[0]
             tenant = req.request_id.split("/", 1)[0]
             if tenant not in self._tenants:
                 self._tenants[tenant] = ids[len(self._tenants) % len(ids)]

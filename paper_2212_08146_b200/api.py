@@ -29,13 +29,17 @@ I64_RANGE = (-(1 << 63), (1 << 63) - 1)
 STORE_KEY_MAX_LEN = 256
 DIRECTIONS = ("input", "output", "inout")
 LITERAL_TYPES = ("i32", "i64", "f32", "f64")
-_KEY_CHARS = re.compile(r"[A-Za-z0-9._/-]+")
+# ``protocol.py:24``: anchored with ``^...$`` and applied with ``re.match``,
+# so -- as in the reference -- one trailing newline is accepted ("k\n").
+_KEY_CHARS = re.compile(r"^[A-Za-z0-9._/-]+$")
 
 
 def valid_store_key(key) -> bool:
-    """``protocol.py:42-47``: 1..256 chars of ``[A-Za-z0-9._/-]``."""
+    """``protocol.py:42-47``: 1..256 chars of ``[A-Za-z0-9._/-]`` under the
+    reference's exact regex semantics (``$`` also matches before a final
+    newline)."""
     return (isinstance(key, str) and 0 < len(key) <= STORE_KEY_MAX_LEN
-            and _KEY_CHARS.fullmatch(key) is not None)
+            and _KEY_CHARS.match(key) is not None)
 
 
 # ---------------------------------------------------------------------------
@@ -65,7 +69,12 @@ class LaunchDims:
 
 @dataclass(frozen=True, eq=False)
 class ScalarLiteral:
-    """Tagged scalar kernel argument; NaN payloads compare equal."""
+    """Tagged scalar kernel argument; NaN payloads compare equal.
+
+    Equality is the reference's (``protocol.py:80-89``): values of the same
+    Python type compare with ``==`` (so ``0.0 == -0.0``), NaN equals NaN.
+    The sign of zero still reaches the kernel: the executor's plan key and
+    the codec's intern key carry float bits (``gpu_executor._plan_key``)."""
 
     type: str
     value: int | float
@@ -73,15 +82,12 @@ class ScalarLiteral:
     def __eq__(self, other):
         if not isinstance(other, ScalarLiteral):
             return NotImplemented
-        if self.type != other.type or type(self.value) is not type(other.value):
+        if self.type != other.type:
             return False
-        if isinstance(self.value, float):
-            if math.isnan(self.value) and math.isnan(other.value):
-                return True
-            # 0.0 == -0.0, but the sign bit reaches the kernel
-            return (self.value == other.value
-                    and math.copysign(1.0, self.value) == math.copysign(1.0, other.value))
-        return self.value == other.value
+        a, b = self.value, other.value
+        if isinstance(a, float) and isinstance(b, float) and math.isnan(a) and math.isnan(b):
+            return True
+        return type(a) is type(b) and a == b
 
     def __hash__(self):
         return hash(self.type)
@@ -352,91 +358,131 @@ def encode_response(resp: KaasResponse) -> bytes:
                       allow_nan=False).encode("utf-8")
 
 
-class _Reader:
-    def __init__(self, strict: bool):
-        self.strict = strict
+# Checked decoder.  The order of the checks and every error message follow
+# ``protocol.py:390-511`` exactly (the first failing check names the error a
+# client sees, so both are part of the drop-in contract).
 
-    def obj(self, v, ctx, allowed):
-        if not isinstance(v, dict):
-            raise SchemaError(f"{ctx}: expected object, got {type(v).__name__}")
-        if self.strict and set(v) - set(allowed):
-            raise SchemaError(f"{ctx}: unknown fields {sorted(set(v) - set(allowed))}")
-        return v
 
-    @staticmethod
-    def get(o, name, ctx, kind):
-        if name not in o:
-            raise SchemaError(f"{ctx}: missing field {name!r}")
-        v = o[name]
-        ok = {"str": lambda x: isinstance(x, str),
-              "int": _is_int,
-              "bool": lambda x: isinstance(x, bool),
-              "list": lambda x: isinstance(x, list),
-              "any": lambda x: True}[kind](v)
-        if not ok:
-            raise SchemaError(f"{ctx}.{name}: expected {kind}, got {type(v).__name__}")
-        return v
+def _kind(v) -> str:
+    return type(v).__name__
+
+
+def _obj(v, ctx):
+    if not isinstance(v, dict):
+        raise SchemaError(f"{ctx}: expected object, got {_kind(v)}")
+    return v
+
+
+def _arr(v, ctx):
+    if not isinstance(v, list):
+        raise SchemaError(f"{ctx}: expected array, got {_kind(v)}")
+    return v
+
+
+def _str(v, ctx):
+    if not isinstance(v, str):
+        raise SchemaError(f"{ctx}: expected string, got {_kind(v)}")
+    return v
+
+
+def _int(v, ctx):
+    if not _is_int(v):
+        raise SchemaError(f"{ctx}: expected integer, got {_kind(v)}")
+    return v
+
+
+def _bool(v, ctx):
+    if not isinstance(v, bool):
+        raise SchemaError(f"{ctx}: expected boolean, got {_kind(v)}")
+    return v
+
+
+def _fld(o, name, ctx):
+    if name not in o:
+        raise SchemaError(f"{ctx}: missing field {name!r}")
+    return o[name]
+
+
+def _only(o, allowed, ctx, strict):
+    if strict:
+        extra = set(o) - set(allowed)
+        if extra:
+            raise SchemaError(f"{ctx}: unknown fields {sorted(extra)}")
 
 
 def _loads(data):
     if not isinstance(data, (bytes, bytearray)):
         raise ParseError("input must be a byte sequence")
     try:
-        return json.loads(bytes(data).decode("utf-8"))
+        text = bytes(data).decode("utf-8")
     except UnicodeDecodeError as exc:
         raise ParseError(f"invalid UTF-8: {exc}") from None
+    try:
+        return json.loads(text)
     except json.JSONDecodeError as exc:
         raise ParseError(f"malformed JSON: {exc}") from None
 
 
+_BUF_FIELDS = ("name", "key", "size", "is_const", "is_ephemeral", "direction")
+_INV_FIELDS = ("kernel_id", "dims", "literals", "args")
+
+
+def _literal_from_doc(v, ctx, strict) -> ScalarLiteral:
+    o = _obj(v, ctx)
+    _only(o, ("type", "value"), ctx, strict)
+    tag = _str(_fld(o, "type", ctx), f"{ctx}.type")
+    if tag not in LITERAL_TYPES:
+        raise SchemaError(f'{ctx}: unknown literal type "{tag}"')
+    val = _fld(o, "value", ctx)
+    if tag in ("i32", "i64"):
+        return ScalarLiteral(tag, _int(val, f"{ctx}.value"))
+    if isinstance(val, str):
+        if val not in _WORDS:
+            raise SchemaError(f'{ctx}: bad float word "{val}"')
+        return ScalarLiteral(tag, _WORDS[val])
+    if isinstance(val, bool) or not isinstance(val, (int, float)):
+        raise SchemaError(f"{ctx}.value: expected number")
+    return ScalarLiteral(tag, float(val))
+
+
+def _dims_from_doc(v, ctx, strict) -> LaunchDims:
+    o = _obj(v, ctx)
+    _only(o, _DIM_NAMES, ctx, strict)
+    return LaunchDims(*[_int(_fld(o, n, ctx), f"{ctx}.{n}") for n in _DIM_NAMES])
+
+
 def request_from_doc(top, strict: bool = False) -> KaasRequest:
-    r = _Reader(strict)
-    top = r.obj(top, "request", ("request_id", "buffers", "invocations"))
-    rid = r.get(top, "request_id", "request", "str")
+    top = _obj(top, "request")
+    _only(top, ("request_id", "buffers", "invocations"), "request", strict)
+    rid = _str(_fld(top, "request_id", "request"), "request_id")
     bufs = []
-    for i, raw in enumerate(r.get(top, "buffers", "request", "list")):
+    for i, raw in enumerate(_arr(_fld(top, "buffers", "request"), "buffers")):
         ctx = f"buffers[{i}]"
-        o = r.obj(raw, ctx, ("name", "key", "size", "is_const", "is_ephemeral", "direction"))
+        o = _obj(raw, ctx)
+        _only(o, _BUF_FIELDS, ctx, strict)
         key = o.get("key")
-        if key is not None and not isinstance(key, str):
-            raise SchemaError(f"{ctx}.key: expected string")
-        direction = r.get(o, "direction", ctx, "str")
+        if key is not None:
+            _str(key, f"{ctx}.key")
+        direction = _str(_fld(o, "direction", ctx), f"{ctx}.direction")
         if direction not in DIRECTIONS:
             raise SchemaError(f'{ctx}: unknown direction "{direction}"')
-        bufs.append(BufferArg(r.get(o, "name", ctx, "str"), r.get(o, "size", ctx, "int"),
-                              direction, key, r.get(o, "is_const", ctx, "bool"),
-                              r.get(o, "is_ephemeral", ctx, "bool")))
+        name = _str(_fld(o, "name", ctx), f"{ctx}.name")
+        size = _int(_fld(o, "size", ctx), f"{ctx}.size")
+        is_const = _bool(_fld(o, "is_const", ctx), f"{ctx}.is_const")
+        is_eph = _bool(_fld(o, "is_ephemeral", ctx), f"{ctx}.is_ephemeral")
+        bufs.append(BufferArg(name, size, direction, key, is_const, is_eph))
     invs = []
-    for i, raw in enumerate(r.get(top, "invocations", "request", "list")):
+    for i, raw in enumerate(_arr(_fld(top, "invocations", "request"), "invocations")):
         ctx = f"invocations[{i}]"
-        o = r.obj(raw, ctx, ("kernel_id", "dims", "literals", "args"))
-        lits = []
-        for j, lraw in enumerate(r.get(o, "literals", ctx, "list")):
-            lctx = f"{ctx}.literals[{j}]"
-            lo = r.obj(lraw, lctx, ("type", "value"))
-            tag = r.get(lo, "type", lctx, "str")
-            if tag not in LITERAL_TYPES:
-                raise SchemaError(f'{lctx}: unknown literal type "{tag}"')
-            val = r.get(lo, "value", lctx, "any")
-            if tag in ("i32", "i64"):
-                if not _is_int(val):
-                    raise SchemaError(f"{lctx}.value: expected integer")
-            elif isinstance(val, str):
-                if val not in _WORDS:
-                    raise SchemaError(f'{lctx}: bad float word "{val}"')
-                val = _WORDS[val]
-            elif isinstance(val, bool) or not isinstance(val, (int, float)):
-                raise SchemaError(f"{lctx}.value: expected number")
-            else:
-                val = float(val)
-            lits.append(ScalarLiteral(tag, val))
-        args = r.get(o, "args", ctx, "list")
-        if not all(isinstance(a, str) for a in args):
-            raise SchemaError(f"{ctx}.args: expected strings")
-        d = r.obj(r.get(o, "dims", ctx, "any"), f"{ctx}.dims", _DIM_NAMES)
-        dims = LaunchDims(*(r.get(d, n, f"{ctx}.dims", "int") for n in _DIM_NAMES))
-        invs.append(KernelInvocation(r.get(o, "kernel_id", ctx, "str"), dims,
-                                     tuple(lits), tuple(args)))
+        o = _obj(raw, ctx)
+        _only(o, _INV_FIELDS, ctx, strict)
+        lits = tuple(_literal_from_doc(l, f"{ctx}.literals[{j}]", strict)
+                     for j, l in enumerate(_arr(_fld(o, "literals", ctx), ctx)))
+        args = tuple(_str(a, f"{ctx}.args[{j}]")
+                     for j, a in enumerate(_arr(_fld(o, "args", ctx), ctx)))
+        kid = _str(_fld(o, "kernel_id", ctx), f"{ctx}.kernel_id")
+        dims = _dims_from_doc(_fld(o, "dims", ctx), f"{ctx}.dims", strict)
+        invs.append(KernelInvocation(kid, dims, lits, args))
     return KaasRequest(rid, tuple(bufs), tuple(invs))
 
 
@@ -549,35 +595,38 @@ _MISSING = object()
 
 
 def response_from_doc(top, strict: bool = False) -> KaasResponse:
-    r = _Reader(strict)
-    top = r.obj(top, "response", ("request_id", "status", "error", "per_invocation",
-                                  "io_stats", "simulated_total_time"))
-    rid = r.get(top, "request_id", "response", "str")
-    code = r.get(top, "status", "response", "str")
+    top = _obj(top, "response")
+    _only(top, ("request_id", "status", "error", "per_invocation", "io_stats",
+                "simulated_total_time"), "response", strict)
+    rid = _str(_fld(top, "request_id", "response"), "request_id")
+    code = _str(_fld(top, "status", "response"), "status")
     if code == "ok":
+        status = Status.make_ok()
         if strict and "error" in top:
             raise SchemaError("response: unexpected error object on ok status")
-        status = Status.make_ok()
     elif code == "error":
-        e = r.obj(r.get(top, "error", "response", "any"), "error", ("kind", "message"))
-        kind = r.get(e, "kind", "error", "str")
+        e = _obj(_fld(top, "error", "response"), "error")
+        _only(e, ("kind", "message"), "error", strict)
+        kind = _str(_fld(e, "kind", "error"), "error.kind")
         if kind not in WIRE_ERROR_KINDS:
             raise SchemaError(f'error: unknown kind "{kind}"')
-        status = Status.make_error(kind, r.get(e, "message", "error", "str"))
+        status = Status.make_error(kind, _str(_fld(e, "message", "error"), "error.message"))
     else:
         raise SchemaError(f'response: unknown status "{code}"')
     per = []
-    for i, raw in enumerate(r.get(top, "per_invocation", "response", "list")):
+    for i, raw in enumerate(_arr(_fld(top, "per_invocation", "response"), "per_invocation")):
         ctx = f"per_invocation[{i}]"
-        o = r.obj(raw, ctx, ("kernel_id", "simulated_compute_time", "launch_overhead"))
-        per.append(InvocationStats(r.get(o, "kernel_id", ctx, "str"),
-                                   r.get(o, "simulated_compute_time", ctx, "int"),
-                                   r.get(o, "launch_overhead", ctx, "int")))
+        o = _obj(raw, ctx)
+        _only(o, ("kernel_id", "simulated_compute_time", "launch_overhead"), ctx, strict)
+        kid = _str(_fld(o, "kernel_id", ctx), f"{ctx}.kernel_id")
+        sct = _int(_fld(o, "simulated_compute_time", ctx), ctx)
+        per.append(InvocationStats(kid, sct, _int(_fld(o, "launch_overhead", ctx), ctx)))
     names = ("store_gets", "store_puts", "bytes_fetched", "bytes_flushed",
              "cache_hits", "cache_misses")
-    io = r.obj(r.get(top, "io_stats", "response", "any"), "io_stats", names)
-    stats = IoStats(*(r.get(io, n, "io_stats", "int") for n in names))
-    total = r.get(top, "simulated_total_time", "response", "int")
+    io = _obj(_fld(top, "io_stats", "response"), "io_stats")
+    _only(io, names, "io_stats", strict)
+    stats = IoStats(*[_int(_fld(io, n, "io_stats"), f"io_stats.{n}") for n in names])
+    total = _int(_fld(top, "simulated_total_time", "response"), "simulated_total_time")
     return KaasResponse(rid, status, tuple(per), stats, total)
 
 

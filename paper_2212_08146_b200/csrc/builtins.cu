@@ -202,7 +202,10 @@ k_matmul(int n, int m, int k, uint64_t cov, const float *__restrict__ a,
   extern __shared__ __align__(16) float mm_smem[];
   float *As = mm_smem, *Bs = mm_smem + S * A_ST;
   const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
-  const int bm = blockIdx.y * BM, bn = blockIdx.x * BN;
+  // 1-D grid, column tiles fastest (the 2-D raster order without grid.y's
+  // 65535 limit on n)
+  const unsigned gx = (unsigned)((m + BN - 1) / BN);
+  const int bm = (int)(blockIdx.x / gx) * BM, bn = (int)(blockIdx.x % gx) * BN;
   const int nk = (k + BK - 1) / BK;
 
   // Per-thread copy slots, fixed across chunks: a running source pointer
@@ -424,18 +427,23 @@ int launch_reduce_sum(cudaStream_t s, int dev, uint64_t n, const float *x, float
   return 0;
 }
 
-// B [k][m] -> Bt [m][k] (32 x 32 smem tiles)
+// B [k][m] -> Bt [m][k] (32 x 32 smem tiles).  A 1-D grid walks the tiles,
+// so no extent hits the 65535 grid.y limit (k up to 2^31 - 1).
 __global__ void k_transpose_b(int k, int m, const float *__restrict__ b, float *__restrict__ bt) {
   __shared__ float t[32][33];
-  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
-  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-    const int r = r0 + i, c = c0 + threadIdx.x;
-    if (r < k && c < m) t[i][threadIdx.x] = b[(size_t)r * m + c];
-  }
-  __syncthreads();
-  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-    const int c = c0 + i, r = r0 + threadIdx.x;
-    if (r < k && c < m) bt[(size_t)c * k + r] = t[threadIdx.x][i];
+  const uint64_t tiles_m = ((uint64_t)m + 31) / 32, tiles = tiles_m * (((uint64_t)k + 31) / 32);
+  for (uint64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int c0 = (int)(tile % tiles_m) * 32, r0 = (int)(tile / tiles_m) * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+      const int r = r0 + i, c = c0 + threadIdx.x;
+      if (r < k && c < m) t[i][threadIdx.x] = b[(size_t)r * m + c];
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+      const int c = c0 + i, r = r0 + threadIdx.x;
+      if (r < k && c < m) bt[(size_t)c * k + r] = t[threadIdx.x][i];
+    }
+    __syncthreads();
   }
 }
 
@@ -487,10 +495,12 @@ int launch_matmul(cudaStream_t s, int dev, uint64_t n, uint64_t m, uint64_t k, u
   // B transposed (16-byte B copies): from the executor's prepared-operand
   // cache when it has one for this weight, else built into per-stream
   // scratch for this launch (one extra pass over B)
-  const char *be = getenv("KAAS_MATMUL_BT");  // dev A/B: 0 = B as given
+  const char *be = KAAS_DEV_ENV("KAAS_MATMUL_BT");  // dev A/B: 0 = B as given
   const bool use_bt = !(be && be[0] == '0') && k > 0 && k % 4 == 0 && aligned16(a);
   auto transpose_into = [&](float *dst) -> int {
-    KAAS_CUDA(launch_pdl(k_transpose_b, dim3((unsigned)((m + 31) / 32), (unsigned)((k + 31) / 32)),
+    const uint64_t tiles = ((m + 31) / 32) * ((k + 31) / 32);
+    const uint64_t cap = (uint64_t)device_props(dev).sm_count * 16;
+    KAAS_CUDA(launch_pdl(k_transpose_b, dim3((unsigned)(tiles < cap ? tiles : cap)),
                          dim3(32, 8), 0, s, (int)k, (int)m, b, dst));
     count_launch();
     return 0;
@@ -528,7 +538,7 @@ int launch_matmul(cudaStream_t s, int dev, uint64_t n, uint64_t m, uint64_t k, u
     const Cfg &c = cfgs[i];
     const uint64_t tbm = (uint64_t)c.ty * c.tm, tbn = (uint64_t)c.tx * c.tn;
     const uint64_t gy = (n + tbm - 1) / tbm, gx = (m + tbn - 1) / tbn;
-    if (gy > 65535) continue;
+    if (gy * gx > 0x7fffffffull) continue;
     const double warps = (double)(gy * gx) * (c.ty * c.tx / 32.0);
     const double useful = (double)(n * m) / (double)(gy * tbm * gx * tbn);
     const double cells = c.tm * c.tn;
@@ -539,16 +549,17 @@ int launch_matmul(cudaStream_t s, int dev, uint64_t n, uint64_t m, uint64_t k, u
       best = i;
     }
   }
-  if (best_score < 0) return fail(KAAS_E_INVALID, "matmul: n too large for grid.y");
-  if (const char *fe = getenv("KAAS_MATMUL_CFG")) {  // dev: force a config (tools/mm_cfg_sweep.py)
+  if (best_score < 0) return fail(KAAS_E_INVALID, "matmul: too many output tiles for one grid");
+  if (const char *fe = KAAS_DEV_ENV("KAAS_MATMUL_CFG")) {  // dev: force a config (tools/mm_cfg_sweep.py)
     const int f = atoi(fe);
     const Cfg &c = cfgs[f < 0 ? 0 : f % (int)(sizeof(cfgs) / sizeof(cfgs[0]))];
-    if ((n + (uint64_t)c.ty * c.tm - 1) / ((uint64_t)c.ty * c.tm) <= 65535) best = f % (int)(sizeof(cfgs) / sizeof(cfgs[0]));
+    (void)c;
+    best = f % (int)(sizeof(cfgs) / sizeof(cfgs[0]));
   }
   const Cfg &c = cfgs[best];
   const unsigned gy = (unsigned)((n + c.ty * c.tm - 1) / (c.ty * c.tm));
   const unsigned gx = (unsigned)((m + c.tx * c.tn - 1) / (c.tx * c.tn));
-  dim3 grid(gx, gy);
+  dim3 grid(gx * gy);
   const int a_vec = (k % 4 == 0) && aligned16(a);
   int rc = 0;
   switch (best) {

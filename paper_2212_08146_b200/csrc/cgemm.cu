@@ -83,8 +83,11 @@ __global__ void k_prep_a(int n, int k2, int ldk, const float *__restrict__ A, fl
 __global__ void k_prep_b(int k, int m, int ldk, const float2 *__restrict__ B, float *__restrict__ Bhi,
                          float *__restrict__ Blo) {
   __shared__ float2 tile[32][33];
-  const int p0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;
+  // 1-D grid over the tiles (no 65535 grid.y limit on k)
+  const uint64_t tiles_m = ((uint64_t)m + 31) / 32, tiles = tiles_m * (((uint64_t)k + 31) / 32);
+  for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+  const int p0 = (int)(t / tiles_m) * 32, j0 = (int)(t % tiles_m) * 32;
   for (int r = ty; r < 32; r += 8) {
     const int p = p0 + r, j = j0 + tx;
     tile[r][tx] = (p < k && j < m) ? B[(size_t)p * m + j] : make_float2(0.f, 0.f);
@@ -108,6 +111,8 @@ __global__ void k_prep_b(int k, int m, int ldk, const float2 *__restrict__ B, fl
     *odd_hi = make_float2(ho0, ho1);
     *even_lo = make_float2(e0 - he0, e1 - he1);
     *odd_lo = make_float2(o0 - ho0, o1 - ho1);
+  }
+  __syncthreads();
   }
 }
 
@@ -221,20 +226,10 @@ struct GemmShape {
   int num_m, num_n;  // tile grid
   int m_complex;     // m (complex columns) for coverage indexing
   unsigned long long cov;  // covered complex cells
-  int ksplit;        // fused4 only: 1, or 2 = each tile's K in two halves on
-                     // two CTAs, both red.add-ed onto a zeroed C ((0+a)+b ==
-                     // (0+b)+a exactly, so the result is deterministic)
-};
-
-template <int BN>
-struct Smem {
-  alignas(1024) float a[STAGES][BM * BK];
-  alignas(1024) float b[STAGES][BN * BK];
-  uint64_t full[STAGES];
-  uint64_t empty[STAGES];
-  uint64_t tfull[2];
-  uint64_t tempty[2];
-  uint32_t tmem_base;
+  int ksplit;        // 1, or 2 = each tile's K in two halves on two CTAs,
+                     // both red.add-ed onto a zeroed C ((0+a)+b == (0+b)+a
+                     // exactly, so the result is deterministic)
+  int kb_chunk;      // k-blocks per fresh-accumulator chunk (see k_cgemm_fused4)
 };
 
 constexpr int kGroupM = 8;  // m-blocks per raster group (= one write-back panel)
@@ -251,155 +246,6 @@ __device__ __forceinline__ void tile_coords(const GemmShape &s, int t, int &mb, 
   nb = r / gsize;
 }
 
-template <int BN>
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
-k_cgemm_tf32x3(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-               const GemmShape s, float *__restrict__ C) {
-  extern __shared__ uint8_t smem_raw[];
-  Smem<BN> &sm = *reinterpret_cast<Smem<BN> *>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr uint32_t kTmemCols = 2 * BN;  // two accumulators
-  constexpr uint32_t kStageBytes = (BM + BN) * BK * 4;
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&map_a);
-    tma_prefetch_desc(&map_b);
-    for (int i = 0; i < STAGES; ++i) {
-      mbar_init(&sm.full[i], 1);
-      mbar_init(&sm.empty[i], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&sm.tfull[i], 1);
-      mbar_init(&sm.tempty[i], 128);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(&sm.tmem_base)),
-                 "r"(kTmemCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = sm.tmem_base;
-
-  const int total_tiles = s.num_m * s.num_n;
-  const int kb_total = 3 * s.kb_per_seg;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      // ===== TMA producer =====
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
-        int mb, nb;
-        tile_coords(s, t, mb, nb);
-        for (int kb = 0; kb < kb_total; ++kb) {
-          const int seg = kb / s.kb_per_seg, kk = kb % s.kb_per_seg;
-          // seg 0: A_hi . B_lo, seg 1: A_lo . B_hi, seg 2: A_hi . B_hi
-          const int arow = (seg == 1 ? s.a_lo_row : 0) + mb * BM;
-          const int brow = (seg == 0 ? s.b_lo_row : 0) + nb * BN;
-          mbar_wait(&sm.empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&sm.full[stage], kStageBytes);
-          tma_load_2d(&map_a, &sm.full[stage], sm.a[stage], kk * BK, arow);
-          tma_load_2d(&map_b, &sm.full[stage], sm.b[stage], kk * BK, brow);
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      // ===== MMA issuer =====
-      constexpr uint32_t idesc = make_idesc(BM, BN);
-      int stage = 0;
-      uint32_t phase = 0;
-      int local = 0;
-      for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++local) {
-        const int acc = local & 1;
-        const uint32_t acc_phase = (local >> 1) & 1;
-        mbar_wait(&sm.tempty[acc], acc_phase ^ 1);
-        tc_fence_after();
-        const uint32_t tmem_d = tmem_base + acc * BN;
-        for (int kb = 0; kb < kb_total; ++kb) {
-          mbar_wait(&sm.full[stage], phase);
-          tc_fence_after();
-          const uint32_t a0 = smem_u32(sm.a[stage]);
-          const uint32_t b0 = smem_u32(sm.b[stage]);
-#pragma unroll
-          for (int k = 0; k < BK / 8; ++k) {
-            const uint64_t ad = make_sw128_desc(a0 + k * 32);
-            const uint64_t bd = make_sw128_desc(b0 + k * 32);
-            tc_mma_tf32(tmem_d, ad, bd, idesc, (kb | k) != 0);
-          }
-          tc_commit(&sm.empty[stage]);  // smem slot free once these MMAs retire
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-        tc_commit(&sm.tfull[acc]);  // accumulator ready for the epilogue
-      }
-    }
-  } else {
-    // ===== epilogue: warps 2..5 =====
-    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
-    int local = 0;
-    for (int t = blockIdx.x; t < total_tiles; t += gridDim.x, ++local) {
-      int mb, nb;
-      tile_coords(s, t, mb, nb);
-      const int acc = local & 1;
-      const uint32_t acc_phase = (local >> 1) & 1;
-      mbar_wait(&sm.tfull[acc], acc_phase);
-      tc_fence_after();
-      const int row = mb * BM + quarter * 32 + lane;
-      const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
-#pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        uint32_t v[32];
-        tmem_ld32(taddr + c0, v);
-        const int col = nb * BN + c0;
-        if (row < s.M) {
-          float *dst = C + (size_t)row * s.N + col;
-          const unsigned long long g0 = (unsigned long long)row * s.m_complex + (col >> 1);
-          const bool full = (col + 32 <= s.N) && (g0 + 16 <= s.cov) &&
-                            ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0);
-          if (full) {
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-              reinterpret_cast<float4 *>(dst)[q] =
-                  make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
-                              __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
-          } else {
-#pragma unroll
-            for (int q = 0; q < 32; ++q) {
-              const int c = col + q;
-              if (c < s.N && (unsigned long long)row * s.m_complex + (c >> 1) < s.cov)
-                dst[q] = __uint_as_float(v[q]);
-            }
-          }
-        }
-      }
-      tc_fence_before();
-      mbar_arrive(&sm.tempty[acc]);
-    }
-  }
-
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  if (warp == 1) {
-    __syncwarp();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(kTmemCols));
-  }
-}
-
 // ---------------------------------------------------------------------------
 // v2: all four operand tiles in every stage, three products per k-step.
 //
@@ -409,6 +255,8 @@ k_cgemm_tf32x3(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
 // accumulator, so K is walked once instead of three times: 2/3 of v1's
 // L2->SMEM operand traffic for the same tensor work.
 constexpr int BK2 = 16;
+// k-blocks (of BK2 interleaved k) per fresh-accumulator chunk: 512 of K
+constexpr int kCgemmChunkKb = 32;
 // ring depth: stages of (2 BM + 2 BN) x 16 fp32 -- 32 KiB at BN = 128, 48 KiB
 // at BN = 256 -- as many as fit next to the barriers (192 KiB either way); the
 // narrow-tile case needs the depth to cover L2 latency (each stage is only
@@ -440,14 +288,30 @@ __device__ __forceinline__ uint64_t make_sw64_desc(uint32_t saddr) {
   return d;
 }
 
+// K-chunked accumulation.  The tensor core adds each MMA's K=8 partial into
+// the FP32 accumulator with less than round-to-nearest accuracy, so one
+// accumulator over all of K loses accuracy about linearly in K (measured:
+// 4.8e-6 rel. Frobenius at 1024^3, 3.8e-5 at 8192^3).  Instead every K chunk
+// of kb_chunk k-blocks goes into a FRESH accumulator (the first MMA of the
+// chunk does not accumulate); the two TMEM accumulators alternate per chunk,
+// and the epilogue warps drain each finished chunk into per-thread FP32
+// running sums (round-to-nearest adds, fixed chunk order -> deterministic)
+// while the MMA warp fills the other accumulator.  The tile's sums are
+// written out after its last chunk.  Eight epilogue warps: warps w and w+4
+// share TMEM lane quarter w % 4 and split the tile's columns in halves, so a
+// thread holds BN / 2 running sums.
+constexpr int kEpiWarps = 8;
+constexpr int GEMM2_THREADS = 64 + 32 * kEpiWarps;
+
 template <int BN>
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
+__global__ void __launch_bounds__(GEMM2_THREADS, 1)
 k_cgemm_fused4(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                const GemmShape s, float *__restrict__ C, unsigned *panel_done) {
   extern __shared__ uint8_t smem_raw[];
   Smem2<BN> &sm = *reinterpret_cast<Smem2<BN> *>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr int STAGES2 = stages2<BN>();
+  constexpr int HALF = BN / 2;  // columns per epilogue thread
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr uint32_t kTmemCols = 2 * BN;
   constexpr uint32_t kStageBytes = (2 * BM + 2 * BN) * BK2 * 4;
@@ -461,7 +325,7 @@ k_cgemm_fused4(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&sm.tfull[i], 1);
-      mbar_init(&sm.tempty[i], 128);
+      mbar_init(&sm.tempty[i], kEpiWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -506,98 +370,114 @@ k_cgemm_fused4(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
       constexpr uint32_t idesc = make_idesc(BM, BN);
       int stage = 0;
       uint32_t phase = 0;
-      int local = 0;
-      for (int u = blockIdx.x; u < total_units; u += gridDim.x, ++local) {
-        const int acc = local & 1;
-        const uint32_t acc_phase = (local >> 1) & 1;
-        mbar_wait(&sm.tempty[acc], acc_phase ^ 1);
-        tc_fence_after();
-        const uint32_t tmem_d = tmem_base + acc * BN;
+      uint32_t chunk = 0;  // chunks issued by this CTA: accumulator = chunk & 1
+      for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
         const int ks = u % s.ksplit, kb0 = ks * kbs / s.ksplit, kb1 = (ks + 1) * kbs / s.ksplit;
-        for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&sm.full[stage], phase);
+        for (int c0 = kb0; c0 < kb1; c0 += s.kb_chunk, ++chunk) {
+          const int c1 = min(kb1, c0 + s.kb_chunk);
+          const uint32_t acc = chunk & 1;
+          mbar_wait(&sm.tempty[acc], ((chunk >> 1) & 1) ^ 1);
           tc_fence_after();
-          const uint32_t ah = smem_u32(sm.a_hi[stage]), al = smem_u32(sm.a_lo[stage]);
-          const uint32_t bh = smem_u32(sm.b_hi[stage]), bl = smem_u32(sm.b_lo[stage]);
+          const uint32_t tmem_d = tmem_base + acc * BN;
+          for (int kb = c0; kb < c1; ++kb) {
+            mbar_wait(&sm.full[stage], phase);
+            tc_fence_after();
+            const uint32_t ah = smem_u32(sm.a_hi[stage]), al = smem_u32(sm.a_lo[stage]);
+            const uint32_t bh = smem_u32(sm.b_hi[stage]), bl = smem_u32(sm.b_lo[stage]);
 #pragma unroll
-          for (int k = 0; k < BK2 / 8; ++k) {
-            const uint32_t off = k * 32;
-            // small terms first, then the main product
-            tc_mma_tf32(tmem_d, make_sw64_desc(ah + off), make_sw64_desc(bl + off), idesc,
-                        kb != kb0 || k != 0);
-            tc_mma_tf32(tmem_d, make_sw64_desc(al + off), make_sw64_desc(bh + off), idesc, 1);
-            tc_mma_tf32(tmem_d, make_sw64_desc(ah + off), make_sw64_desc(bh + off), idesc, 1);
+            for (int k = 0; k < BK2 / 8; ++k) {
+              const uint32_t off = k * 32;
+              // small terms first, then the main product; the chunk's first
+              // MMA starts a fresh accumulator
+              tc_mma_tf32(tmem_d, make_sw64_desc(ah + off), make_sw64_desc(bl + off), idesc,
+                          kb != c0 || k != 0);
+              tc_mma_tf32(tmem_d, make_sw64_desc(al + off), make_sw64_desc(bh + off), idesc, 1);
+              tc_mma_tf32(tmem_d, make_sw64_desc(ah + off), make_sw64_desc(bh + off), idesc, 1);
+            }
+            tc_commit(&sm.empty[stage]);
+            if (++stage == STAGES2) {
+              stage = 0;
+              phase ^= 1;
+            }
           }
-          tc_commit(&sm.empty[stage]);
-          if (++stage == STAGES2) {
-            stage = 0;
-            phase ^= 1;
-          }
+          tc_commit(&sm.tfull[acc]);
         }
-        tc_commit(&sm.tfull[acc]);
       }
     }
   } else {
-    const int quarter = warp & 3;
-    int local = 0;
-    for (int u = blockIdx.x; u < total_units; u += gridDim.x, ++local) {
+    // ===== epilogue: warps 2 .. 2 + kEpiWarps - 1 =====
+    const int quarter = warp & 3;               // TMEM lane quarter this warp may access
+    const int half = (warp - 2) / 4;            // which half of the tile's columns
+    uint32_t chunk = 0;
+    for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
       int mb, nb;
       tile_coords(s, u / s.ksplit, mb, nb);
-      const int acc = local & 1;
-      const uint32_t acc_phase = (local >> 1) & 1;
-      mbar_wait(&sm.tfull[acc], acc_phase);
-      tc_fence_after();
+      const int ks = u % s.ksplit, kb0 = ks * kbs / s.ksplit, kb1 = (ks + 1) * kbs / s.ksplit;
+      const uint32_t lane_base = tmem_base + ((uint32_t)(quarter * 32) << 16) + half * HALF;
+      float sum[HALF];
+#pragma unroll
+      for (int j = 0; j < HALF; ++j) sum[j] = 0.f;
+      for (int c0 = kb0; c0 < kb1; c0 += s.kb_chunk, ++chunk) {
+        const uint32_t acc = chunk & 1;
+        mbar_wait(&sm.tfull[acc], (chunk >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int q = 0; q < HALF / 32; ++q) {
+          uint32_t v[32];
+          tmem_ld32(lane_base + acc * BN + 32 * q, v);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) sum[32 * q + j] = __fadd_rn(sum[32 * q + j], __uint_as_float(v[j]));
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.tempty[acc]);
+      }
       const int row = mb * BM + quarter * 32 + lane;
-      const uint32_t taddr = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
-#pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        uint32_t v[32];
-        tmem_ld32(taddr + c0, v);
-        const int col = nb * BN + c0;
-        if (row < s.M) {
-          float *dst = C + (size_t)row * s.N + col;
+      const int col0 = nb * BN + half * HALF;
+      if (row < s.M) {
+        float *dst = C + (size_t)row * s.N + col0;
+#pragma unroll
+        for (int q = 0; q < HALF / 32; ++q) {
+          const int col = col0 + 32 * q;
+          float *d = dst + 32 * q;
           const unsigned long long g0 = (unsigned long long)row * s.m_complex + (col >> 1);
           const bool full = (col + 32 <= s.N) && (g0 + 16 <= s.cov) &&
-                            ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0);
+                            ((reinterpret_cast<uintptr_t>(d) & 15u) == 0);
           if (s.ksplit > 1) {  // K half: add onto the zeroed C
             if (full) {
 #pragma unroll
-              for (int q = 0; q < 8; ++q)
-                asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4 * q),
-                             "f"(__uint_as_float(v[4 * q])), "f"(__uint_as_float(v[4 * q + 1])),
-                             "f"(__uint_as_float(v[4 * q + 2])), "f"(__uint_as_float(v[4 * q + 3]))
+              for (int j = 0; j < 8; ++j)
+                asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(d + 4 * j),
+                             "f"(sum[32 * q + 4 * j]), "f"(sum[32 * q + 4 * j + 1]),
+                             "f"(sum[32 * q + 4 * j + 2]), "f"(sum[32 * q + 4 * j + 3])
                              : "memory");
             } else {
 #pragma unroll
-              for (int q = 0; q < 32; ++q) {
-                const int c = col + q;
+              for (int j = 0; j < 32; ++j) {
+                const int c = col + j;
                 if (c < s.N && (unsigned long long)row * s.m_complex + (c >> 1) < s.cov)
-                  atomicAdd(dst + q, __uint_as_float(v[q]));
+                  atomicAdd(d + j, sum[32 * q + j]);
               }
             }
           } else if (full) {
 #pragma unroll
-            for (int q = 0; q < 8; ++q)
-              reinterpret_cast<float4 *>(dst)[q] =
-                  make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
-                              __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+            for (int j = 0; j < 8; ++j)
+              reinterpret_cast<float4 *>(d)[j] = make_float4(sum[32 * q + 4 * j], sum[32 * q + 4 * j + 1],
+                                                             sum[32 * q + 4 * j + 2], sum[32 * q + 4 * j + 3]);
           } else {
 #pragma unroll
-            for (int q = 0; q < 32; ++q) {
-              const int c = col + q;
-              if (c < s.N && (unsigned long long)row * s.m_complex + (c >> 1) < s.cov)
-                dst[q] = __uint_as_float(v[q]);
+            for (int j = 0; j < 32; ++j) {
+              const int c = col + j;
+              if (c < s.N && (unsigned long long)row * s.m_complex + (c >> 1) < s.cov) d[j] = sum[32 * q + j];
             }
           }
         }
       }
-      tc_fence_before();
-      mbar_arrive(&sm.tempty[acc]);
       if (panel_done != nullptr) {
         // publish "tile done" for its row panel (group of GM m-blocks) so the
         // copy stream can stream that panel to the host while tiles compute
         __threadfence();
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
         if (warp == 2 && lane == 0) {
           __threadfence_system();
           atomicAdd(&panel_done[mb / kGroupM], 1u);
@@ -693,7 +573,7 @@ int launch_gemm2(cudaStream_t s, int dev, const CUtensorMap &ma, const CUtensorM
     KAAS_CUDA(cudaEventRecord(ev_ready, s));
     KAAS_CUDA(cudaStreamWaitEvent(po->out_stream, ev_ready, 0));
   }
-  k_cgemm_fused4<BN><<<grid, GEMM_THREADS, smem, s>>>(ma, mb, shape, C,
+  k_cgemm_fused4<BN><<<grid, GEMM2_THREADS, smem, s>>>(ma, mb, shape, C,
                                                       progressive ? sc->panel_done : nullptr);
   count_launch();
   KAAS_CUDA(cudaGetLastError());
@@ -720,26 +600,6 @@ int launch_gemm2(cudaStream_t s, int dev, const CUtensorMap &ma, const CUtensorM
   if (copied < po->bytes)
     KAAS_CUDA(cudaMemcpyAsync((char *)po->host + copied, (const char *)C + copied,
                               po->bytes - copied, cudaMemcpyDeviceToHost, po->out_stream));
-  return 0;
-}
-
-bool cgemm_v1() {
-  const char *e = getenv("KAAS_CGEMM_V");  // dev A/B: "1" = segment-pass kernel
-  return e && e[0] == '1';
-}
-
-template <int BN>
-int launch_gemm(cudaStream_t s, int dev, const CUtensorMap &ma, const CUtensorMap &mb,
-                const GemmShape &shape, float *C) {
-  const size_t smem = sizeof(Smem<BN>) + 1024;
-  KAAS_CUDA(cudaFuncSetAttribute(k_cgemm_tf32x3<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
-  const int tiles = shape.num_m * shape.num_n;
-  int grid = device_props(dev).sm_count;
-  if (grid > tiles) grid = tiles;
-  k_cgemm_tf32x3<BN><<<grid, GEMM_THREADS, smem, s>>>(ma, mb, shape, C);
-  count_launch();
-  KAAS_CUDA(cudaGetLastError());
   return 0;
 }
 
@@ -787,7 +647,8 @@ int launch_cgemm(cudaStream_t s, int dev, int n, int m, int k, uint64_t cov, con
     count_launch();
   }
   if (!(b_ext && prep->b_ready)) {
-    dim3 gb((m + 31) / 32, (k + 31) / 32);
+    const uint64_t tiles = (uint64_t)((m + 31) / 32) * (uint64_t)((k + 31) / 32);
+    dim3 gb((unsigned)(tiles < (uint64_t)sms * 16 ? tiles : (uint64_t)sms * 16));
     // also zero-fills the K padding columns [2k, ldk)
     k_prep_b<<<gb, dim3(32, 8), 0, s>>>(k, m, ldk, reinterpret_cast<const float2 *>(B), Bhi, Blo);
     count_launch();
@@ -799,25 +660,19 @@ int launch_cgemm(cudaStream_t s, int dev, int n, int m, int k, uint64_t cov, con
   const int N = 2 * m;
   const int tiles256 = ((n + BM - 1) / BM) * ((N + 255) / 256);
   const bool full_cov = cov >= (uint64_t)n * m;
-  const char *ke = getenv("KAAS_CGEMM_KSPLIT");  // dev A/B: 0 = never split K
-  const bool ksplit2 = !(ke && ke[0] == '0') && !cgemm_v1() && full_cov && tiles256 < sms &&
-                       2 * tiles256 <= sms && ldk / BK2 >= 16;
+  const char *ke = KAAS_DEV_ENV("KAAS_CGEMM_KSPLIT");  // dev A/B: 0 = never split K
+  const bool ksplit2 = !(ke && ke[0] == '0') && full_cov && tiles256 < sms && 2 * tiles256 <= sms &&
+                       ldk / BK2 >= 16;
   const bool narrow = tiles256 < sms && !ksplit2;
   const int BNv = narrow ? 128 : 256;
 
   CUtensorMap ma, mbm;
-  const bool v1 = cgemm_v1();
-  if (v1) {
-    if ((rc = make_map(&ma, Ahi, (uint64_t)2 * n, ldk, BM))) return rc;
-    if ((rc = make_map(&mbm, Bhi, (uint64_t)2 * N, ldk, BNv))) return rc;
-  } else {
-    if ((rc = make_map(&ma, Ahi, (uint64_t)2 * n, ldk, BM, BK2, CU_TENSOR_MAP_SWIZZLE_64B))) return rc;
-    if ((rc = make_map(&mbm, Bhi, (uint64_t)2 * N, ldk, BNv, BK2, CU_TENSOR_MAP_SWIZZLE_64B))) return rc;
-  }
+  if ((rc = make_map(&ma, Ahi, (uint64_t)2 * n, ldk, BM, BK2, CU_TENSOR_MAP_SWIZZLE_64B))) return rc;
+  if ((rc = make_map(&mbm, Bhi, (uint64_t)2 * N, ldk, BNv, BK2, CU_TENSOR_MAP_SWIZZLE_64B))) return rc;
   GemmShape shape;
   shape.M = n;
   shape.N = N;
-  shape.kb_per_seg = ldk / BK;
+  shape.kb_per_seg = ldk / BK2;
   shape.a_lo_row = n;
   shape.b_lo_row = N;
   shape.num_m = (n + BM - 1) / BM;
@@ -825,15 +680,11 @@ int launch_cgemm(cudaStream_t s, int dev, int n, int m, int k, uint64_t cov, con
   shape.m_complex = m;
   shape.cov = cov;
   shape.ksplit = ksplit2 ? 2 : 1;
+  shape.kb_chunk = kCgemmChunkKb;
+  if (const char *ce = KAAS_DEV_ENV("KAAS_CGEMM_CHUNK")) shape.kb_chunk = atoi(ce) > 0 ? atoi(ce) : 1 << 30;
   if (ksplit2) KAAS_CUDA(cudaMemsetAsync(C, 0, (size_t)n * m * 8, s));
-  if (!v1) {
-    shape.kb_per_seg = ldk / BK2;
-    return narrow ? launch_gemm2<128>(s, dev, ma, mbm, shape, C, sc, po)
-                  : launch_gemm2<256>(s, dev, ma, mbm, shape, C, sc, po);
-  }
-  rc = narrow ? launch_gemm<128>(s, dev, ma, mbm, shape, C) : launch_gemm<256>(s, dev, ma, mbm, shape, C);
-  if (rc) return rc;
-  return po ? plain_copy_after(s, po, C) : 0;
+  return narrow ? launch_gemm2<128>(s, dev, ma, mbm, shape, C, sc, po)
+                : launch_gemm2<256>(s, dev, ma, mbm, shape, C, sc, po);
 }
 
 }  // namespace kaas

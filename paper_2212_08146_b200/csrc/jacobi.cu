@@ -970,12 +970,14 @@ k_jacobi_tmem(const __grid_constant__ ChainParams p, float *partials, unsigned *
       unsigned spins = 0;
       while (pending) {
         if (++spins > (1u << 22)) __trap();  // a lost producer: fail loudly, never hang
+#ifdef KAAS_DEV
         if (p.tagged == 3 && spins > 1) break;  // dev: no waiting (compute-only timing; wrong results)
         if (spins > 1 && p.poll_ns) {  // dev A/B: busy back-off (cycles) between polls
           const long long t = clock64();
           while (clock64() - t < p.poll_ns) {
           }
         }
+#endif
 #pragma unroll
         for (int u = 0; u < kColC4; ++u)
           if (pending & (1u << u)) q[u] = ld_relaxed_u64x4(src + 4 * (cbase + 32 * u));
@@ -1120,7 +1122,7 @@ unsigned *&jacobi_trace_buffer() {
 }
 
 bool use_cols_kernel(int dev, int n, uint64_t cov, int blocks) {
-  const char *e = getenv("KAAS_JACOBI_PATH");  // dev A/B: cols (default where it fits)
+  const char *e = KAAS_DEV_ENV("KAAS_JACOBI_PATH");  // dev A/B: cols (default where it fits)
   if (e && e[0] != 'c') return false;
   return n % 4 == 0 && n >= 2048 && n <= kColW * 32 * kColC4 * 4 &&
          (cov + blocks - 1) / blocks <= (uint64_t)kColRows &&
@@ -1129,7 +1131,7 @@ bool use_cols_kernel(int dev, int n, uint64_t cov, int blocks) {
 
 // the band in TMEM + registers + smem (default); KAAS_JACOBI_TMEM=0 = L2 tier
 bool use_tmem_kernel() {
-  const char *e = getenv("KAAS_JACOBI_TMEM");  // dev A/B
+  const char *e = KAAS_DEV_ENV("KAAS_JACOBI_TMEM");  // dev A/B
   return !(e && e[0] == '0');
 }
 
@@ -1146,12 +1148,12 @@ int rows_threads(int dev, uint64_t cov) {
 bool rows_prefetch() {
   // dev A/B: hoisting the next sweep's first A loads above the grid barrier
   // measured slower (7.02 vs 6.41 us/sweep), so it is off by default
-  const char *e = getenv("KAAS_JACOBI_PREFETCH");
+  const char *e = KAAS_DEV_ENV("KAAS_JACOBI_PREFETCH");
   return e && e[0] == '1';
 }
 
 bool use_rows_kernel(int n) {
-  const char *e = getenv("KAAS_JACOBI_PATH");  // dev A/B: rows (default) | generic
+  const char *e = KAAS_DEV_ENV("KAAS_JACOBI_PATH");  // dev A/B: rows (default) | generic
   if (e && e[0] == 'g') return false;
   return n % 4 == 0 && (size_t)n * 4 <= 160 * 1024;
 }
@@ -1268,7 +1270,7 @@ int launch_jacobi_chain(cudaStream_t s, int dev, const JacobiChain &c, StreamScr
   bool use_rows = use_rows_kernel(c.n) && aligned16(c.A);
   for (int t = 0; t < c.sweeps && use_rows; ++t)
     if (!aligned16(c.x_in[t])) use_rows = false;
-  const char *xd = getenv("KAAS_JACOBI_XDIRECT");  // dev A/B (default on)
+  const char *xd = KAAS_DEV_ENV("KAAS_JACOBI_XDIRECT");  // dev A/B (default on)
   const bool xdirect = !(xd && xd[0] == '0');
   const bool pf = rows_prefetch();
   const void *rfn = xdirect ? (pf ? (const void *)k_jacobi_rows<true, true, true>
@@ -1325,17 +1327,20 @@ int launch_jacobi_chain(cudaStream_t s, int dev, const JacobiChain &c, StreamScr
       // in-place sweep) publishes x through tags instead of grid barriers
       // (every row must be produced each sweep: full coverage)
       bool chained = sc->jac_xt != nullptr && c.n <= kJacTaggedMaxN && c.cov >= (uint64_t)c.n;
-      if (const char *e = getenv("KAAS_JACOBI_TAGS"))  // dev A/B: 0 = grid barrier per sweep
+      if (const char *e = KAAS_DEV_ENV("KAAS_JACOBI_TAGS"))  // dev A/B: 0 = grid barrier per sweep
         chained = chained && e[0] != '0';
       for (int t = done; t < done + cnt && chained; ++t)
         chained = c.x_in[t] != c.x_out[t] && (t == done || c.x_in[t] == c.x_out[t - 1]);
       if (chained) {
-        p.tagged = getenv("KAAS_JACOBI_NOWAIT") ? 3 : 1;  // dev: 3 = compute-only timing
+        p.tagged = 1;
+#ifdef KAAS_DEV
+        if (KAAS_DEV_ENV("KAAS_JACOBI_NOWAIT")) p.tagged = 3;  // dev: compute-only timing
+#endif
         static unsigned *trace_buf = nullptr;  // dev: KAAS_JACOBI_TRACE=1 (tools/jtrace.py)
-        if (getenv("KAAS_JACOBI_TRACE") && !trace_buf) cudaMalloc((void **)&trace_buf, 32 * 148 * 3 * 4);
-        p.trace = getenv("KAAS_JACOBI_TRACE") ? trace_buf : nullptr;
+        if (KAAS_DEV_ENV("KAAS_JACOBI_TRACE") && !trace_buf) cudaMalloc((void **)&trace_buf, 32 * 148 * 3 * 4);
+        p.trace = KAAS_DEV_ENV("KAAS_JACOBI_TRACE") ? trace_buf : nullptr;
         jacobi_trace_buffer() = p.trace;
-        const char *pe = getenv("KAAS_JACOBI_POLL_NS");  // dev A/B
+        const char *pe = KAAS_DEV_ENV("KAAS_JACOBI_POLL_NS");  // dev A/B
         p.poll_ns = pe ? atoi(pe) : 0;
       }
       const bool tm = use_tmem_kernel();
@@ -1382,11 +1387,13 @@ int launch_jacobi_chain(cudaStream_t s, int dev, const JacobiChain &c, StreamScr
 
 }  // namespace kaas
 
-// dev only (not in include/kaas_b200.h): copy the last traced Jacobi chain's
-// per-CTA timestamps (KAAS_JACOBI_TRACE=1) to the host; tools/jtrace.py
+#ifdef KAAS_DEV
+// dev build only (not in include/kaas_b200.h): copy the last traced Jacobi
+// chain's per-CTA timestamps (KAAS_JACOBI_TRACE=1) to the host; tools/jtrace.py
 extern "C" int kaas_dev_jacobi_trace(void *host, unsigned long bytes) {
   unsigned *buf = kaas::jacobi_trace_buffer();
   if (!buf) return 1;
   if (bytes > 32ul * 148 * 3 * 4) bytes = 32ul * 148 * 3 * 4;
   return cudaMemcpy(host, buf, bytes, cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 2;
 }
+#endif

@@ -89,6 +89,19 @@ static int stream_device(cudaStream_t s, int *dev) {
   return 0;
 }
 
+// Make the calling thread's current device the one `stream` belongs to, so
+// every export works from any thread (a pool's worker threads, or a caller
+// that drives an idle executor inline) whatever device it last touched.
+static int bind_stream_device(cudaStream_t s) {
+  int dev = 0, cur = -1;
+  KAAS_CUDA(cudaStreamGetDevice(s, &dev));
+  KAAS_CUDA(cudaGetDevice(&cur));
+  if (cur != dev) KAAS_CUDA(cudaSetDevice(dev));
+  return 0;
+}
+
+__global__ void k_inject_fault() { __trap(); }
+
 // ---------------------------------------------------------------------------
 // kernel table: literal signature, buffer count, written args
 // (mirrors backend.py:236-243 plus the two new kernels)
@@ -609,6 +622,7 @@ int kaas_free_async(uint64_t stream, uint64_t dptr) {
 
 int kaas_memset_async(uint64_t dptr, int value, uint64_t bytes, uint64_t stream) {
   if (bytes == 0) return 0;
+  if (int rc = bind_stream_device((cudaStream_t)stream)) return rc;
   KAAS_CUDA(cudaMemsetAsync((void *)dptr, value, bytes, (cudaStream_t)stream));
   return 0;
 }
@@ -638,18 +652,21 @@ int kaas_host_unregister(void *ptr) {
 
 int kaas_memcpy_h2d_async(uint64_t dst, const void *src, uint64_t bytes, uint64_t stream) {
   if (bytes == 0) return 0;
+  if (int rc = bind_stream_device((cudaStream_t)stream)) return rc;
   KAAS_CUDA(cudaMemcpyAsync((void *)dst, src, bytes, cudaMemcpyHostToDevice, (cudaStream_t)stream));
   return 0;
 }
 
 int kaas_memcpy_d2h_async(void *dst, uint64_t src, uint64_t bytes, uint64_t stream) {
   if (bytes == 0) return 0;
+  if (int rc = bind_stream_device((cudaStream_t)stream)) return rc;
   KAAS_CUDA(cudaMemcpyAsync(dst, (const void *)src, bytes, cudaMemcpyDeviceToHost, (cudaStream_t)stream));
   return 0;
 }
 
 int kaas_memcpy_d2d_async(uint64_t dst, uint64_t src, uint64_t bytes, uint64_t stream) {
   if (bytes == 0) return 0;
+  if (int rc = bind_stream_device((cudaStream_t)stream)) return rc;
   KAAS_CUDA(cudaMemcpyAsync((void *)dst, (const void *)src, bytes, cudaMemcpyDeviceToDevice,
                             (cudaStream_t)stream));
   return 0;
@@ -660,9 +677,37 @@ int kaas_enable_peer(int dev, int peer) {
   cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
   if (e == cudaErrorPeerAccessAlreadyEnabled) {
     cudaGetLastError();
-    return 0;
+  } else {
+    KAAS_CUDA(e);
   }
-  KAAS_CUDA(e);
+  // Cache entries come from the peer's stream-ordered pool: peer access to
+  // pool memory is granted per pool (cudaDeviceEnablePeerAccess covers only
+  // cudaMalloc memory), so let `dev` map `peer`'s pool allocations too.
+  if (dev != peer) {
+    cudaMemPool_t pool;
+    KAAS_CUDA(cudaDeviceGetDefaultMemPool(&pool, peer));
+    cudaMemAccessDesc desc = {};
+    desc.location.type = cudaMemLocationTypeDevice;
+    desc.location.id = dev;
+    desc.flags = cudaMemAccessFlagsProtReadWrite;
+    KAAS_CUDA(cudaMemPoolSetAccess(pool, &desc, 1));
+  }
+  return 0;
+}
+
+int kaas_device_check(int dev) {
+  KAAS_CUDA(cudaSetDevice(dev));
+  KAAS_CUDA(cudaDeviceSynchronize());  // a sticky fault reports here on every call
+  KAAS_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int kaas_inject_fault(uint64_t stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (int rc = bind_stream_device(s)) return rc;
+  k_inject_fault<<<1, 1, 0, s>>>();
+  count_launch();
+  KAAS_CUDA(cudaGetLastError());
   return 0;
 }
 
@@ -675,6 +720,7 @@ int kaas_can_access_peer(int dev, int peer, int *can) {
 int kaas_memcpy_p2p_async(uint64_t dst, int dst_dev, uint64_t src, int src_dev, uint64_t bytes,
                           uint64_t stream) {
   if (bytes == 0) return 0;
+  if (int rc = bind_stream_device((cudaStream_t)stream)) return rc;
   KAAS_CUDA(cudaMemcpyPeerAsync((void *)dst, dst_dev, (const void *)src, src_dev, bytes,
                                 (cudaStream_t)stream));
   return 0;

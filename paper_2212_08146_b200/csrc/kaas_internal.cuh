@@ -11,6 +11,17 @@
 
 namespace kaas {
 
+// ---- developer switches ------------------------------------------------------
+// A/B switches read from the environment exist only in developer builds
+// (make dev -> libkaas_b200_dev.so, -DKAAS_DEV).  The product library never
+// reads the environment: every switch folds to its default at compile time.
+#ifdef KAAS_DEV
+#include <cstdlib>
+#define KAAS_DEV_ENV(name) std::getenv(name)
+#else
+#define KAAS_DEV_ENV(name) (static_cast<const char *>(nullptr))
+#endif
+
 // ---- error plumbing --------------------------------------------------------
 void set_error(const std::string &msg);
 int fail(int code, const std::string &msg);

@@ -35,11 +35,10 @@ touch it is freed only after the request's streams drain.
 from __future__ import annotations
 
 import itertools
-import os
 import threading
 
 from collections import OrderedDict
-from dataclasses import dataclass, field
+from dataclasses import dataclass, field, replace
 
 import numpy as np
 
@@ -56,6 +55,7 @@ from .api import (
 from .cache import CacheState, DeviceBuffer
 from .faults import (
     BufferBusyError,
+    DeviceError,
     InvalidRequestError,
     KaasError,
     SizeMismatchError,
@@ -340,10 +340,18 @@ class GpuExecutor:
         self._plans_by_value: _LRU = _LRU(256)  # (buffers, invocations) -> plan
         self._plans_by_parts: _LRU = _LRU(256)  # (id(buffers), id(invocations)) -> plan
         pc = config.prepared_capacity
-        if pc is None and os.environ.get("KAAS_PREPARED_CAP"):  # dev A/B
-            pc = int(os.environ["KAAS_PREPARED_CAP"])
-        self._prep_cap = 4 * config.capacity if pc is None else pc
+        if pc is None:
+            # outside the ledger: 4x the ledger, but never more than half of
+            # what the device has beyond it (several executors may share a GPU)
+            total = native.device_info(self.device).total_mem
+            pc = max(0, min(4 * config.capacity, (total - config.capacity) // 2))
+        self._prep_cap = pc
         self._prep_bytes = 0
+        self._skipped: list = []  # zero-fills elided for the request being begun
+        # set when a CUDA fault left the device unusable (a sticky error): the
+        # executor then answers Internal without touching the device, and a
+        # pool's router stops placing requests here (service.py:71-78 analogue)
+        self.poisoned: str | None = None
 
     # -- device memory ------------------------------------------------------
 
@@ -359,6 +367,12 @@ class GpuExecutor:
         self._alloc(buf, self.s_exec)
         if name is None or name not in self._skip_zero:
             native.memset_async(buf.ptr, 0, buf.size, self.s_exec)
+        else:
+            # the plan proved the first kernel overwrites every byte; if the
+            # request fails before that kernel runs, begin() zero-fills it
+            self._skipped.append(buf)
+        if self._cur is None:  # a direct resolve_buffer call: contents final on return
+            self.s_exec.sync()
 
     def _drop(self, buf: DeviceBuffer) -> None:
         """on_drop hook: an entry left the table or an ephemeral was freed.
@@ -376,7 +390,7 @@ class GpuExecutor:
             owner = self._cur
         if owner is not None:
             owner.graveyard.append(ptr)  # freed on s_exec when the owner completes
-        else:
+        elif self.poisoned is None:  # a faulted context frees nothing (it is torn down whole)
             native.free_async(self.s_in if stream is None else stream, ptr)
 
     # -- prepared operands ------------------------------------------------------
@@ -410,7 +424,11 @@ class GpuExecutor:
         # eviction) keeps using scratch; the first cache hit prepares it
         if buf._hits == 0 or self._prep_bytes + nbytes > self._prep_cap:
             return None
-        slot = [native.malloc_async(self.s_exec, nbytes), nbytes, False]
+        try:
+            ptr = native.malloc_async(self.s_exec, nbytes)
+        except DeviceError:  # device memory short: this launch uses scratch instead
+            return None
+        slot = [ptr, nbytes, False]
         self._prep_bytes += nbytes
         if d is None:
             buf._derived = d = {}
@@ -521,6 +539,9 @@ class GpuExecutor:
                 f"buffer {arg.name!r}: store object {arg.key!r} is"
                 f" {len(payload)} bytes, request declares {arg.size}")
         cur = self._cur
+        standalone = cur is None  # resolve_buffer called directly (executor.py:233 API)
+        if standalone:
+            cur = _Req(0, None)
         if buf.ptr:
             self._wait_for_user(buf)
             self._fence_lends(buf)
@@ -528,7 +549,7 @@ class GpuExecutor:
         self._mark(buf)
         if not buf.ptr:
             self._alloc(buf, self.s_in)
-        if self.time_requests and not cur.has_fills:
+        if self.time_requests and not cur.has_fills and cur.events is not None:
             cur.events[4].record(self.s_in)
         cur.has_fills = True
         borrowed = False
@@ -552,6 +573,9 @@ class GpuExecutor:
             buf._ready.record(self.s_in)
             self.peers.publish(self.executor_id, buf, version, buf._ready)
         buf.dirty = False
+        if standalone:  # no request owns the copy: finish it before returning
+            self.s_in.sync()
+            cur.keepalive.clear()
         self.clock.advance_ns(self.backend.timing.fetch_time_ns(arg.size))
         stats.store_gets += 1
         stats.bytes_fetched += arg.size
@@ -733,23 +757,26 @@ class GpuExecutor:
         request -- so requests begun later see the same cache state."""
         t0 = self.clock.now_ns
         stats = _ReqStats()
+        if self.poisoned is not None:
+            return self._finish(req, stats, t0, Status.make_error(
+                "Internal", f"device {self.device} is unusable after a fault: {self.poisoned}"))
         plan = self._plan(req)
         if plan.error is not None:
             return self._finish(req, stats, t0, plan.error)
 
         self._req_seq += 1
         self._skip_zero = plan.skip_zero
+        self._skipped = []
         rec = _Req(self._req_seq, req)
-        rec.events = self._events()
         self._cur = rec
-        ev = rec.events
-        if self.time_requests:
-            ev[0].record(self.s_in)
-            self.s_exec.wait(ev[0])
-            self.s_out.wait(ev[0])
         resolved: dict[str, DeviceBuffer] = {}
         ephemerals: list[DeviceBuffer] = []
         try:
+            rec.events = ev = self._events()
+            if self.time_requests:
+                ev[0].record(self.s_in)
+                self.s_exec.wait(ev[0])
+                self.s_out.wait(ev[0])
             by_name = req.by_name
             for nm in plan.names:
                 arg = by_name[nm]
@@ -761,16 +788,27 @@ class GpuExecutor:
             self._launch(rec, plan, resolved)
             self._enqueue_flush(rec, plan.names, resolved, stats)
         except KaasError as exc:
+            if isinstance(exc, DeviceError):
+                self._check_poison()
             self._skip_zero = frozenset()
+            # the kernel that would have overwritten these never runs: they
+            # must read as zeros, like the reference's fresh allocations
+            # (a clean output entry survives the failure)
+            for buf in self._skipped:
+                if buf.ptr and self.poisoned is None:
+                    native.memset_async(buf.ptr, 0, buf.size, self.s_exec)
+            self._skipped = []
             # a host-detected failure enqueued no kernels; drain so the
             # request's fills/zero-fills finish before its buffers are freed
             self._cur = None
             self.complete()
             self._drain_streams_quietly()
             self._release(resolved, ephemerals, drop_dirty=True)
-            for ptr in rec.graveyard:
-                native.free_async(self.s_exec, ptr)
-            self._ev_pool.append(rec.events)
+            if self.poisoned is None:
+                for ptr in rec.graveyard:
+                    native.free_async(self.s_exec, ptr)
+            if rec.events is not None:
+                self._ev_pool.append(rec.events)
             return self._finish(req, stats, t0, Status.make_error(exc.kind, exc.message))
         self._release(resolved, ephemerals, drop_dirty=False)
         for key, _, _, _ in rec.pending:
@@ -791,9 +829,21 @@ class GpuExecutor:
             if through is not None and seq > through:
                 break
             ev = rec.events
-            if not block and not ev[1].done():
-                break
-            ev[1].sync()
+            if not block:
+                try:
+                    if not ev[1].done():
+                        break
+                except DeviceError:
+                    pass  # faulted: the sync below reports it for this request
+            try:
+                ev[1].sync()
+            except DeviceError as exc:
+                # the device faulted under this request: nothing it computed
+                # may reach the store; it (and every later one) fails in band
+                self._check_poison()
+                rec.pending = []
+                rec.response = replace(rec.response, per_invocation=(),
+                                       status=Status.make_error("Internal", str(exc)))
             for key, blob, size, buf in rec.pending:
                 if self._pinned_store:
                     version = self.store.put_owned(key, blob)
@@ -806,11 +856,12 @@ class GpuExecutor:
                 if (self.peers is not None and isinstance(version, int) and buf.ptr
                         and self.cache.entries.get(key) is buf and not buf.dirty):
                     self.peers.publish(self.executor_id, buf, version, None)
-            for ptr in rec.graveyard:
-                native.free_async(self.s_exec, ptr)
+            if self.poisoned is None:
+                for ptr in rec.graveyard:
+                    native.free_async(self.s_exec, ptr)
             self.dev_stats.requests += 1
             del self._inflight[seq]
-            if self.time_requests:  # spans read later (DeviceStats.resolve), events pooled then
+            if self.time_requests and self.poisoned is None:  # spans read later (DeviceStats.resolve)
                 self.dev_stats.defer(ev, rec.has_kernels, rec.has_fills)
             else:
                 self._ev_pool.append(ev)
@@ -937,6 +988,10 @@ class GpuExecutor:
                 buf.dirty = False
         rec.events[1].record(self.s_out)
 
+    def _check_poison(self) -> None:
+        if self.poisoned is None:
+            self.poisoned = native.device_check(self.device)
+
     def _drain_streams_quietly(self) -> None:
         """Failure-path drain: a sticky device error must not escape execute."""
         try:
@@ -998,6 +1053,11 @@ class GpuExecutor:
             self.complete()
         except KaasError:
             pass
+        if self.poisoned is not None:
+            # a faulted context: every device call fails; its memory goes
+            # with the process (or a device reset), only the ledger is cleared
+            self.cache.entries.clear()
+            return
         self._drain_streams_quietly()
         for key in list(self.cache.entries):
             buf = self.cache.entries[key]

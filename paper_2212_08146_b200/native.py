@@ -104,6 +104,8 @@ EXPORTS = {
     "kaas_init_device": [C.c_int],
     "kaas_device_info_get": [C.c_int, C.POINTER(DeviceInfo)],
     "kaas_launch_counter": [_pu64],
+    "kaas_device_check": [C.c_int],
+    "kaas_inject_fault": [_u64],
     "kaas_stream_create": [C.c_int, C.c_int, _pu64],
     "kaas_stream_destroy": [_u64],
     "kaas_stream_sync": [_u64],
@@ -202,6 +204,17 @@ def launch_counter() -> int:
     return v.value
 
 
+def device_check(dev: int) -> str | None:
+    """None when ``dev`` is usable, else the sticky error's text."""
+    rc = load().kaas_device_check(dev)
+    return None if rc == 0 else f"{last_error()} (code {rc})"
+
+
+def inject_fault(stream: "Stream") -> None:
+    """Tests only: a trapping kernel on ``stream`` (poisons the context)."""
+    call("kaas_inject_fault", stream.handle)
+
+
 _inited: set[int] = set()
 _init_lock = threading.Lock()
 
@@ -212,6 +225,13 @@ def init_device(dev: int) -> None:
             return
         call("kaas_init_device", dev)
         _inited.add(dev)
+
+
+def bind_thread(dev: int) -> None:
+    """Make ``dev`` the calling thread's current device (a pool worker does
+    this once at start; the C exports also bind each call's stream device)."""
+    init_device(dev)
+    call("kaas_init_device", dev)
 
 
 class Stream:

@@ -38,12 +38,15 @@ class KaasService:
                  devices: list[int] | None = None, executor_factory=None,
                  log_decisions: bool = False, max_inflight: int = 3, peer_fills: bool = True,
                  reserve_bytes: int = 0):
+        explicit_devices = devices is not None
         if executor_factory is None:
             devices = devices if devices is not None else visible_devices()
             if not devices:
                 raise RuntimeError("no CUDA devices visible (libkaas_b200 has no CPU path)")
         if n_executors is None:
-            n_executors = len(devices) if devices else 1
+            # the reference default is one executor (service.py:24); an explicit
+            # device list means one executor per listed GPU
+            n_executors = len(devices) if explicit_devices else 1
         if n_executors < 1:
             raise ValueError("need at least one executor")
         self.store = store
@@ -89,7 +92,16 @@ class KaasService:
         for t in self._threads:
             t.start()
 
+    def _after(self, executor) -> None:
+        """A faulted (poisoned) executor leaves the placement set."""
+        if getattr(executor, "poisoned", None) is not None and \
+                executor.executor_id not in self.router.down:
+            self.router.mark_down(executor.executor_id)
+
     def _worker(self, executor) -> None:
+        dev = getattr(executor, "device", None)
+        if dev is not None:
+            native.bind_thread(dev)  # this thread's current device, once
         if hasattr(executor, "begin"):
             return self._pipelined_worker(executor)
         q = self._queues[executor.executor_id]
@@ -124,6 +136,7 @@ class KaasService:
                 return
             req, fut = entry
             self.router.update_digest(eid, resp, req)
+            self._after(executor)
             fut.set_result(resp)
 
         executor.on_complete = on_complete
@@ -162,6 +175,7 @@ class KaasService:
                 continue
             if isinstance(rec, KaasResponse):  # failed on the host: nothing in flight
                 self.router.update_digest(eid, rec, req)
+                self._after(executor)
                 fut.set_result(rec)
                 continue
             futs[rec.seq] = (req, fut)
@@ -196,6 +210,7 @@ class KaasService:
                         self.router.update_digest(eid, failed, req)
                         raise
                     self.router.update_digest(eid, resp, req)
+                    self._after(ex)
                     return resp
             finally:
                 owner.release()

@@ -204,3 +204,145 @@ def test_peer_fills_preserve_decisions_and_bytes(cuda):
     assert sum(g.dev_stats.p2p_bytes for g in gexs) > 0 and peers.lends > 0
     for g in gexs:
         g.close()
+
+
+# -- the reference's direct resolve_buffer API (pkg/tests/test_executor.py:63-107)
+
+
+def _direct_executor(capacity=1 << 20):
+    store = PinnedStore()
+    return GpuExecutor(ExecutorConfig(capacity=capacity), store), store
+
+
+def test_resolve_buffer_called_directly(cuda):
+    """TestResolveBuffer (test_executor.py:63-107) against the GPU executor:
+    resolve_buffer works outside execute() -- zero-filled ephemerals, NotFound,
+    const hits, SizeMismatch, non-const refetch -- and the bytes are final
+    when it returns."""
+    from paper_2212_08146_b200.api import BufferArg
+    from paper_2212_08146_b200.faults import NotFoundError, SizeMismatchError
+    from paper_2212_08146_b200.gpu_executor import _ReqStats
+
+    ex, store = _direct_executor()
+    try:
+        buf = ex.resolve_buffer(BufferArg("tmp", 32, "inout", is_ephemeral=True))
+        assert buf.key is None and buf.pinned == 1
+        assert buf.snapshot() == b"\x00" * 32
+        ex.cache.free_ephemeral(buf)
+        with pytest.raises(NotFoundError):
+            ex.resolve_buffer(BufferArg("x", 8, "input", key="absent"))
+        store.put("w", bytes(range(64)))
+        arg = BufferArg("w", 64, "input", key="w", is_const=True)
+        first = _ReqStats()
+        b1 = ex.resolve_buffer(arg, first)
+        ex.cache.unpin(b1)
+        assert first.store_gets == 1 and b1.snapshot() == bytes(range(64))
+        second = _ReqStats()
+        b2 = ex.resolve_buffer(arg, second)
+        assert b2 is b1 and second.store_gets == 0 and second.cache_hits == 1
+        ex.cache.unpin(b2)
+        store.put("w60", bytes(60))
+        with pytest.raises(SizeMismatchError):
+            ex.resolve_buffer(BufferArg("w60", 64, "input", key="w60", is_const=True))
+        store.put("k", b"\x01" * 8)
+        karg = BufferArg("x", 8, "inout", key="k")
+        b1 = ex.resolve_buffer(karg)
+        ex.cache.unpin(b1)
+        store.put("k", b"\x02" * 8)
+        b2 = ex.resolve_buffer(karg)
+        assert b2.snapshot() == b"\x02" * 8
+        ex.cache.unpin(b2)
+    finally:
+        ex.close()
+
+
+def test_failed_request_leaves_zero_output_not_leftover_memory(cuda):
+    """A cgemm output's zero-fill is elided (the kernel overwrites every byte);
+    if a later buffer of the same request fails to resolve, the kernel never
+    runs and the output entry that stays cached (clean, as in the reference,
+    SURVEY App. A.8) must read as zeros -- never as leftover pool memory."""
+    from paper_2212_08146_b200.api import (BufferArg, KaasRequest, KernelInvocation,
+                                           LaunchDims, i32)
+    from paper_2212_08146_b200 import native
+
+    n = 64
+    store = PinnedStore()
+    ostore = DictStore()
+    ex = GpuExecutor(ExecutorConfig(capacity=8 << 20), store)
+    oex = OracleExecutor(8 << 20, ostore)
+    try:
+        rng = np.random.default_rng(3)
+        for s_ in (store, ostore):
+            s_.put("A", (rng.standard_normal(2 * n * n).astype("<f4")).tobytes())
+            s_.put("B", (rng.standard_normal(2 * n * n).astype("<f4")).tobytes())
+            s_.put("Z", bytes(8 * n * n))
+        # dirty the device pool with non-zero bytes the output may be carved from
+        junk = [native.malloc_async(ex.s_exec, 8 * n * n) for _ in range(8)]
+        for p in junk:
+            native.memset_async(p, 0x7F, 8 * n * n, ex.s_exec)
+        for p in junk:
+            native.free_async(ex.s_exec, p)
+        ex.s_exec.sync()
+        bad = KaasRequest("bad", (
+            BufferArg("A", 8 * n * n, "input", key="A", is_const=True),
+            BufferArg("B", 8 * n * n, "input", key="B", is_const=True),
+            BufferArg("C", 8 * n * n, "output", key="C"),
+            BufferArg("X", 64, "input", key="missing"),
+            BufferArg("R", 4, "output", is_ephemeral=True)), (
+            KernelInvocation("cgemm", LaunchDims(grid_x=n * n), (i32(n), i32(n), i32(n)), ("A", "B", "C")),
+            KernelInvocation("reduce_sum", LaunchDims(), (i32(16),), ("X", "R"))))
+        read = KaasRequest("read", (
+            BufferArg("C", 8 * n * n, "input", key="C", is_const=True),
+            BufferArg("Z", 8 * n * n, "input", key="Z", is_const=True),
+            BufferArg("O", 8 * n * n, "output", key="O")), (
+            KernelInvocation("vector_add", LaunchDims(grid_x=2 * n * n), (i32(2 * n * n),), ("C", "Z", "O")),))
+        for req in (bad, read):
+            g, o = ex.execute(req), oex.execute(req)
+            assert response_to_doc(g) == response_to_doc(o), req.request_id
+        assert not ex.execute(bad).status.ok
+        assert bytes(store.get("O")) == bytes(8 * n * n)
+        assert ex.execute(read).io_stats.cache_hits == 2
+    finally:
+        ex.close()
+
+
+POISON_SCRIPT = r"""
+import sys
+sys.path.insert(0, sys.argv[1])
+from paper_2212_08146_b200 import native
+from paper_2212_08146_b200 import workloads as W
+from paper_2212_08146_b200.hoststore import PinnedStore
+from paper_2212_08146_b200.pool import KaasService
+
+store = PinnedStore()
+W.seed_jacobi(store, 256, prefix="p")
+req = lambda i: W.jacobi_request(f"p{i}", 256, 4, "p/A/256", "p/b/256", "p/x0/256", "p/x", "p/r")
+with KaasService(store, n_executors=2, capacity=64 << 20, policy="rr", devices=[0]) as svc:
+    assert svc.submit(req(0)).status.ok
+    ex0 = svc.executors[0]
+    native.inject_fault(ex0.s_exec)       # a trapping kernel: a sticky device fault
+    r = svc.submit(req(1))                # routed to executor 1 (rr): same context -> fails
+    outs = [svc.submit(req(i)) for i in range(2, 6)]
+    assert all(not o.status.ok and o.status.error_kind == "Internal" for o in outs), outs
+    assert all(e.poisoned for e in svc.executors), [e.poisoned for e in svc.executors]
+    assert svc.router.down == {0, 1}
+print("POISON-OK")
+"""
+
+
+def test_device_fault_poisons_executor_and_router_routes_away(cuda, tmp_path):
+    """SURVEY §5 failure row: a sticky CUDA fault (fault injection: a kernel
+    that traps) marks the executor poisoned; every later request on it is
+    answered Internal in band without touching the device, and the router
+    stops placing requests there.  Runs in a subprocess -- the fault kills
+    that process's CUDA context."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "poison.py"
+    script.write_text(POISON_SCRIPT)
+    out = subprocess.run([sys.executable, str(script), root], capture_output=True, text=True,
+                         timeout=300)
+    assert "POISON-OK" in out.stdout, out.stdout + out.stderr

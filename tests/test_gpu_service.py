@@ -127,3 +127,94 @@ def test_gpu_report_v2_over_http(cuda):
     assert rep == g
     devs = meas["rr"]["devices"]
     assert len(devs) == 2 and all(d["kernel_launches"] > 0 for d in devs)
+
+
+def _decisions_only_kernels():
+    """The oracle's kernel table with the numerics dropped: same literal
+    types, arity, writes and FMA counts (virtual time), no data -- decisions
+    do not depend on kernel outputs."""
+    from oracle.kernels import KERNELS
+
+    def fma(kid):
+        if kid == "cgemm":
+            return lambda d, l, v: 4 * l[0].value * l[1].value * l[2].value
+        if kid == "jacobi_sweep":
+            return lambda d, l, v: l[0].value * l[0].value
+        raise KeyError(kid)
+    return {kid: (spec[0], spec[1], spec[2], fma(kid)) for kid, spec in KERNELS.items()
+            if kid in ("cgemm", "jacobi_sweep")}
+
+
+class _SizedStore:
+    """Oracle-side store: only object sizes matter for decisions."""
+
+    def __init__(self, sizes):
+        self.sizes = dict(sizes)
+
+    def get(self, key):
+        if key not in self.sizes:
+            raise KeyError(key)
+        return memoryview(bytearray(self.sizes[key]))
+
+    def put(self, key, payload):
+        self.sizes[key] = len(payload)
+
+
+@pytest.mark.parametrize("policy", ["affinity:2", "static", "exclusive", "rr"])
+def test_sixteen_client_mixed_decisions_replay(cuda, policy):
+    """BASELINE configs[3] (shrunk): 16 client threads, mixed cGEMM + Jacobi
+    under LRU pressure, 4 executors.  Every logged routing decision is
+    replayed through the oracle policy on the logged state (SURVEY §7.3
+    #10), and each executor's request sequence through an oracle executor:
+    statuses, IoStats, per-invocation and total virtual times identical."""
+    import threading
+
+    from oracle.executor import OracleExecutor
+    from oracle.router import OracleRouter
+    from paper_2212_08146_b200 import workloads as W
+    from paper_2212_08146_b200.api import response_to_doc
+
+    store = PinnedStore()
+    uni = W.mixed_universe(store, n_cgemm=6, cg_n=512, n_jacobi=6, jac_n=1024, seed=3)
+    reqs = W.mixed_requests(uni, 160, sweeps=20, seed=5)
+    cap = 3 * 4 * 1024 * 1024 + 2 * 2 * 1024 * 1024  # ~5 const matrices per executor: evictions
+    sizes = {k: len(store.get(k)) for k in store.keys()}
+    got = {}
+    with KaasService(store, n_executors=4, capacity=cap, policy=policy, devices=[0],
+                     log_decisions=True) as svc:
+        lock = threading.Lock()
+        it = iter(range(len(reqs)))
+
+        def client():
+            while True:
+                with lock:
+                    i = next(it, None)
+                if i is None:
+                    return
+                got[reqs[i].request_id] = svc.submit(reqs[i])
+
+        threads = [threading.Thread(target=client) for _ in range(16)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        decisions = list(svc.router.decisions)
+    assert len(decisions) == len(reqs) and all(r.status.ok for r in got.values())
+    by_id = {r.request_id: r for r in reqs}
+    # 1. decision function: the oracle policy on the logged state
+    orc = OracleRouter([0, 1, 2, 3], policy)
+    per_exec = {e: [] for e in range(4)}
+    for rid, chosen, state in decisions:
+        for e, (depth, items) in state.items():
+            orc.depth[e] = depth
+            orc.keys[e].clear()
+            orc.keys[e].update(items)
+        assert orc.pick(by_id[rid]) == chosen, rid
+        per_exec[chosen].append(rid)
+    # 2. each executor's sequence (FIFO per executor = routing order)
+    kernels = _decisions_only_kernels()
+    for e, rids in per_exec.items():
+        oex = OracleExecutor(cap, _SizedStore(sizes), kernels=kernels)
+        for rid in rids:
+            want = response_to_doc(oex.execute(by_id[rid]))
+            assert response_to_doc(got[rid]) == want, (e, rid)

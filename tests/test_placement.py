@@ -166,3 +166,30 @@ def test_exclusive_isolates_tenants_and_static_is_stable():
     s = Router([0, 1, 2, 3], parse_policy("static"))
     q = const_request("w1", "w2")
     assert len({s.route(q) for _ in range(20)}) == 1
+
+
+def test_new_policies_route_malformed_requests_instead_of_raising():
+    """A request with a non-str id (or non-str const keys) is routed -- the
+    executor then answers InvalidRequest in band, as with the reference's
+    own policies -- never an exception out of Router.route."""
+    from paper_2212_08146_b200.api import BufferArg, KaasRequest
+    from paper_2212_08146_b200.placement import Router, parse_policy
+
+    bad = [KaasRequest(5), KaasRequest(None), KaasRequest(""),
+           KaasRequest("r", (BufferArg("a", 4, "input", key=7, is_const=True),))]
+    for spec in ("static", "exclusive"):
+        r = Router([0, 1, 2], parse_policy(spec))
+        for req in bad:
+            assert r.route(req) in (0, 1, 2)
+
+
+def test_router_skips_executors_marked_down():
+    from paper_2212_08146_b200.api import KaasRequest
+    from paper_2212_08146_b200.placement import Router, parse_policy
+
+    r = Router([0, 1, 2], parse_policy("rr"))
+    r.mark_down(1)
+    assert [r.route(KaasRequest(f"q{i}")) for i in range(4)] == [0, 2, 0, 2]
+    r.mark_down(0)
+    r.mark_down(2)
+    assert r.route(KaasRequest("all-down")) in (0, 1, 2)  # still answered (in band)

@@ -1,6 +1,7 @@
 """Dev: per-CTA phase timestamps of the Jacobi column kernel (sweeps 100..131).
 
-    KAAS_JACOBI_TRACE=1 python tools/jtrace.py [n]
+    make -C paper_2212_08146_b200/csrc dev   # the trace exists only in the dev build
+    python tools/jtrace.py [n]
 
 Stamps (globaltimer, ns): t0 = CTA's warp 0 has its x, t1 = warp 0's row
 partials done, t2 = the CTA's rows published.  Prints the per-sweep spread
@@ -16,6 +17,7 @@ import numpy as np
 
 sys.path.insert(0, ".")
 os.environ.setdefault("KAAS_JACOBI_TRACE", "1")
+os.environ.setdefault("KAAS_B200_LIB", "paper_2212_08146_b200/libkaas_b200_dev.so")
 from paper_2212_08146_b200 import native  # noqa: E402
 sys.argv = [sys.argv[0], "jacobi"] + sys.argv[1:2] + ["500", "1"]
 sys.path.insert(0, "tools")
