@@ -48,6 +48,9 @@ METRIC = "KaaS req/s & p50/p99 latency (cGEMM, Jacobi) at 1/2/4/8 B200; % roofli
 JACOBI_N, JACOBI_SWEEPS = 4096, 500
 # L2-resident re-read bandwidth, 64 MiB buffer, all SMs (tools/l2bw.cu, profiles/l2bw_r01.txt)
 L2_PEAK_GBS = 19047.7
+# the x exchange alone (no arithmetic), 148 CTAs, 256-bit per-lane polls:
+# best of the runs in profiles/r01/probes/xchg.txt
+XCHG_FLOOR_US = 1.165
 
 
 def percentile(vals, q):
@@ -292,7 +295,9 @@ def measure_mixed(device, clients=16, count=160, policy="affinity:8", capacity=5
             "p99_ms": percentile(lat, 0.99) * 1e3, "hit_rate": hits / max(1, hits + misses),
             "h2d_bytes": h2d, "h2d_gbs": h2d / (h2d_ms * 1e6) if h2d_ms else None,
             "evictions": evictions, "gpus": len(devices), "requests_per_gpu": per_gpu,
-            "device_busy_frac": ex_dev_ms / (wall * 1e3 * len(devices))}
+            "device_span_sum_over_wall": ex_dev_ms / (wall * 1e3 * len(devices)),
+            "note": "device spans of pipelined requests overlap (up to 3 in flight per GPU), "
+                    "so their sum over the wall time can exceed 1"}
 
 
 def measure_peer_fill(device, n=8192, reps=3):
@@ -339,6 +344,87 @@ def measure_peer_fill(device, n=8192, reps=3):
             "fill_bytes": 2 * 8 * n * n,
             "h2d_gbs": statistics.median(h2d), "p2p_gbs": statistics.median(p2p),
             "p2p_over_h2d": statistics.median(p2p) / statistics.median(h2d)}
+
+
+def measure_pool(devices, kind, clients_per_gpu=4, per_gpu=150, policy="affinity:4"):
+    """ONE ``KaasService`` over every GPU in ``devices``:
+    the router, the per-GPU worker threads and the GIL are all in the
+    measured path -- unlike the headline's one-process-per-GPU sharding.
+    ``kind`` = jacobi (N=4096, 500 sweeps) or cgemm1024; 2 systems per GPU
+    (distinct const A, b / A, B), requests cycle over them, affinity routing
+    keeps each system's requests where it is cached.  One warm-up pass,
+    then a timed pass: total and per-GPU req/s, p50/p99 wall latency, and the
+    process CPU time per request (host work, GIL included)."""
+    from paper_2212_08146_b200 import workloads as W
+    from paper_2212_08146_b200.benchlib import run_stream
+    from paper_2212_08146_b200.hoststore import PinnedStore
+    from paper_2212_08146_b200.pool import KaasService
+    store = PinnedStore()
+    ng = len(devices)
+    systems = 2 * ng
+    n = JACOBI_N if kind == "jacobi" else 1024
+    for i in range(systems):
+        if kind == "jacobi":
+            W.seed_jacobi(store, n, prefix=f"pj{i}", seed=40 + i)
+        else:
+            W.seed_cgemm(store, n, prefix=f"pc{i}", seed=40 + i)
+
+    def req(i):
+        j = i % systems
+        if kind == "jacobi":
+            return W.jacobi_request(f"t{j}/pool{i}", n, JACOBI_SWEEPS, f"pj{j}/A/{n}", f"pj{j}/b/{n}",
+                                    f"pj{j}/x0/{n}", f"pj/x{j}", f"pj/r{j}")
+        return W.cgemm_request(f"t{j}/pool{i}", n, f"pc{j}/A/{n}", f"pc{j}/B/{n}", f"pc/C{j}")
+    count = per_gpu * ng
+    reqs = [req(i) for i in range(count)]
+    with KaasService(store, capacity=2 << 30, policy=policy, devices=list(devices)) as svc:
+        run_stream(svc, reqs[: max(4 * systems, count // 4)], clients_per_gpu * ng)  # warm: fills, pools
+        served0 = [e.dev_stats.requests for e in svc.executors]
+        cpu0, t0 = time.process_time(), time.perf_counter()
+        resps, lat = run_stream(svc, reqs, clients_per_gpu * ng)
+        wall = time.perf_counter() - t0
+        cpu = time.process_time() - cpu0
+        per = [e.dev_stats.requests - s0 for e, s0 in zip(svc.executors, served0)]
+        p2p = sum(e.dev_stats.p2p_bytes for e in svc.executors)
+    errors = sum(0 if r.status.ok else 1 for r in resps)
+    return {"workload": f"{kind} requests through ONE KaasService over {ng} GPU(s): "
+                        f"{clients_per_gpu * ng} client threads, {systems} const systems, {policy}",
+            "gpus": ng, "requests": count, "errors": errors,
+            "req_per_s": count / wall, "req_per_s_per_gpu": count / wall / ng,
+            "requests_per_gpu": per, "p50_ms": percentile(lat, 0.5) * 1e3,
+            "p99_ms": percentile(lat, 0.99) * 1e3,
+            "host_cpu_us_per_request": cpu / count * 1e6,
+            "host_cpu_cores_busy": cpu / wall, "p2p_fill_bytes": p2p}
+
+
+def cgemm_cpu_baseline(n, seconds=10.0):
+    """The reference CPU executor path for a cGEMM kaasReq (oracle executor,
+    numpy complex BLAS), timed on this box's host cores: warm requests (A, B
+    cached), bounded to ``seconds`` (at least one)."""
+    try:
+        from threadpoolctl import threadpool_limits
+        ctx = threadpool_limits(limits=len(os.sched_getaffinity(0)), user_api="blas")
+    except ImportError:
+        import contextlib
+        ctx = contextlib.nullcontext()
+    from oracle.executor import DictStore, OracleExecutor
+    from paper_2212_08146_b200 import workloads as W
+    with ctx:
+        store = DictStore()
+        W.seed_cgemm(store, n, prefix="cc")
+        ex = OracleExecutor(8 * (8 * n * n), store)
+        req = lambda i: W.cgemm_request(f"cc/{i}", n, f"cc/A/{n}", f"cc/B/{n}", "cc/C")  # noqa: E731
+        ex.execute(req(0))  # cold fetch, untimed
+        lat, t0 = [], time.perf_counter()
+        while not lat or (time.perf_counter() - t0 < seconds and len(lat) < 50):
+            t = time.perf_counter()
+            assert ex.execute(req(len(lat) + 1)).status.ok
+            lat.append(time.perf_counter() - t)
+        threads, _ = cpu_threads()
+    return {"value": len(lat) / sum(lat), "unit": "req/s", "cores": threads, "kind": "port",
+            "sample": f"{len(lat)} warm cgemm {n}^3 kaasReqs through the CPU oracle executor "
+                      f"(numpy complex BLAS, BLAS threads={threads})",
+            "p50_ms": percentile(lat, 0.5) * 1e3}
 
 
 def measure_resnet(device, steps=5):
@@ -420,6 +506,15 @@ def ours(args, rank, world, local_rank, dist):
     alg_bytes = 4 * n * n + 12 * n + 4
     achieved = alg_bytes / sweep_s / 1e9
     svc.close()
+    # what actually binds a sweep: A lives on chip, so not HBM.  FP32 FMA
+    # issue (n^2 FMAs per sweep over 148 SMs x 128 lanes at the measured SM
+    # clock) and the SM-to-SM exchange of x (its measured floor for this
+    # pattern, tools/xchg.cu: profiles/r01/probes/xchg.txt) are serial
+    # within a sweep
+    sm_mhz = clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
+    sms = native.device_info(local_rank).sm_count
+    fma_floor_s = n * n / (sms * 128 * sm_mhz * 1e6)
+    xchg_floor_s = XCHG_FLOOR_US * 1e-6
 
     result = None
     if rank == 0:
@@ -445,10 +540,18 @@ def ours(args, rank, world, local_rank, dist):
             extra("mixed", measure_mixed, local_rank,
                   devices=[(local_rank + i) % nvis for i in range(min(world, nvis))])
             extra("resnet50_chain", measure_resnet, local_rank)
+            pool_devs = [(local_rank + i) % nvis for i in range(min(world, nvis))]
+            extra("pool_jacobi", measure_pool, pool_devs, "jacobi")
+            extra("pool_cgemm1024", measure_pool, pool_devs, "cgemm")
             for key in ("cgemm1024", "cgemm8192"):
                 e = extras[key]
                 if "error" in e:
                     continue
+                try:
+                    e["cpu_baseline"] = cgemm_cpu_baseline(1024 if key == "cgemm1024" else 8192,
+                                                           seconds=5.0)
+                except Exception as exc:  # noqa: BLE001
+                    e["cpu_baseline"] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
                 e["roofline"] = {
                     "bound": "tensor", "unit": "TFLOP/s",
                     "achieved": e["tf32_issued_tflops"],
@@ -512,6 +615,18 @@ def ours(args, rank, world, local_rank, dist):
                         "tools/pingpong.cu) plus ~1 us of on-chip arithmetic",
                 "l2_peak_measured_gbs": L2_PEAK_GBS,
                 "frac_of_l2": achieved / L2_PEAK_GBS,
+                "binding": {
+                    "resource": "fp32 FMA issue + SM-to-SM exchange of x (serial per sweep); "
+                                "HBM does not bind (A is read once per request)",
+                    "fma_per_sweep": n * n, "sm_mhz": sm_mhz,
+                    "fma_floor_us": fma_floor_s * 1e6,
+                    "fma_frac": fma_floor_s / sweep_s,
+                    "exchange_floor_us": XCHG_FLOOR_US,
+                    "exchange_floor_source": "tools/xchg.cu all-to-all tagged exchange alone, "
+                                             "148 CTAs (profiles/r01/probes/xchg.txt)",
+                    "critical_path_floor_us": (fma_floor_s + xchg_floor_s) * 1e6,
+                    "frac": (fma_floor_s + xchg_floor_s) / sweep_s,
+                },
             },
             "cpu_baseline": cpu,
             "gpu_launches": launches,

@@ -9,21 +9,28 @@
 // so A needs no de-interleave and C is written interleaved directly.
 //
 // 3xTF32 split for FP32 accuracy: x = hi + lo, hi = rna_tf32(x), lo = x - hi
-// (exact).  C = A_hi.B_lo + A_lo.B_hi + A_hi.B_hi, small terms first, all in
-// one FP32 accumulator in TMEM.  (1xTF32 measures 2.9e-4 rel. Frobenius on
-// 1024^3 -- over the 1e-4 budget; 3xTF32 measures ~1e-7.)
+// (exact).  C = A_hi.B_lo + A_lo.B_hi + A_hi.B_hi, small terms first.  (1xTF32
+// measures 2.9e-4 rel. Frobenius on 1024^3 -- over the 1e-4 budget.)  The
+// tensor core's accumulation is not round-to-nearest, so K is accumulated in
+// chunks of 512: each chunk in a fresh TMEM accumulator, the chunks summed in
+// FP32 round-to-nearest by the epilogue in fixed order (error flat in K).
 //
 // Pipeline per launch:
 //   1. prep kernels (HBM-bound): A -> [A_hi; A_lo] (K-major, K padded to 32)
-//      and B -> [Bt_hi; Bt_lo] = B_exp^T (K-major), built with an smem transpose.
+//      and B -> [Bt_hi; Bt_lo] = B_exp^T (K-major), built with an smem
+//      transpose; skipped when the executor has them cached for a const input.
 //   2. persistent warp-specialised GEMM, one CTA per SM:
-//        warp 0  TMA producer (cp.async.bulk.tensor, SWIZZLE_128B, 4-stage ring)
+//        warp 0  TMA producer (cp.async.bulk.tensor, SWIZZLE_64B, all four
+//                operand tiles per stage)
 //        warp 1  TMEM allocator + single-thread tcgen05.mma issuer (kind::tf32,
-//                M=128, N=BN, K=8), commits release smem stages / publish tiles
-//        warps 2-5 epilogue: tcgen05.ld 32x32b -> registers -> st.global (C is
-//                interleaved complex, row-major), coverage-masked
-//      TMEM holds two BN-column accumulators so the epilogue of tile t
-//      overlaps the main loop of tile t+1.
+//                M=128, N=BN, K=8), three products per k-step; commits release
+//                smem stages and publish finished K chunks
+//        warps 2-9 epilogue: tcgen05.ld 32x32b -> FP32 running sums in
+//                registers -> st.global (C interleaved complex, row-major),
+//                coverage-masked
+//      TMEM holds two BN-column accumulators that alternate per K chunk, so
+//      draining chunk c overlaps the MMAs of chunk c+1 (and a tile's write-out
+//      overlaps the next tile's first chunk).
 #include <cuda.h>
 
 #include <atomic>

@@ -36,6 +36,7 @@ def test_our_arm_line(cuda):
     assert BASE_KEYS <= set(d) and d["value"] > 0 and d["higher_is_better"] is True
     r = d["roofline"]
     assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= set(r) and r["frac"] > 0
+    assert 0 < r["binding"]["frac"] <= 1.0 and r["binding"]["fma_floor_us"] > 0
     assert {"value", "unit", "cores", "kind", "sample"} <= set(d["cpu_baseline"])
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] >= d["steps"]

@@ -282,15 +282,16 @@ def test_resnet_chain_bit_exact(gpu, depth):
     K up to 4608, run the small-tile configs)."""
     ex, store = gpu
     layers = W.resnet50_gemms()[:depth]
-    W.seed_resnet(store, prefix="rn", layers=layers)
+    pfx = f"rn{depth}"  # fresh keys: both executors start cold
+    W.seed_resnet(store, prefix=pfx, layers=layers)
     ostore = DictStore()
-    W.seed_resnet(ostore, prefix="rn", layers=layers)
-    req = W.resnet_chain_request("rn", prefix="rn", layers=layers, out_key="rn/out")
+    W.seed_resnet(ostore, prefix=pfx, layers=layers)
+    req = W.resnet_chain_request("rn", prefix=pfx, layers=layers, out_key=f"{pfx}/out")
     r = _run(ex, req)
     o = OracleExecutor(1 << 30, ostore).execute(req)
     assert o.status.ok and r.per_invocation == o.per_invocation
     assert r.simulated_total_time == o.simulated_total_time
-    assert canon(store.get("rn/out")) == canon(ostore.get("rn/out"))
+    assert canon(store.get(f"{pfx}/out")) == canon(ostore.get(f"{pfx}/out"))
 
 
 @pytest.mark.parametrize("n", [2048, 4096])
