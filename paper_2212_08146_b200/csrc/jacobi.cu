@@ -28,6 +28,7 @@
 #include <cooperative_groups.h>
 
 #include <atomic>
+#include <cstdio>
 #include <cstdlib>
 
 #include "kaas_internal.cuh"
@@ -234,6 +235,7 @@ k_jacobi_sweep(int n, int cov, const float *__restrict__ A, const float *__restr
 // ---- persistent multi-sweep kernel ----------------------------------------
 
 constexpr int kChainMaxPtrs = 16;
+constexpr int kTraceStamps = 5;  // dev trace: per sweep and CTA (tools/jtrace.py)
 constexpr int kChainMaxSweeps = 2048;
 
 struct ChainParams {
@@ -665,8 +667,8 @@ k_jacobi_cols(const __grid_constant__ ChainParams p, float *partials, unsigned *
                     : zero4();
     }
     const bool tr = p.trace != nullptr && s >= 100 && s < 132 && threadIdx.x == 0;
-    unsigned *trp = tr ? p.trace + ((s - 100) * 148 + (blockIdx.x < 148 ? blockIdx.x : 147)) * 3 : nullptr;
-    if (tr) trp[0] = gtimer_lo();  // warp 0's x has arrived
+    unsigned *trp = tr ? p.trace + ((s - 100) * 148 + (blockIdx.x < 148 ? blockIdx.x : 147)) * kTraceStamps : nullptr;
+    if (tr) trp[1] = gtimer_lo();  // warp 0's x has arrived
     auto dot = [&](const float4 (&a)[kColC4]) {
       float acc = 0.f;
 #pragma unroll
@@ -756,7 +758,7 @@ k_jacobi_cols(const __grid_constant__ ChainParams p, float *partials, unsigned *
       mine = lane < 16 ? mine : other;
     }
     red[warp][lane] = mine;  // slot "lane"
-    if (tr) trp[1] = gtimer_lo();  // warp 0's compute done
+    if (tr) trp[3] = gtimer_lo();  // warp 0's compute done
     __syncthreads();
     float *slot = partials + (s & 1) * kMaxJacobiBlocks;
     if (warp == 0) {
@@ -781,7 +783,7 @@ k_jacobi_cols(const __grid_constant__ ChainParams p, float *partials, unsigned *
         if (lane == 0) slot[blockIdx.x] = res;
       }
     }
-    if (tr) trp[2] = gtimer_lo();  // rows published
+    if (tr) trp[4] = gtimer_lo();  // rows published
     if (want_resid || !p.tagged) {
       grid_sync_mono(sync + 3, epoch++);  // also orders red[] reuse
       if (want_resid && blockIdx.x == 0 && threadIdx.x < 32)
@@ -805,15 +807,15 @@ k_jacobi_cols(const __grid_constant__ ChainParams p, float *partials, unsigned *
 // the 128 B/clk LDS path, and the two overlap, so a sweep's 458 KB per SM
 // costs ~1,000 cycles instead of the L2 tier's ~2 us.  Nothing is re-read
 // from L2 or HBM after the fill.
-constexpr int kTmRT = 16;   // TMEM rows
-constexpr int kTmRR = 6;    // register rows
-constexpr int kTmRS = 6;    // shared-memory rows
-static_assert(kTmRT + kTmRR + kTmRS == kColRows, "row tiers must cover the band");
-constexpr int kTmBatch = 1;  // TMEM rows per tcgen05.ld batch
-constexpr int kTmDep = 4;    // batches in flight (each waits on the dots kTmDep batches back)
+constexpr int kTmRT = 16;   // TMEM rows; the other 12 rows: RR in registers, 12 - RR in smem
+constexpr int kTmOther = kColRows - kTmRT;
 // padded so no other 1-CTA/SM kernel that allocates TMEM can be co-resident
-constexpr size_t kTmTier = (size_t)kTmRS * kColC4 * kColT * sizeof(float4);
-constexpr size_t kTmSmem = kTmTier > 116 * 1024 ? kTmTier : 116 * 1024;
+template <int RS>
+constexpr size_t tm_smem() {
+  return (size_t)RS * kColC4 * kColT * sizeof(float4) > 116 * 1024
+             ? (size_t)RS * kColC4 * kColT * sizeof(float4)
+             : 116 * 1024;
+}
 
 #define KAAS_TMEM_LD16(taddr, v)                                                               \
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 "                                      \
@@ -863,8 +865,15 @@ __device__ __forceinline__ float sum2(unsigned long long v) {
   return lo + hi;
 }
 
+// RR register rows, kTmOther - RR shared-memory rows.  MODE 0: the register
+// and smem rows first, then the TMEM rows (DEP tcgen05.ld in flight).  MODE 1:
+// interleaved -- step i loads TMEM row i while it computes register/smem row
+// i, so the TMEM stream (425 B/clk) and the LDS stream (128 B/clk) overlap.
+template <int RR, int MODE, int DEP>
 __global__ void __launch_bounds__(kColT, 1)
 k_jacobi_tmem(const __grid_constant__ ChainParams p, float *partials, unsigned *sync) {
+  constexpr int kTmRR = RR, kTmRS = kTmOther - RR, kTmDep = DEP, kTmBatch = 1;
+  static_assert(kTmRS >= 0 && kTmRR + kTmRS <= 16, "one 16-slot reduction set for the non-TMEM rows");
   extern __shared__ __align__(16) float4 acache[];  // [kTmRS][kColC4][kColT]
   __shared__ float red[kColW][32];
   __shared__ uint32_t tmem_base;
@@ -953,6 +962,11 @@ k_jacobi_tmem(const __grid_constant__ ChainParams p, float *partials, unsigned *
     float *x_out = p.ptrs[p.idx[s][1]];
     const bool want_resid = (p.idx[s][2] & 0x80) != 0;
     const bool from_tags = p.tagged && s > 0;
+#ifdef KAAS_DEV
+    const bool tr = p.trace != nullptr && s >= 100 && s < 132 && threadIdx.x == 0;
+    unsigned *trp = tr ? p.trace + ((s - 100) * 148 + (blockIdx.x < 148 ? blockIdx.x : 147)) * kTraceStamps : nullptr;
+    if (tr) trp[0] = gtimer_lo();  // warp 0 starts waiting for x
+#endif
     float4 xr[kColC4];
     if (!from_tags) {
 #pragma unroll
@@ -996,9 +1010,9 @@ k_jacobi_tmem(const __grid_constant__ ChainParams p, float *partials, unsigned *
                                   __uint_as_float((unsigned)q[u].w[2]), __uint_as_float((unsigned)q[u].w[3]))
                     : zero4();
     }
-    const bool tr = p.trace != nullptr && s >= 100 && s < 132 && threadIdx.x == 0;
-    unsigned *trp = tr ? p.trace + ((s - 100) * 148 + (blockIdx.x < 148 ? blockIdx.x : 147)) * 3 : nullptr;
-    if (tr) trp[0] = gtimer_lo();
+#ifdef KAAS_DEV
+    if (tr) trp[1] = gtimer_lo();  // x arrived
+#endif
     // packed FP32 (FFMA2, fma.rn.f32x2): even and odd columns accumulate in
     // the two halves of one 64-bit register pair, added at the end -- half
     // the FMA issue slots (2.43 -> 2.33 us/sweep); the order is fixed, so
@@ -1011,6 +1025,27 @@ k_jacobi_tmem(const __grid_constant__ ChainParams p, float *partials, unsigned *
         acc = ffma2(pack2(a[u].z, a[u].w), pack2(xr[u].z, xr[u].w), acc);
       }
       return sum2(acc);
+    };
+    // MODE 2: two independent FFMA2 chains per row (chunks 0-1 and 2-3),
+    // half the dependent-FMA latency per row at one extra add
+    auto dot2 = [&](const float4 (&a)[kColC4]) {
+      unsigned long long c0 = 0ull, c1 = 0ull;
+#pragma unroll
+      for (int u = 0; u < kColC4; u += 2) {
+        c0 = ffma2(pack2(a[u].x, a[u].y), pack2(xr[u].x, xr[u].y), c0);
+        c1 = ffma2(pack2(a[u + 1].x, a[u + 1].y), pack2(xr[u + 1].x, xr[u + 1].y), c1);
+        c0 = ffma2(pack2(a[u].z, a[u].w), pack2(xr[u].z, xr[u].w), c0);
+        c1 = ffma2(pack2(a[u + 1].z, a[u + 1].w), pack2(xr[u + 1].z, xr[u + 1].w), c1);
+      }
+      return sum2(c0) + sum2(c1);
+    };
+    auto dot2_t = [&](const uint32_t (&t)[16]) {
+      float4 a[kColC4];
+#pragma unroll
+      for (int u = 0; u < kColC4; ++u)
+        a[u] = make_float4(__uint_as_float(t[4 * u]), __uint_as_float(t[4 * u + 1]),
+                           __uint_as_float(t[4 * u + 2]), __uint_as_float(t[4 * u + 3]));
+      return dot2(a);
     };
     auto dot_t = [&](const uint32_t (&t)[16]) {
       unsigned long long acc = 0ull;
@@ -1036,46 +1071,80 @@ k_jacobi_tmem(const __grid_constant__ ChainParams p, float *partials, unsigned *
       }
       return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 16);
     };
-    // set 1 = register rows, smem rows, 4 empty (reduced first, so only one
-    // set of partials is live while TMEM rows stream in); set 0 = TMEM rows
-    float m1;
-    {
-      float w[16];
+    float m0, m1;
+    if (MODE == 0) {
+      // set 1 = register rows, smem rows, 4 empty (reduced first, so only one
+      // set of partials is live while TMEM rows stream in); set 0 = TMEM rows
+      {
+        float w[16];
 #pragma unroll
-      for (int r = 0; r < kTmRR; ++r) w[r] = dot(areg[r]);
+        for (int r = 0; r < kTmRR; ++r) w[r] = dot(areg[r]);
 #pragma unroll
-      for (int r = 0; r < kTmRS; ++r) {
-        float4 a[kColC4];
+        for (int r = 0; r < kTmRS; ++r) {
+          float4 a[kColC4];
 #pragma unroll
-        for (int u = 0; u < kColC4; ++u) a[u] = lds4(&acache[(r * kColC4 + u) * kColT + tid]);
-        w[kTmRR + r] = dot(a);
+          for (int u = 0; u < kColC4; ++u) a[u] = lds4(&acache[(r * kColC4 + u) * kColT + tid]);
+          w[kTmRR + r] = dot(a);
+        }
+#pragma unroll
+        for (int k = kTmRR + kTmRS; k < 16; ++k) w[k] = 0.f;
+        m1 = reduce16(w);
       }
+#ifdef KAAS_DEV
+      if (tr) trp[2] = gtimer_lo();  // register + shared-memory rows done
+#endif
+      {
+        float v[16];
 #pragma unroll
-      for (int k = kTmRR + kTmRS; k < 16; ++k) w[k] = 0.f;
-      m1 = reduce16(w);
-    }
-    float m0;
-    {
-      float v[16];
+        for (int bt = 0; bt < kTmRT / kTmBatch; ++bt) {
+          uint32_t t[kTmBatch][16];
+          // the batch's address depends (by an opaque 0) on the previous batch's
+          // dots, so ptxas cannot hoist every tcgen05.ld of the sweep to the
+          // top and hold all 256 values in registers at once
+          const uint32_t dep =
+              bt < kTmDep ? 0u : (__float_as_uint(v[(bt - kTmDep + 1) * kTmBatch - 1]) & p.zero);
 #pragma unroll
-      for (int bt = 0; bt < kTmRT / kTmBatch; ++bt) {
-        uint32_t t[kTmBatch][16];
-        // the batch's address depends (by an opaque 0) on the previous batch's
-        // dots, so ptxas cannot hoist every tcgen05.ld of the sweep to the
-        // top and hold all 256 values in registers at once
-        const uint32_t dep =
-            bt < kTmDep ? 0u : (__float_as_uint(v[(bt - kTmDep + 1) * kTmBatch - 1]) & p.zero);
+          for (int j = 0; j < kTmBatch; ++j) KAAS_TMEM_LD16(taddr + dep + 16u * (bt * kTmBatch + j), t[j]);
+          tmem_wait_ld();
 #pragma unroll
-        for (int j = 0; j < kTmBatch; ++j) KAAS_TMEM_LD16(taddr + dep + 16u * (bt * kTmBatch + j), t[j]);
+          for (int j = 0; j < kTmBatch; ++j) v[bt * kTmBatch + j] = dot_t(t[j]);
+        }
+        m0 = reduce16(v);
+      }
+    } else {
+      // interleaved: TMEM row i is in flight while register / smem row i is
+      // computed (its LDS issued after the tcgen05.ld, before the wait)
+      float v[16], w[16];
+#pragma unroll
+      for (int i = 0; i < kTmRT; ++i) {
+        uint32_t t[16];
+        const uint32_t dep = i < kTmDep ? 0u : (__float_as_uint(v[i - kTmDep]) & p.zero);
+        KAAS_TMEM_LD16(taddr + dep + 16u * i, t);
+        if (i < kTmRR) {
+          w[i] = MODE == 2 ? dot2(areg[i < kTmRR ? i : 0]) : dot(areg[i < kTmRR ? i : 0]);
+        } else if (i < kTmRR + kTmRS) {
+          const int r = i - kTmRR;
+          float4 a[kColC4];
+#pragma unroll
+          for (int u = 0; u < kColC4; ++u) a[u] = lds4(&acache[(r * kColC4 + u) * kColT + tid]);
+          w[i] = MODE == 2 ? dot2(a) : dot(a);
+        } else {
+          w[i] = 0.f;
+        }
         tmem_wait_ld();
-#pragma unroll
-        for (int j = 0; j < kTmBatch; ++j) v[bt * kTmBatch + j] = dot_t(t[j]);
+        v[i] = MODE == 2 ? dot2_t(t) : dot_t(t);
       }
+#ifdef KAAS_DEV
+      if (tr) trp[2] = gtimer_lo();  // all rows' partial dots done
+#endif
+      m1 = reduce16(w);
       m0 = reduce16(v);
     }
     const float mine = lane < 16 ? m0 : m1;
     red[warp][lane] = mine;
-    if (tr) trp[1] = gtimer_lo();
+#ifdef KAAS_DEV
+    if (tr) trp[3] = gtimer_lo();  // TMEM rows + reductions done
+#endif
     __syncthreads();
     float *slot = partials + (s & 1) * kMaxJacobiBlocks;
     if (warp == 0) {
@@ -1099,7 +1168,9 @@ k_jacobi_tmem(const __grid_constant__ ChainParams p, float *partials, unsigned *
         if (lane == 0) slot[blockIdx.x] = res;
       }
     }
-    if (tr) trp[2] = gtimer_lo();
+#ifdef KAAS_DEV
+    if (tr) trp[4] = gtimer_lo();  // published
+#endif
     if (want_resid || !p.tagged) {
       grid_sync_mono(sync + 3, epoch++);
       if (want_resid && blockIdx.x == 0 && threadIdx.x < 32)
@@ -1127,6 +1198,32 @@ bool use_cols_kernel(int dev, int n, uint64_t cov, int blocks) {
   return n % 4 == 0 && n >= 2048 && n <= kColW * 32 * kColC4 * 4 &&
          (cov + blocks - 1) / blocks <= (uint64_t)kColRows &&
          device_props(dev).max_smem_optin >= (int)(kColSmem + sizeof(float) * kColW * 32);
+}
+
+// TMEM-tier kernel variant: the product default, or (dev builds)
+// KAAS_JACOBI_TMV="RR,MODE,DEP" for A/B runs (tools/jacobi_var.sh)
+struct TmVariant {
+  int rr, mode, dep;
+  const void *fn;
+  size_t smem;
+};
+#define KAAS_TMV(RR, MODE, DEP) \
+  TmVariant { RR, MODE, DEP, (const void *)k_jacobi_tmem<RR, MODE, DEP>, tm_smem<kTmOther - RR>() }
+constexpr int kTmDefRR = 6, kTmDefMode = 1, kTmDefDep = 4;
+const TmVariant &tm_variant() {
+  static const TmVariant def = KAAS_TMV(kTmDefRR, kTmDefMode, kTmDefDep);
+#ifdef KAAS_DEV
+  static const TmVariant vars[] = {KAAS_TMV(6, 0, 4), KAAS_TMV(6, 1, 2), KAAS_TMV(6, 1, 3),
+                                   KAAS_TMV(6, 2, 3), KAAS_TMV(6, 2, 4), KAAS_TMV(6, 2, 5),
+                                   KAAS_TMV(7, 2, 4), KAAS_TMV(8, 2, 4)};
+  if (const char *e = KAAS_DEV_ENV("KAAS_JACOBI_TMV")) {
+    int rr = 0, mode = 0, dep = 0;
+    if (sscanf(e, "%d,%d,%d", &rr, &mode, &dep) == 3)
+      for (const TmVariant &v : vars)
+        if (v.rr == rr && v.mode == mode && v.dep == dep) return v;
+  }
+#endif
+  return def;
 }
 
 // the band in TMEM + registers + smem (default); KAAS_JACOBI_TMEM=0 = L2 tier
@@ -1337,16 +1434,20 @@ int launch_jacobi_chain(cudaStream_t s, int dev, const JacobiChain &c, StreamScr
         if (KAAS_DEV_ENV("KAAS_JACOBI_NOWAIT")) p.tagged = 3;  // dev: compute-only timing
 #endif
         static unsigned *trace_buf = nullptr;  // dev: KAAS_JACOBI_TRACE=1 (tools/jtrace.py)
-        if (KAAS_DEV_ENV("KAAS_JACOBI_TRACE") && !trace_buf) cudaMalloc((void **)&trace_buf, 32 * 148 * 3 * 4);
+        if (KAAS_DEV_ENV("KAAS_JACOBI_TRACE") && !trace_buf) cudaMalloc((void **)&trace_buf, 32 * 148 * kTraceStamps * 4);
         p.trace = KAAS_DEV_ENV("KAAS_JACOBI_TRACE") ? trace_buf : nullptr;
         jacobi_trace_buffer() = p.trace;
         const char *pe = KAAS_DEV_ENV("KAAS_JACOBI_POLL_NS");  // dev A/B
         p.poll_ns = pe ? atoi(pe) : 0;
       }
       const bool tm = use_tmem_kernel();
-      const void *cfn = tm ? (const void *)k_jacobi_tmem : (const void *)k_jacobi_cols;
-      const size_t csmem = tm ? kTmSmem : kColSmem;
+      const TmVariant &tv = tm_variant();
+      const void *cfn = tm ? tv.fn : (const void *)k_jacobi_cols;
+      const size_t csmem = tm ? tv.smem : kColSmem;
       static std::atomic<uint64_t> attr_done[2];  // per kernel, bit per device (dev < 64)
+#ifdef KAAS_DEV
+      KAAS_CUDA(cudaFuncSetAttribute(cfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
+#endif
       if (!(attr_done[tm].load(std::memory_order_relaxed) >> (dev & 63) & 1)) {
         KAAS_CUDA(cudaFuncSetAttribute(cfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
         attr_done[tm].fetch_or(1ull << (dev & 63));
@@ -1393,7 +1494,7 @@ int launch_jacobi_chain(cudaStream_t s, int dev, const JacobiChain &c, StreamScr
 extern "C" int kaas_dev_jacobi_trace(void *host, unsigned long bytes) {
   unsigned *buf = kaas::jacobi_trace_buffer();
   if (!buf) return 1;
-  if (bytes > 32ul * 148 * 3 * 4) bytes = 32ul * 148 * 3 * 4;
+  if (bytes > 32ul * 148 * kaas::kTraceStamps * 4) bytes = 32ul * 148 * kaas::kTraceStamps * 4;
   return cudaMemcpy(host, buf, bytes, cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 2;
 }
 #endif

@@ -3,10 +3,10 @@
     make -C paper_2212_08146_b200/csrc dev   # the trace exists only in the dev build
     python tools/jtrace.py [n]
 
-Stamps (globaltimer, ns): t0 = CTA's warp 0 has its x, t1 = warp 0's row
-partials done, t2 = the CTA's rows published.  Prints the per-sweep spread
-of each phase across CTAs and the critical path from publish to the next
-sweep's x arrival.
+Stamps (globaltimer, ns), warp 0 of each CTA: poll start, x arrived,
+register + shared-memory rows done, TMEM rows + reductions done, rows
+published.  Prints per-phase medians and the critical path from the last
+publish to the next sweep's x arrival.
 """
 
 import ctypes as C
@@ -25,18 +25,25 @@ import kbench  # noqa: E402
 
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 4096
 kbench.jacobi(n, 500, 1)
-buf = (C.c_uint * (32 * 148 * 3))()
+buf = (C.c_uint * (32 * 148 * 5))()
 rc = native.load().kaas_dev_jacobi_trace(buf, C.sizeof(buf))
 assert rc == 0, rc
-t = np.frombuffer(buf, dtype=np.uint32).astype(np.int64).reshape(32, 148, 3)
-t -= t[0, :, 0].min()
+t = np.frombuffer(buf, dtype=np.uint32).astype(np.int64).reshape(32, 148, 5)
+t -= t[0, :, 1].min()
 t %= 1 << 32
-for s in range(0, 31, 6):
-    a, b, c = t[s, :, 0], t[s, :, 1], t[s, :, 2]
-    nxt = t[s + 1, :, 0]
-    print(f"sweep {100 + s}: x-arrival spread {a.max() - a.min():5d} ns | compute (t1-t0) "
-          f"p50 {np.median(b - a):5.0f} max {np.max(b - a):5d} | tail (t2-t1) p50 {np.median(c - b):5.0f} "
-          f"max {np.max(c - b):5d} | last publish -> next arrival p50 {np.median(nxt - c.max()):5.0f} "
-          f"| sweep period {np.median(nxt - a):5.0f}")
-per = (t[31, :, 0] - t[0, :, 0]) / 31
+# stamps (warp 0 of each CTA): 0 poll start, 1 x arrived, 2 register+smem rows
+# done, 3 TMEM rows + reductions done, 4 published
+rows = []
+for s in range(0, 31):
+    p0, xa, mid, cd, pub = (t[s, :, i] for i in range(5))
+    nxt = t[s + 1, :, 1]
+    rows.append((np.median(xa - p0), np.median(mid - xa), np.median(cd - mid), np.median(pub - cd),
+                 np.median(nxt - pub.max()), pub.max() - pub.min(), xa.max() - xa.min(),
+                 np.median(nxt - xa)))
+r = np.array(rows)
+names = ["wait for x (poll)", "reg+smem rows", "TMEM rows+reduce", "CTA reduce+publish",
+         "last publish->next arrival", "publish spread", "arrival spread", "sweep period"]
+for i, nm in enumerate(names):
+    print(f"{nm:28s} median over sweeps {np.median(r[:, i]):7.0f} ns   (min {r[:, i].min():6.0f}, max {r[:, i].max():6.0f})")
+per = (t[31, :, 1] - t[0, :, 1]) / 31
 print(f"mean sweep period {per.mean():.0f} ns")
