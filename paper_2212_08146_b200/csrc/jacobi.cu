@@ -1187,6 +1187,353 @@ k_jacobi_tmem(const __grid_constant__ ChainParams p, float *partials, unsigned *
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
 }
 
+#ifdef KAAS_DEV
+// ---- split-publish kernel (dev build only: measured slower) -----------------
+//
+// Measured on B200 (round 2): 2.71 us/sweep with the polls in program order,
+// 3.31 us/sweep with them software-pipelined, against 2.19 for k_jacobi_tmem.
+// A poll round on lines other SMs have just written costs ~0.5-0.9 us, the
+// early rows' publish spread across CTAs is ~0.5 us, so the early x of the
+// next sweep is rarely complete when phase C ends and the second reduction
+// and CTA barrier per sweep are not paid back.  Kept as the A/B reference
+// (KAAS_JACOBI_TMV=s in a dev build).
+//
+// Same on-chip band as k_jacobi_tmem, but a sweep no longer needs all of x
+// before any work starts.  Rows i with (i >> 2) even are "early", the others
+// "late"; x's early columns are the even float4 chunks, late columns the odd
+// ones, and every thread owns two early chunks (2t, 2t + 512) and two late
+// chunks (2t + 1, 2t + 513).  Per sweep:
+//   A  all rows x early columns          (needs only the early x of sweep s)
+//   B  early rows x late columns -> reduce -> publish the early rows
+//   C  late rows x late columns  -> reduce -> publish the late rows
+// so phase A of sweep s+1 overlaps the exchange of sweep s's late rows, and
+// the critical path per sweep is exchange + A + B instead of exchange + all
+// of the arithmetic.  Each row's dot product is (early part) + (late part):
+// a fixed order, so results are deterministic.
+//
+// Band storage, 16 early + 16 late slots (a band has 12..16 of each; empty
+// slots are zeros and sit in the shared-memory tier, which is skipped):
+//   early slots 0-7 / late slots 0-7   TMEM (16 columns per thread per slot:
+//                                      8 early-column values, then 8 late)
+//   early 8-10 / late 8-10             registers
+//   early 11-15 / late 11-15           shared memory
+constexpr int kSpT = 8, kSpR = 3, kSpS = 5;  // TMEM / register / smem slots per half
+static_assert(kSpT + kSpR + kSpS == 16, "16 slots per half");
+constexpr size_t kSpSmem = (size_t)2 * kSpS * 4 * kColT * sizeof(float4) > 116 * 1024
+                               ? (size_t)2 * kSpS * 4 * kColT * sizeof(float4)
+                               : 116 * 1024;
+
+#define KAAS_TMEM_LD8(taddr, v)                                                                \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"       \
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),     \
+                 "=r"(v[6]), "=r"(v[7])                                                      \
+               : "r"(taddr))
+
+__global__ void __launch_bounds__(kColT, 1)
+k_jacobi_split(const __grid_constant__ ChainParams p, float *partials, unsigned *sync) {
+  extern __shared__ __align__(16) float4 acache[];  // [2 * kSpS][4][kColT]
+  __shared__ float red[2][kColW][16];
+  __shared__ uint32_t tmem_base;
+  __shared__ signed char slot_row[2][16];  // band-local row of each early / late slot, -1 = empty
+  const int n = p.n, n4 = n >> 2;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  int r0, r1;
+  band(p.cov, r0, r1);
+  const int R = r1 - r0;
+  const uint64_t pol = l2_policy(false);
+  // this thread's chunks: u = 0, 1 early columns, u = 2, 3 late columns
+  const int chunk[4] = {2 * tid, 2 * tid + 512, 2 * tid + 1, 2 * tid + 513};
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&tmem_base)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (lane < 2) {  // slot -> row tables (ascending rows per half)
+      int k = 0;
+      for (int rl = 0; rl < R; ++rl)
+        if ((((r0 + rl) >> 2) & 1) == lane && k < 16) slot_row[lane][k++] = (signed char)rl;
+      for (; k < 16; ++k) slot_row[lane][k] = -1;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t taddr = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(warp >> 2) * 256u;
+
+  // A[r0 + rl][chunk u] with the diagonal zeroed; empty slots / absent columns 0
+  auto lda = [&](int rl, int u) -> float4 {
+    float4 a = zero4();
+    const int c4 = chunk[u];
+    if (rl < 0 || c4 >= n4) return a;
+    a = ld_a(p.A + (size_t)(r0 + rl) * n + 4 * c4, pol);
+    const int i = r0 + rl;
+    if (c4 == (i >> 2)) {
+      const int d = i & 3;
+      a.x = d == 0 ? 0.f : a.x;
+      a.y = d == 1 ? 0.f : a.y;
+      a.z = d == 2 ? 0.f : a.z;
+      a.w = d == 3 ? 0.f : a.w;
+    }
+    return a;
+  };
+#pragma unroll 1
+  for (int t = 0; t < 2 * kSpT; ++t) {  // TMEM slot t: half t / kSpT, slot t % kSpT
+    const int rl = slot_row[t / kSpT][t % kSpT];
+    uint32_t v[16];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float4 a = lda(rl, u);
+      v[4 * u + 0] = __float_as_uint(a.x);
+      v[4 * u + 1] = __float_as_uint(a.y);
+      v[4 * u + 2] = __float_as_uint(a.z);
+      v[4 * u + 3] = __float_as_uint(a.w);
+    }
+    KAAS_TMEM_ST16(taddr + 16u * t, v);
+  }
+  float4 areg[2][kSpR][4];
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int k = 0; k < kSpR; ++k)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) areg[h][k][u] = lda(slot_row[h][kSpT + k], u);
+#pragma unroll 1
+  for (int h = 0; h < 2; ++h)
+#pragma unroll 1
+    for (int k = 0; k < kSpS; ++k)
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        acache[((h * kSpS + k) * 4 + u) * kColT + tid] = lda(slot_row[h][kSpT + kSpR + k], u);
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+
+  // warp 0, lane l < 16: early slot l and late slot l (their rows, b, 1/a_ii)
+  int rowE = -1, rowL = -1;
+  float bE = 0.f, rE = 1.f, bL = 0.f, rL = 1.f;
+  if (warp == 0 && lane < 16) {
+    if (slot_row[0][lane] >= 0) {
+      rowE = r0 + slot_row[0][lane];
+      bE = __ldg(p.b + rowE);
+      rE = 1.0f / __ldg(p.A + (size_t)rowE * n + rowE);
+    }
+    if (slot_row[1][lane] >= 0) {
+      rowL = r0 + slot_row[1][lane];
+      bL = __ldg(p.b + rowL);
+      rL = 1.0f / __ldg(p.A + (size_t)rowL * n + rowL);
+    }
+  }
+
+  // Software-pipelined exchange: the loads that poll for the next sweep's
+  // early x are issued right after this CTA publishes its own early rows
+  // (every CTA publishes them at about that time) and checked after phase C;
+  // the loads for the late x are issued after the late publish and checked
+  // after the next phase A.  A poll round's latency (~0.5 us on lines other
+  // SMs just wrote) is thereby hidden behind phases C and A.
+  auto dot8 = [&](const float4 &a0, const float4 &a1, const float4 &x0, const float4 &x1) {
+    unsigned long long acc = 0ull;
+    acc = ffma2(pack2(a0.x, a0.y), pack2(x0.x, x0.y), acc);
+    acc = ffma2(pack2(a0.z, a0.w), pack2(x0.z, x0.w), acc);
+    acc = ffma2(pack2(a1.x, a1.y), pack2(x1.x, x1.y), acc);
+    acc = ffma2(pack2(a1.z, a1.w), pack2(x1.z, x1.w), acc);
+    return sum2(acc);
+  };
+  auto u2f4 = [](const uint32_t *t) {
+    return make_float4(__uint_as_float(t[0]), __uint_as_float(t[1]), __uint_as_float(t[2]), __uint_as_float(t[3]));
+  };
+  auto reduce16 = [&](float (&v)[16]) {
+#pragma unroll
+    for (int h = 8; h >= 1; h >>= 1) {
+      const bool up = (lane & h) != 0;
+#pragma unroll
+      for (int k = 0; k < h; ++k) {
+        const float send = up ? v[k] : v[k + h];
+        const float keep = up ? v[k + h] : v[k];
+        v[k] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+      }
+    }
+    return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 16);
+  };
+  // slots of half h against the x chunk pair (x0, x1) = chunks u0, u0 + 1,
+  // added into acc[16]; TMEM slot k in flight while register / smem slot k
+  // is computed (straight-line: empty smem slots are zeros, computed anyway)
+  auto half_pass = [&](int h, int u0, const float4 &x0, const float4 &x1, float (&acc)[16]) {
+#pragma unroll
+    for (int k = 0; k < kSpT; ++k) {
+      uint32_t t[8];
+      const uint32_t dep = k < 3 ? 0u : (__float_as_uint(acc[k - 3]) & p.zero);
+      KAAS_TMEM_LD8(taddr + dep + 16u * (h * kSpT + k) + (u0 ? 8u : 0u), t);
+      if (k < kSpR) {
+        acc[kSpT + k] += dot8(areg[h][k][u0], areg[h][k][u0 + 1], x0, x1);
+      } else {
+        const int j = k - kSpR;
+        const float4 a0 = lds4(&acache[((h * kSpS + j) * 4 + u0) * kColT + tid]);
+        const float4 a1 = lds4(&acache[((h * kSpS + j) * 4 + u0 + 1) * kColT + tid]);
+        acc[kSpT + kSpR + j] += dot8(a0, a1, x0, x1);
+      }
+      tmem_wait_ld();
+      acc[k] += dot8(u2f4(t), u2f4(t + 4), x0, x1);
+    }
+  };
+  // tagged-word polls: issue the loads of chunk pair u0 (no wait) / finish
+  // them (re-poll any chunk whose tag is not `want` yet)
+  auto issue = [&](TagWords4 (&q)[2], int u0, const unsigned long long *src) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+      if (chunk[u0 + j] < n4) q[j] = ld_relaxed_u64x4(src + 4 * chunk[u0 + j]);
+  };
+  auto tag_ok = [&](const TagWords4 &q, unsigned want) {
+    return (unsigned)(q.w[0] >> 32) == want && (unsigned)(q.w[1] >> 32) == want &&
+           (unsigned)(q.w[2] >> 32) == want && (unsigned)(q.w[3] >> 32) == want;
+  };
+  auto finish = [&](TagWords4 (&q)[2], int u0, const unsigned long long *src, unsigned want, float4 &x0,
+                    float4 &x1) {
+    unsigned spins = 0;
+#pragma unroll 1
+    for (;;) {
+      bool ok = true;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) ok = ok && (chunk[u0 + j] >= n4 || tag_ok(q[j], want));
+      if (ok) break;
+      if (++spins > (1u << 22)) __trap();  // a lost producer: fail loudly, never hang
+#ifdef KAAS_DEV
+      if (p.tagged == 3) break;
+#endif
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        if (chunk[u0 + j] < n4 && !tag_ok(q[j], want)) q[j] = ld_relaxed_u64x4(src + 4 * chunk[u0 + j]);
+    }
+    float4 *xs[2] = {&x0, &x1};
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+      *xs[j] = chunk[u0 + j] < n4
+                   ? make_float4(__uint_as_float((unsigned)q[j].w[0]), __uint_as_float((unsigned)q[j].w[1]),
+                                 __uint_as_float((unsigned)q[j].w[2]), __uint_as_float((unsigned)q[j].w[3]))
+                   : zero4();
+  };
+  auto plain = [&](const float *x_in, int u) {
+    return chunk[u] < n4 ? __ldcg(reinterpret_cast<const float4 *>(x_in) + chunk[u]) : zero4();
+  };
+
+  float xprevE = 0.f, xprevL = 0.f;
+  unsigned epoch = 0;
+  float4 xe0 = zero4(), xe1 = zero4(), xl0 = zero4(), xl1 = zero4();  // x of the current sweep
+  TagWords4 qe[2], ql[2];  // in-flight polls: next sweep's early / this sweep's late x
+  bool late_inflight = false;
+  for (int s = 0; s < p.sweeps; ++s) {
+    const float *x_in = p.ptrs[p.idx[s][0]];
+    float *x_out = p.ptrs[p.idx[s][1]];
+    const bool want_resid = (p.idx[s][2] & 0x80) != 0;
+    const bool from_tags = p.tagged && s > 0;
+    const unsigned want = p.tag0 + (unsigned)s;
+    const unsigned long long *src = p.xt + (size_t)(s & 1) * kJacTaggedMaxN;
+    unsigned long long *dst = p.xt + (size_t)((s + 1) & 1) * kJacTaggedMaxN;
+    const bool next_tagged = p.tagged && s + 1 < p.sweeps;
+#ifdef KAAS_DEV
+    const bool tr = p.trace != nullptr && s >= 100 && s < 132 && threadIdx.x == 0;
+    unsigned *trp = tr ? p.trace + ((s - 100) * 148 + (blockIdx.x < 148 ? blockIdx.x : 147)) * kTraceStamps : nullptr;
+    if (tr) trp[0] = gtimer_lo();
+#endif
+    if (!from_tags) {  // first sweep, or grid-barrier mode: x_in is complete in memory
+      xe0 = plain(x_in, 0);
+      xe1 = plain(x_in, 1);
+      xl0 = plain(x_in, 2);
+      xl1 = plain(x_in, 3);
+    }
+#ifdef KAAS_DEV
+    if (tr) trp[1] = gtimer_lo();
+#endif
+    float vE[16], vL[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) vE[k] = vL[k] = 0.f;
+    // ---- phase A: every row x the early columns
+    half_pass(0, 0, xe0, xe1, vE);
+    half_pass(1, 0, xe0, xe1, vL);
+    if (from_tags) {
+      if (!late_inflight) issue(ql, 2, src);
+      finish(ql, 2, src, want, xl0, xl1);
+    }
+    late_inflight = false;
+#ifdef KAAS_DEV
+    if (tr) trp[2] = gtimer_lo();
+#endif
+    // ---- phase B: early rows x the late columns, then publish them
+    half_pass(0, 2, xl0, xl1, vE);
+    {
+      const float m = reduce16(vE);
+      if (lane < 16) red[0][warp][lane] = m;
+    }
+    __syncthreads();
+    float res = 0.f;
+    if (warp == 0 && rowE >= 0) {
+      float tot = 0.f;
+#pragma unroll
+      for (int w = 0; w < kColW; ++w) tot += red[0][w][lane];
+      const float xn = (bE - tot) * rE;
+      if (p.tagged) st_relaxed_u64(dst + rowE, tagged_word(xn, want + 1));
+      x_out[rowE] = xn;
+      res = fabsf(xn - (from_tags ? xprevE : __ldcg(x_in + rowE)));
+      xprevE = xn;
+    }
+    // every CTA publishes its early rows about now: poll for them while
+    // phase C runs
+    if (next_tagged) issue(qe, 0, dst);
+    // ---- phase C: late rows x the late columns, then publish them
+    half_pass(1, 2, xl0, xl1, vL);
+    {
+      const float m = reduce16(vL);
+      if (lane < 16) red[1][warp][lane] = m;
+    }
+#ifdef KAAS_DEV
+    if (tr) trp[3] = gtimer_lo();
+#endif
+    __syncthreads();
+    float *slot = partials + (s & 1) * kMaxJacobiBlocks;
+    if (warp == 0) {
+      if (rowL >= 0) {
+        float tot = 0.f;
+#pragma unroll
+        for (int w = 0; w < kColW; ++w) tot += red[1][w][lane];
+        const float xn = (bL - tot) * rL;
+        if (p.tagged) st_relaxed_u64(dst + rowL, tagged_word(xn, want + 1));
+        x_out[rowL] = xn;
+        res += fabsf(xn - (from_tags ? xprevL : __ldcg(x_in + rowL)));
+        xprevL = xn;
+      }
+      if (want_resid) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) res += __shfl_xor_sync(0xffffffffu, res, off);
+        if (lane == 0) slot[blockIdx.x] = res;
+      }
+    }
+    if (want_resid || !p.tagged) {
+      grid_sync_mono(sync + 3, epoch++);
+      if (want_resid && blockIdx.x == 0 && threadIdx.x < 32)
+        finish_resid(slot, gridDim.x, p.ptrs[p.idx[s][2] & 0x7f]);
+    }
+    if (next_tagged) {
+      // late x of the next sweep: every CTA publishes it about now -- in
+      // flight across the next phase A; the next early x: finish its polls
+      issue(ql, 2, dst);
+      late_inflight = true;
+      finish(qe, 0, dst, want + 1, xe0, xe1);
+    }
+#ifdef KAAS_DEV
+    if (tr) trp[4] = gtimer_lo();
+#endif
+  }
+
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+}
+
+#endif  // KAAS_DEV
+
 unsigned *&jacobi_trace_buffer() {
   static unsigned *buf = nullptr;
   return buf;
@@ -1213,6 +1560,9 @@ constexpr int kTmDefRR = 6, kTmDefMode = 1, kTmDefDep = 4;
 const TmVariant &tm_variant() {
   static const TmVariant def = KAAS_TMV(kTmDefRR, kTmDefMode, kTmDefDep);
 #ifdef KAAS_DEV
+  static const TmVariant split = TmVariant{0, 9, 0, (const void *)k_jacobi_split, kSpSmem};
+  if (const char *e = KAAS_DEV_ENV("KAAS_JACOBI_TMV"))
+    if (e[0] == 's') return split;
   static const TmVariant vars[] = {KAAS_TMV(6, 0, 4), KAAS_TMV(6, 1, 2), KAAS_TMV(6, 1, 3),
                                    KAAS_TMV(6, 2, 3), KAAS_TMV(6, 2, 4), KAAS_TMV(6, 2, 5),
                                    KAAS_TMV(7, 2, 4), KAAS_TMV(8, 2, 4)};
