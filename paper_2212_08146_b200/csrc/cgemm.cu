@@ -694,4 +694,12 @@ int launch_cgemm(cudaStream_t s, int dev, int n, int m, int k, uint64_t cov, con
                 : launch_gemm2<256>(s, dev, ma, mbm, shape, C, sc, po);
 }
 
+int encode_map_f32(CUtensorMap *map, const float *base, uint64_t rows, uint64_t ld, uint32_t box_rows,
+                   uint32_t box_k, int swizzle_bytes) {
+  const CUtensorMapSwizzle swz = swizzle_bytes == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                                 : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                       : CU_TENSOR_MAP_SWIZZLE_NONE;
+  return make_map(map, base, rows, ld, box_rows, box_k, swz);
+}
+
 }  // namespace kaas

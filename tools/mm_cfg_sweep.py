@@ -18,13 +18,15 @@ tot_model, tot_best = 0.0, 0.0
 for m, n, k in shapes:
     def run(cfg):
         env = dict(os.environ)
+        env["KAAS_B200_LIB"] = "paper_2212_08146_b200/libkaas_b200_dev.so"
+        env["KAAS_MATMUL_LK"] = "0"
         if cfg is not None:
             env["KAAS_MATMUL_CFG"] = str(cfg)
         out = subprocess.run([sys.executable, "tools/kbench.py", "matmul", str(m), str(n), str(k), "10"],
                              capture_output=True, text=True, env=env).stdout
         return float(out.split(":")[1].split("us")[0])
     model = run(None)
-    times = [run(c) for c in range(10)]
+    times = [run(c) for c in range(14)]
     best = min(times)
     tot_model += model
     tot_best += best
