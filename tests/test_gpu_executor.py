@@ -167,8 +167,9 @@ def test_pipelined_begin_complete_matches_sequential(cuda, depth):
 
 
 def test_peer_fills_preserve_decisions_and_bytes(cuda):
-    """Two executors sharing a PeerDirectory (same GPU: D2D; across GPUs the
-    same path is an NVLink peer copy).  Fills of objects the other executor
+    """Two executors sharing a PeerDirectory: on two GPUs when the box has
+    them (cudaMemcpyPeerAsync over NVLink between pool allocations, peer
+    access granted per pool), else on one (the same path as a D2D copy).  Fills of objects the other executor
     holds at the current store version are device-to-device copies; every
     response, cache state and store byte still equals the reference
     (two oracle executors over one store, same interleaving)."""
@@ -188,7 +189,14 @@ def test_peer_fills_preserve_decisions_and_bytes(cuda):
         reqs[20 * i:20 * i] = [w, r]
     cap = 4 << 20
     peers = PeerDirectory()
-    gexs = [GpuExecutor(ExecutorConfig(capacity=cap, executor_id=e, debug=True), gstore) for e in (0, 1)]
+    from paper_2212_08146_b200 import native
+    ndev = native.device_count()
+    devs = (0, 1 % ndev)  # the second executor on a second GPU when there is one: NVLink P2P
+    if devs[1] != devs[0]:
+        native.init_device(devs[1])
+        assert native.enable_peer(devs[0], devs[1]) and native.enable_peer(devs[1], devs[0])
+    gexs = [GpuExecutor(ExecutorConfig(capacity=cap, executor_id=e, debug=True, device=devs[e]), gstore)
+            for e in (0, 1)]
     for g in gexs:
         g.peers = peers
     oexs = [OracleExecutor(cap, ostore) for _ in (0, 1)]
