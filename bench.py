@@ -380,10 +380,12 @@ def measure_pool(devices, kind, clients_per_gpu=4, per_gpu=150, policy="affinity
     with KaasService(store, capacity=2 << 30, policy=policy, devices=list(devices)) as svc:
         run_stream(svc, reqs[: max(4 * systems, count // 4)], clients_per_gpu * ng)  # warm: fills, pools
         served0 = [e.dev_stats.requests for e in svc.executors]
+        host0 = sum(e.dev_stats.host_ms for e in svc.executors)
         cpu0, t0 = time.process_time(), time.perf_counter()
         resps, lat = run_stream(svc, reqs, clients_per_gpu * ng)
         wall = time.perf_counter() - t0
         cpu = time.process_time() - cpu0
+        host_ms = sum(e.dev_stats.host_ms for e in svc.executors) - host0
         per = [e.dev_stats.requests - s0 for e, s0 in zip(svc.executors, served0)]
         p2p = sum(e.dev_stats.p2p_bytes for e in svc.executors)
     errors = sum(0 if r.status.ok else 1 for r in resps)
@@ -393,8 +395,13 @@ def measure_pool(devices, kind, clients_per_gpu=4, per_gpu=150, policy="affinity
             "req_per_s": count / wall, "req_per_s_per_gpu": count / wall / ng,
             "requests_per_gpu": per, "p50_ms": percentile(lat, 0.5) * 1e3,
             "p99_ms": percentile(lat, 0.99) * 1e3,
-            "host_cpu_us_per_request": cpu / count * 1e6,
-            "host_cpu_cores_busy": cpu / wall, "p2p_fill_bytes": p2p}
+            "host_us_per_request": host_ms / count * 1e3,
+            "host_busy_frac": host_ms / (wall * 1e3),
+            "host_note": "host_us_per_request = executor begin()/complete() time without the waits "
+                         "for the device (decisions, enqueues, puts, responses: the Python work the "
+                         "pool's threads share under the GIL); process_cpu_us_per_request also "
+                         "counts CUDA's spin-waits",
+            "process_cpu_us_per_request": cpu / count * 1e6, "p2p_fill_bytes": p2p}
 
 
 def cgemm_cpu_baseline(n, seconds=10.0):
@@ -488,10 +495,12 @@ def ours(args, rank, world, local_rank, dist):
     sampler.start()
     launches0 = native.launch_counter()
     h2d0, d2h0 = ex.dev_stats.h2d_bytes, ex.dev_stats.d2h_bytes
+    host0 = ex.dev_stats.host_ms
     flusher = L2Flusher(local_rank)
     lat, dev, kern = run_requests(svc, make_req, args.steps, 1000, flusher)
     wall = sum(lat)
     launches = native.launch_counter() - launches0
+    host_us = (ex.dev_stats.host_ms - host0) / args.steps * 1e3
     h2d = (ex.dev_stats.h2d_bytes - h2d0) // args.steps
     d2h = (ex.dev_stats.d2h_bytes - d2h0) // args.steps
     clocks = sampler.stop()
@@ -602,6 +611,7 @@ def ours(args, rank, world, local_rank, dist):
             "e2e": {"value": world * args.steps / wall_max, "unit": "req/s",
                     "p50_ms": percentile(lat, 0.5) * 1e3, "p99_ms": percentile(lat, 0.99) * 1e3,
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                    "host_us_per_request": host_us,
                     "note": "service.submit() per step with pinned host store objects; A,b are "
                             "const cache hits (0 B), x0 re-fetched (16 KiB), x + resid flushed"},
             "roofline": {
@@ -612,13 +622,16 @@ def ours(args, rank, world, local_rank, dist):
                 "kernel": "k_jacobi_tmem (500 sweeps, one cooperative launch; A on chip, x via tagged words)",
                 "unit_bytes": alg_bytes, "sweep_us": sweep_s * 1e6,
                 "note": "A (64 MiB) is read from HBM once per request (L2 flushed between "
-                        "requests; ncu: 67.2 MB DRAM per 500-sweep launch) and then held on "
+                        "requests; ncu: 67.5 MB DRAM per 500-sweep launch) and then held on "
                         "chip for all 500 sweeps: 16 of each SM's 28 rows in tensor memory, "
                         "6 in registers, 6 in shared memory. Achieved = algorithmic bytes / "
-                        "sweep time, so it exceeds the HBM copy peak by design. The sweep is "
-                        "bound by the all-to-all x exchange between the 148 CTAs (exchange "
-                        "alone: 1.5 us/sweep, tools/xchg.cu; one SM->SM hop 366 ns, "
-                        "tools/pingpong.cu) plus ~1 us of on-chip arithmetic",
+                        "sweep time, so it exceeds the HBM copy peak by design: HBM does not "
+                        "bind -- see 'binding'. Per sweep (tools/jtrace.py): ~0.93 us of "
+                        "on-chip arithmetic (TMEM + shared-memory streams interleaved, FFMA2), "
+                        "~0.16 us CTA reduce + publish, ~0.85-0.95 us from the last publish "
+                        "to the next x arrival (one poll round on lines other SMs just wrote: "
+                        "0.47 us mean / 0.63 us slowest CTA even with no waiting, "
+                        "tools/l2home.cu)",
                 "l2_peak_measured_gbs": L2_PEAK_GBS,
                 "frac_of_l2": achieved / L2_PEAK_GBS,
                 "binding": {

@@ -36,6 +36,7 @@ from __future__ import annotations
 
 import itertools
 import threading
+import time
 
 from collections import OrderedDict
 from dataclasses import dataclass, field, replace
@@ -123,9 +124,9 @@ class DeviceStats:
 
     __slots__ = ("requests", "_device_ms", "_last_device_ms", "_kernel_ms", "_last_kernel_ms",
                  "h2d_bytes", "_h2d_ms", "d2h_bytes", "p2p_bytes", "kernel_launches", "_pending",
-                 "_release", "_lock")
+                 "_release", "_lock", "host_ms")
     FIELDS = ("requests", "device_ms", "last_device_ms", "kernel_ms", "last_kernel_ms",
-              "h2d_bytes", "h2d_ms", "d2h_bytes", "p2p_bytes", "kernel_launches")
+              "h2d_bytes", "h2d_ms", "d2h_bytes", "p2p_bytes", "kernel_launches", "host_ms")
 
     def __init__(self, release=None):
         self.requests = 0
@@ -138,6 +139,10 @@ class DeviceStats:
         self.d2h_bytes = 0
         self.p2p_bytes = 0
         self.kernel_launches = 0
+        # host time in begin() and complete() (decisions, enqueues, puts,
+        # response), excluding the waits for the device: the per-request
+        # Python/GIL work a pool of executors shares
+        self.host_ms = 0.0
         self._pending: list = []   # (events, has_kernels, has_fills), all complete on the device
         self._release = release    # events -> the executor's pool once read
         self._lock = threading.Lock()  # the worker resolves while a reader may too
@@ -352,6 +357,8 @@ class GpuExecutor:
         # executor then answers Internal without touching the device, and a
         # pool's router stops placing requests here (service.py:71-78 analogue)
         self.poisoned: str | None = None
+        self._timing_depth = 0  # host-time accounting (begin / complete may nest)
+        self._wait_s = 0.0
 
     # -- device memory ------------------------------------------------------
 
@@ -748,6 +755,20 @@ class GpuExecutor:
         return rec.response
 
     def begin(self, req: KaasRequest):
+        """Make every decision for ``req`` and enqueue its device work (see
+        ``_begin``); host time is accounted in ``dev_stats.host_ms``."""
+        if self._timing_depth:
+            return self._begin(req)
+        self._timing_depth += 1
+        t = time.perf_counter()
+        self._wait_s = 0.0
+        try:
+            return self._begin(req)
+        finally:
+            self._timing_depth -= 1
+            self.dev_stats.host_ms += (time.perf_counter() - t - self._wait_s) * 1e3
+
+    def _begin(self, req: KaasRequest):
         """Make every decision for ``req`` and enqueue its device work.
 
         Returns the finished ``KaasResponse`` when the request fails on the
@@ -823,6 +844,18 @@ class GpuExecutor:
         flushed objects, release deferred frees.  ``through`` = last seq to
         finish (all when None).  With ``block=False`` only requests whose
         device work is already done are finished.  Returns how many."""
+        if self._timing_depth:
+            return self._complete(through, block)
+        self._timing_depth += 1
+        t = time.perf_counter()
+        self._wait_s = 0.0
+        try:
+            return self._complete(through, block)
+        finally:
+            self._timing_depth -= 1
+            self.dev_stats.host_ms += (time.perf_counter() - t - self._wait_s) * 1e3
+
+    def _complete(self, through: int | None, block: bool) -> int:
         done = 0
         while self._inflight:
             seq, rec = next(iter(self._inflight.items()))
@@ -836,7 +869,9 @@ class GpuExecutor:
                 except DeviceError:
                     pass  # faulted: the sync below reports it for this request
             try:
+                tw = time.perf_counter()
                 ev[1].sync()
+                self._wait_s += time.perf_counter() - tw
             except DeviceError as exc:
                 # the device faulted under this request: nothing it computed
                 # may reach the store; it (and every later one) fails in band
