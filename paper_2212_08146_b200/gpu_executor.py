@@ -38,7 +38,7 @@ import itertools
 import threading
 import time
 
-from collections import OrderedDict
+from collections import OrderedDict, deque
 from dataclasses import dataclass, field, replace
 
 import numpy as np
@@ -305,6 +305,8 @@ class GpuExecutor:
     """Owns one device cache on one GPU; requests are decided strictly in
     arrival order and may overlap on the device (``begin`` / ``complete``)."""
 
+    recycle_blocks = True  # device block free list (class-level switch for A/B runs)
+
     def __init__(self, config: ExecutorConfig, store, backend: GpuBackend | None = None,
                  time_requests: bool = True):
         self.config = config
@@ -353,6 +355,9 @@ class GpuExecutor:
         self._prep_cap = pc
         self._prep_bytes = 0
         self._skipped: list = []  # zero-fills elided for the request being begun
+        self._blocks: dict[int, deque] = {}  # recycled device blocks by size (FIFO)
+        self._block_bytes = 0
+        self._block_cap = max(256 << 20, min(2 << 30, config.capacity // 2))
         # set when a CUDA fault left the device unusable (a sticky error): the
         # executor then answers Internal without touching the device, and a
         # pool's router stops placing requests here (service.py:71-78 analogue)
@@ -367,8 +372,50 @@ class GpuExecutor:
         buf._req = self._req_seq
 
     def _alloc(self, buf: DeviceBuffer, stream: native.Stream) -> None:
-        buf.ptr = native.malloc_async(stream, buf.size)
+        buf.ptr = self._dmalloc(buf.size, stream)
         buf.dev = self.device
+
+    # Device blocks are recycled by exact size: a block whose last user has
+    # completed on the device goes back to a per-executor free list instead
+    # of cudaFreeAsync, and the next allocation of that size takes it
+    # without a C-ABI crossing (a warm Jacobi request replaces 4 blocks).
+    # The free list is outside the ledger (decisions never see it) and is
+    # emptied before any allocation is allowed to fail.
+    def _dmalloc(self, nbytes: int, stream: native.Stream) -> int:
+        lst = self._blocks.get(nbytes)
+        if lst:
+            # first freed, first reused: a steady request stream gets the same
+            # block for the same buffer every time, so its memoised launch
+            # (descriptor table keyed by the buffer addresses) keeps hitting
+            self._block_bytes -= nbytes
+            return lst.popleft()
+        try:
+            return native.malloc_async(stream, nbytes)
+        except DeviceError:
+            if not self._block_bytes:
+                raise
+            self._release_blocks()
+            return native.malloc_async(stream, nbytes)
+
+    def _dfree(self, ptr: int, nbytes: int, stream: native.Stream) -> None:
+        """``ptr``'s last user is done on the device (or ordered by stream waits)."""
+        if self.poisoned is not None:
+            return  # a faulted context frees nothing (it is torn down whole)
+        if nbytes and self.recycle_blocks and self._block_bytes + nbytes <= self._block_cap:
+            lst = self._blocks.get(nbytes)
+            if lst is None:
+                lst = self._blocks[nbytes] = deque()
+            lst.append(ptr)
+            self._block_bytes += nbytes
+        else:
+            native.free_async(stream, ptr)
+
+    def _release_blocks(self) -> None:
+        for lst in self._blocks.values():
+            for ptr in lst:
+                native.free_async(self.s_exec, ptr)
+        self._blocks.clear()
+        self._block_bytes = 0
 
     def _alloc_zeroed(self, buf: DeviceBuffer, name: str | None = None) -> None:
         self._alloc(buf, self.s_exec)
@@ -389,16 +436,16 @@ class GpuExecutor:
         self._fence_lends(buf)
         self._clear_derived(buf)
         ptr, buf.ptr = buf.ptr, 0
-        self._free_after_user(buf, ptr)
+        self._free_after_user(buf, ptr, buf.size)
 
-    def _free_after_user(self, buf: DeviceBuffer, ptr: int, stream=None) -> None:
+    def _free_after_user(self, buf: DeviceBuffer, ptr: int, nbytes: int, stream=None) -> None:
         owner = self._inflight.get(buf._req)
         if owner is None and self._cur is not None and buf._req == self._cur.seq:
             owner = self._cur
         if owner is not None:
-            owner.graveyard.append(ptr)  # freed on s_exec when the owner completes
-        elif self.poisoned is None:  # a faulted context frees nothing (it is torn down whole)
-            native.free_async(self.s_in if stream is None else stream, ptr)
+            owner.graveyard.append((ptr, nbytes))  # released when the owner completes
+        else:
+            self._dfree(ptr, nbytes, self.s_in if stream is None else stream)
 
     # -- prepared operands ------------------------------------------------------
     # cGEMM's 3xTF32 split of A and split + 4M expansion + transpose of B are
@@ -416,7 +463,7 @@ class GpuExecutor:
             self._prep_bytes -= nbytes
             # allocated and used on s_exec: free there too, so the pool can
             # hand the block straight to the next prepared operand
-            self._free_after_user(buf, ptr, self.s_exec)
+            self._free_after_user(buf, ptr, nbytes, self.s_exec)
 
     def _derived_slot(self, buf: DeviceBuffer, key, nbytes: int):
         """-> [ptr, nbytes, ready] for ``key`` on ``buf``, allocating (on the
@@ -432,7 +479,7 @@ class GpuExecutor:
         if buf._hits == 0 or self._prep_bytes + nbytes > self._prep_cap:
             return None
         try:
-            ptr = native.malloc_async(self.s_exec, nbytes)
+            ptr = self._dmalloc(nbytes, self.s_exec)
         except DeviceError:  # device memory short: this launch uses scratch instead
             return None
         slot = [ptr, nbytes, False]
@@ -825,9 +872,8 @@ class GpuExecutor:
             self.complete()
             self._drain_streams_quietly()
             self._release(resolved, ephemerals, drop_dirty=True)
-            if self.poisoned is None:
-                for ptr in rec.graveyard:
-                    native.free_async(self.s_exec, ptr)
+            for ptr, nbytes in rec.graveyard:
+                self._dfree(ptr, nbytes, self.s_exec)
             if rec.events is not None:
                 self._ev_pool.append(rec.events)
             return self._finish(req, stats, t0, Status.make_error(exc.kind, exc.message))
@@ -891,9 +937,8 @@ class GpuExecutor:
                 if (self.peers is not None and isinstance(version, int) and buf.ptr
                         and self.cache.entries.get(key) is buf and not buf.dirty):
                     self.peers.publish(self.executor_id, buf, version, None)
-            if self.poisoned is None:
-                for ptr in rec.graveyard:
-                    native.free_async(self.s_exec, ptr)
+            for ptr, nbytes in rec.graveyard:
+                self._dfree(ptr, nbytes, self.s_exec)
             self.dev_stats.requests += 1
             del self._inflight[seq]
             if self.time_requests and self.poisoned is None:  # spans read later (DeviceStats.resolve)
@@ -1100,6 +1145,7 @@ class GpuExecutor:
             buf._pinned = 0
             buf._dirty = False
             self.cache.remove(key)
+        self._release_blocks()
         self._drain_streams_quietly()
         for s in (self.s_in, self.s_exec, self.s_out):
             s.sync()
