@@ -237,13 +237,14 @@ struct GemmShape {
                      // both red.add-ed onto a zeroed C ((0+a)+b == (0+b)+a
                      // exactly, so the result is deterministic)
   int kb_chunk;      // k-blocks per fresh-accumulator chunk (see k_cgemm_fused4)
+  int group_m;       // m-blocks per raster group
 };
 
-constexpr int kGroupM = 8;  // m-blocks per raster group (= one write-back panel)
+constexpr int kGroupM = 8;  // m-blocks per write-back panel (and the default raster group)
 
 __device__ __forceinline__ void tile_coords(const GemmShape &s, int t, int &mb, int &nb) {
-  // group 8 m-blocks together so concurrently running CTAs share B tiles in L2
-  constexpr int GM = kGroupM;
+  // group m-blocks together so concurrently running CTAs share B tiles in L2
+  const int GM = s.group_m;
   const int per_group = GM * s.num_n;
   const int g = t / per_group;
   const int first_m = g * GM;
@@ -688,6 +689,8 @@ int launch_cgemm(cudaStream_t s, int dev, int n, int m, int k, uint64_t cov, con
   shape.cov = cov;
   shape.ksplit = ksplit2 ? 2 : 1;
   shape.kb_chunk = kCgemmChunkKb;
+  shape.group_m = kGroupM;
+  if (const char *ge = KAAS_DEV_ENV("KAAS_CGEMM_GROUPM")) shape.group_m = atoi(ge) > 0 ? atoi(ge) : kGroupM;
   if (const char *ce = KAAS_DEV_ENV("KAAS_CGEMM_CHUNK")) shape.kb_chunk = atoi(ce) > 0 ? atoi(ce) : 1 << 30;
   if (ksplit2) KAAS_CUDA(cudaMemsetAsync(C, 0, (size_t)n * m * 8, s));
   return narrow ? launch_gemm2<128>(s, dev, ma, mbm, shape, C, sc, po)

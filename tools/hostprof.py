@@ -34,5 +34,9 @@ pr.enable()
 for i in range(200):
     svc.submit(req(1000 + i))
 pr.disable()
-pstats.Stats(pr).sort_stats("tottime").print_stats(35)
+st = pstats.Stats(pr)
+st.sort_stats("tottime").print_stats(30)
+st.sort_stats("cumulative").print_callees("_begin")
+st.print_callees("_complete")
+st.print_callees("_launch")
 svc.close()
