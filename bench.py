@@ -83,6 +83,61 @@ def profile_traffic(name):
 # ---------------------------------------------------------------------------
 # clocks sampling (B200_PROFILING.md recipe)
 
+class NvmlSampler:
+    """Clocks, power and clock-event reasons sampled through NVML every
+    ``period`` seconds in a thread -- dense enough for a timed region of a
+    few tens of milliseconds (nvidia-smi -lms 200 yields one sample there)."""
+
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
+
+    def __init__(self, gpu: int, period: float = 0.005):
+        import pynvml
+        self.nv = pynvml
+        pynvml.nvmlInit()
+        self.h = pynvml.nvmlDeviceGetHandleByIndex(gpu)
+        self.period = period
+        self.samples: list[tuple[float, float, int]] = []
+        self._stop = threading.Event()
+        self._thread = None
+
+    def start(self):
+        self._thread = threading.Thread(target=self._run, daemon=True)
+        self._thread.start()
+
+    def _run(self):
+        nv, h = self.nv, self.h
+        while not self._stop.is_set():
+            try:
+                self.samples.append((float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)),
+                                     nv.nvmlDeviceGetPowerUsage(h) / 1000.0,
+                                     int(nv.nvmlDeviceGetCurrentClocksEventReasons(h))))
+            except Exception:  # noqa: BLE001 -- a failed read is a missing sample
+                pass
+            self._stop.wait(self.period)
+
+    def stop(self) -> dict:
+        self._stop.set()
+        if self._thread is not None:
+            self._thread.join(timeout=2)
+        nv = self.nv
+        smax = float(nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM))
+        reasons = sorted({name for name, attr in self.REASONS for _, _, r in self.samples
+                          if r & getattr(nv, attr)})
+        loaded = [c for c, p, _ in self.samples if p > 200.0] or [c for c, _, _ in self.samples]
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": smax,
+                "reasons": reasons, "samples": len(self.samples), "source": "nvml, 5 ms"}
+
+
+def clock_sampler(gpu: int):
+    try:
+        return NvmlSampler(gpu)
+    except Exception:  # noqa: BLE001 -- no NVML: the nvidia-smi recipe
+        return ClockSampler(gpu)
+
+
 class ClockSampler:
     QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -491,7 +546,7 @@ def ours(args, rank, world, local_rank, dist):
     gc.collect()
     gc.freeze()
     barrier(dist)
-    sampler = ClockSampler(local_rank)
+    sampler = clock_sampler(local_rank)
     sampler.start()
     launches0 = native.launch_counter()
     h2d0, d2h0 = ex.dev_stats.h2d_bytes, ex.dev_stats.d2h_bytes
