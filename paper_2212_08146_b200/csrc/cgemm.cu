@@ -504,6 +504,245 @@ k_cgemm_fused4(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
 }
 
 // ---------------------------------------------------------------------------
+// CTA-pair kernel (cta_group::2): two SMs of a TPC compute one M256 x N256
+// tile.  Each CTA loads its own 128 rows of A and 128 of the tile's 256
+// Bt rows (N half) per stage -- 32 KiB instead of 48 KiB -- and the leader
+// issues tcgen05.mma.cta_group::2 (M=256, N=256, K=8), which reads A and B
+// from both CTAs' shared memory; each CTA's TMEM accumulates its 128 rows x
+// all 256 columns.  Operand traffic per output element is 2/3 of the 1-CTA
+// M128 x N256 tile's.  Everything else is k_cgemm_fused4's: three products
+// per k-step, K-chunked accumulation drained by 8 epilogue warps per CTA,
+// progressive write-back.
+//
+// Barriers (per CTA unless noted): full[s] -- the LEADER's counts both CTAs'
+// TMA bytes (the peer's copies signal it through the cluster address with
+// the peer bit cleared) and only the leader arms it; empty[s] -- in both
+// CTAs, released by the leader's MMA commit multicast to both; tfull[a] --
+// both CTAs, MMA commit multicast; tempty[a] -- the LEADER's counts the
+// epilogue warps of both CTAs (the peer's arrive remotely).
+constexpr int kPairStages = 6;
+struct SmemPair {
+  alignas(1024) float a_hi[kPairStages][BM * BK2];
+  alignas(1024) float a_lo[kPairStages][BM * BK2];
+  alignas(1024) float b_hi[kPairStages][128 * BK2];
+  alignas(1024) float b_lo[kPairStages][128 * BK2];
+  uint64_t full[kPairStages];
+  uint64_t empty[kPairStages];
+  uint64_t tfull[2];
+  uint64_t tempty[2];
+  uint32_t tmem_base;
+};
+constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;  // shared::cluster address of the pair's rank 0
+
+__device__ __forceinline__ uint32_t pair_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap *map, uint64_t *bar, void *dst, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar) & kPeerBitMask), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_tf32_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                 uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, {%5, %5, %5, %5, %5, %5, %5, %5}, p;\n\t}" ::"r"(
+          tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(0u)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_pair(uint64_t *bar) {  // arrive on bar in both CTAs
+  asm volatile(
+      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t *bar) {  // the pair's rank-0 copy of bar
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(smem_u32(bar)));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM2_THREADS, 1)
+k_cgemm_pair(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+             const GemmShape s, float *__restrict__ C, unsigned *panel_done) {
+  constexpr int BN = 256, HALF = BN / 2;
+  extern __shared__ uint8_t smem_raw[];
+  SmemPair &sm = *reinterpret_cast<SmemPair *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = pair_rank();
+  const bool leader = rank == 0;
+  constexpr uint32_t kTmemCols = 2 * BN;
+  constexpr uint32_t kPairStageBytes = (2 * BM + 2 * 128) * BK2 * 4;  // one CTA's share
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&map_a);
+    tma_prefetch_desc(&map_b);
+    for (int i = 0; i < kPairStages; ++i) {
+      mbar_init(&sm.full[i], 1);
+      mbar_init(&sm.empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sm.tfull[i], 1);
+      mbar_init(&sm.tempty[i], 2 * kEpiWarps);  // only the leader's copy is used
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&sm.tmem_base)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();  // both CTAs' barriers initialised and TMEM allocated
+  tc_fence_after();
+  const uint32_t tmem_base = sm.tmem_base;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int tiles = s.num_m * s.num_n;  // num_m counts 256-row tiles here
+  const int kbs = s.kb_per_seg;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = pair; t < tiles; t += npairs) {
+        int mb, nb;
+        tile_coords(s, t, mb, nb);
+        const int arow = mb * 256 + (int)rank * 128, brow = nb * BN + (int)rank * 128;
+        for (int kb = 0; kb < kbs; ++kb) {
+          mbar_wait(&sm.empty[stage], phase ^ 1);
+          if (leader) mbar_arrive_expect_tx(&sm.full[stage], 2 * kPairStageBytes);
+          tma_load_2d_pair(&map_a, &sm.full[stage], sm.a_hi[stage], kb * BK2, arow);
+          tma_load_2d_pair(&map_a, &sm.full[stage], sm.a_lo[stage], kb * BK2, s.a_lo_row + arow);
+          tma_load_2d_pair(&map_b, &sm.full[stage], sm.b_hi[stage], kb * BK2, brow);
+          tma_load_2d_pair(&map_b, &sm.full[stage], sm.b_lo[stage], kb * BK2, s.b_lo_row + brow);
+          if (++stage == kPairStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = make_idesc(256, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t chunk = 0;
+      for (int t = pair; t < tiles; t += npairs) {
+        for (int c0 = 0; c0 < kbs; c0 += s.kb_chunk, ++chunk) {
+          const int c1 = min(kbs, c0 + s.kb_chunk);
+          const uint32_t acc = chunk & 1;
+          mbar_wait(&sm.tempty[acc], ((chunk >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t tmem_d = tmem_base + acc * BN;
+          for (int kb = c0; kb < c1; ++kb) {
+            mbar_wait(&sm.full[stage], phase);
+            tc_fence_after();
+            const uint32_t ah = smem_u32(sm.a_hi[stage]), al = smem_u32(sm.a_lo[stage]);
+            const uint32_t bh = smem_u32(sm.b_hi[stage]), bl = smem_u32(sm.b_lo[stage]);
+#pragma unroll
+            for (int k = 0; k < BK2 / 8; ++k) {
+              const uint32_t off = k * 32;
+              tc_mma_tf32_pair(tmem_d, make_sw64_desc(ah + off), make_sw64_desc(bl + off), idesc,
+                               kb != c0 || k != 0);
+              tc_mma_tf32_pair(tmem_d, make_sw64_desc(al + off), make_sw64_desc(bh + off), idesc, 1);
+              tc_mma_tf32_pair(tmem_d, make_sw64_desc(ah + off), make_sw64_desc(bh + off), idesc, 1);
+            }
+            tc_commit_pair(&sm.empty[stage]);
+            if (++stage == kPairStages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          tc_commit_pair(&sm.tfull[acc]);
+        }
+      }
+    }
+  } else {
+    const int quarter = warp & 3;
+    const int half = (warp - 2) / 4;
+    uint32_t chunk = 0;
+    for (int t = pair; t < tiles; t += npairs) {
+      int mb, nb;
+      tile_coords(s, t, mb, nb);
+      const uint32_t lane_base = tmem_base + ((uint32_t)(quarter * 32) << 16) + half * HALF;
+      float sum[HALF];
+#pragma unroll
+      for (int j = 0; j < HALF; ++j) sum[j] = 0.f;
+      for (int c0 = 0; c0 < kbs; c0 += s.kb_chunk, ++chunk) {
+        const uint32_t acc = chunk & 1;
+        mbar_wait(&sm.tfull[acc], (chunk >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int q = 0; q < HALF / 32; ++q) {
+          uint32_t v[32];
+          tmem_ld32(lane_base + acc * BN + 32 * q, v);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) sum[32 * q + j] = __fadd_rn(sum[32 * q + j], __uint_as_float(v[j]));
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_leader(&sm.tempty[acc]);
+      }
+      const int row = mb * 256 + (int)rank * 128 + quarter * 32 + lane;
+      const int col0 = nb * BN + half * HALF;
+      if (row < s.M) {
+        float *dst = C + (size_t)row * s.N + col0;
+#pragma unroll
+        for (int q = 0; q < HALF / 32; ++q) {
+          const int col = col0 + 32 * q;
+          float *d = dst + 32 * q;
+          const unsigned long long g0 = (unsigned long long)row * s.m_complex + (col >> 1);
+          const bool full = (col + 32 <= s.N) && (g0 + 16 <= s.cov) &&
+                            ((reinterpret_cast<uintptr_t>(d) & 15u) == 0);
+          if (full) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              reinterpret_cast<float4 *>(d)[j] = make_float4(sum[32 * q + 4 * j], sum[32 * q + 4 * j + 1],
+                                                             sum[32 * q + 4 * j + 2], sum[32 * q + 4 * j + 3]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int c = col + j;
+              if (c < s.N && (unsigned long long)row * s.m_complex + (c >> 1) < s.cov) d[j] = sum[32 * q + j];
+            }
+          }
+        }
+      }
+      if (panel_done != nullptr) {
+        __threadfence();
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+        // each CTA reports its own 128-row m-block (the host counts panels in those)
+        const int mb128 = mb * 2 + (int)rank;
+        if (warp == 2 && lane == 0 && mb128 * BM < s.M) {
+          __threadfence_system();
+          atomicAdd(&panel_done[mb128 / kGroupM], 1u);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // neither CTA leaves while the pair's MMAs may touch its smem / TMEM
+  tc_fence_after();
+  if (warp == 1) {
+    __syncwarp();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols));
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host side
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
@@ -611,6 +850,63 @@ int launch_gemm2(cudaStream_t s, int dev, const CUtensorMap &ma, const CUtensorM
   return 0;
 }
 
+// CTA-pair launch: shape.num_m counts 256-row tiles, map_b's box is 128 rows
+// (each CTA's half of the N256 tile).  Progressive write-back panels are in
+// 128-row m-blocks as for the 1-CTA kernel.
+int launch_pair(cudaStream_t s, int dev, const CUtensorMap &ma, const CUtensorMap &mb, const GemmShape &shape,
+                float *C, StreamScratch *sc, const ProgressiveOut *po) {
+  const size_t smem = sizeof(SmemPair) + 1024;
+  static std::atomic<uint64_t> attr_done{0};
+  if (!(attr_done.load(std::memory_order_relaxed) >> (dev & 63) & 1)) {
+    KAAS_CUDA(cudaFuncSetAttribute(k_cgemm_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_done.fetch_or(1ull << (dev & 63));
+  }
+  const int tiles = shape.num_m * shape.num_n;
+  int pairs = device_props(dev).sm_count / 2;
+  if (pairs > tiles) pairs = tiles;
+  const int num_m128 = (shape.M + BM - 1) / BM;
+  const int npanels = (num_m128 + kGroupM - 1) / kGroupM;
+  WaitValue32Fn waitv = get_wait_value();
+  const bool progressive = po != nullptr && waitv != nullptr && npanels > 1 && npanels <= kMaxPanels &&
+                           sc->panel_done != nullptr;
+  if (po && !sc->cg_ev_ready) {
+    KAAS_CUDA(cudaEventCreateWithFlags(&sc->cg_ev_ready, cudaEventDisableTiming));
+    KAAS_CUDA(cudaEventCreateWithFlags(&sc->cg_ev_done, cudaEventDisableTiming));
+  }
+  cudaEvent_t ev_ready = sc->cg_ev_ready, ev_done = sc->cg_ev_done;
+  if (progressive) {
+    KAAS_CUDA(cudaMemsetAsync(sc->panel_done, 0, npanels * sizeof(unsigned), s));
+    KAAS_CUDA(cudaEventRecord(ev_ready, s));
+    KAAS_CUDA(cudaStreamWaitEvent(po->out_stream, ev_ready, 0));
+  }
+  k_cgemm_pair<<<2 * pairs, GEMM2_THREADS, smem, s>>>(ma, mb, shape, C, progressive ? sc->panel_done : nullptr);
+  count_launch();
+  KAAS_CUDA(cudaGetLastError());
+  if (!po) return 0;
+  const uint64_t row_bytes = (uint64_t)shape.m_complex * 8;
+  uint64_t copied = 0;
+  if (progressive) {
+    for (int p = 0; p < npanels; ++p) {
+      const int mb0 = p * kGroupM, mbs = min(kGroupM, num_m128 - mb0);
+      const int row0 = mb0 * BM, row1 = min(shape.M, (mb0 + mbs) * BM);
+      const unsigned want = (unsigned)(mbs * shape.num_n);
+      CUresult r = waitv((CUstream)po->out_stream, (CUdeviceptr)(sc->panel_done + p), want,
+                         0 /* CU_STREAM_WAIT_VALUE_GEQ */);
+      if (r != CUDA_SUCCESS) return fail(KAAS_E_UNSUPPORTED, "cuStreamWaitValue32 failed");
+      const uint64_t off = (uint64_t)row0 * row_bytes, len = (uint64_t)(row1 - row0) * row_bytes;
+      KAAS_CUDA(cudaMemcpyAsync((char *)po->host + off, (const char *)C + off, len, cudaMemcpyDeviceToHost,
+                                po->out_stream));
+      copied = off + len;
+    }
+  }
+  KAAS_CUDA(cudaEventRecord(ev_done, s));
+  KAAS_CUDA(cudaStreamWaitEvent(po->out_stream, ev_done, 0));
+  if (copied < po->bytes)
+    KAAS_CUDA(cudaMemcpyAsync((char *)po->host + copied, (const char *)C + copied, po->bytes - copied,
+                              cudaMemcpyDeviceToHost, po->out_stream));
+  return 0;
+}
+
 }  // namespace
 
 static int plain_copy_after(cudaStream_t s, const ProgressiveOut *po, const float *C) {
@@ -674,8 +970,37 @@ int launch_cgemm(cudaStream_t s, int dev, int n, int m, int k, uint64_t cov, con
   const bool narrow = tiles256 < sms && !ksplit2;
   const int BNv = narrow ? 128 : 256;
 
+  // 1..8 waves of M256 x N256 tiles: CTA pairs (2-5% faster at 2048^3 and
+  // 4096^3).  Beyond that the 1-CTA kernel: both are tensor-pipe bound under
+  // the board power cap there, and the pair draws more power per flop (its
+  // operand exchange between the two SMs), so it settles ~5% lower in SM
+  // clock and is 2.6% slower at 8192^3 (profiles/r02/probes/cgemm_pair.txt).
+  // Dev A/B: KAAS_CGEMM_PAIR=0 never, =1 always.
+  const char *pe = KAAS_DEV_ENV("KAAS_CGEMM_PAIR");
+  const int tiles_pair = ((n + 255) / 256) * ((N + 255) / 256);
+  const bool pair = !narrow && !ksplit2 && tiles_pair >= sms / 2 &&
+                    (pe ? pe[0] == '1' : tiles_pair <= 8 * (sms / 2));
   CUtensorMap ma, mbm;
   if ((rc = make_map(&ma, Ahi, (uint64_t)2 * n, ldk, BM, BK2, CU_TENSOR_MAP_SWIZZLE_64B))) return rc;
+  if (pair) {
+    if ((rc = make_map(&mbm, Bhi, (uint64_t)2 * N, ldk, 128, BK2, CU_TENSOR_MAP_SWIZZLE_64B))) return rc;
+    GemmShape ps;
+    ps.M = n;
+    ps.N = N;
+    ps.kb_per_seg = ldk / BK2;
+    ps.a_lo_row = n;
+    ps.b_lo_row = N;
+    ps.num_m = (n + 255) / 256;
+    ps.num_n = (N + 255) / 256;
+    ps.m_complex = m;
+    ps.cov = cov;
+    ps.ksplit = 1;
+    ps.kb_chunk = kCgemmChunkKb;
+    ps.group_m = kGroupM / 2;
+    if (const char *ge = KAAS_DEV_ENV("KAAS_CGEMM_GROUPM")) ps.group_m = atoi(ge) > 0 ? atoi(ge) : kGroupM / 2;
+    if (const char *ce = KAAS_DEV_ENV("KAAS_CGEMM_CHUNK")) ps.kb_chunk = atoi(ce) > 0 ? atoi(ce) : 1 << 30;
+    return launch_pair(s, dev, ma, mbm, ps, C, sc, po);
+  }
   if ((rc = make_map(&mbm, Bhi, (uint64_t)2 * N, ldk, BNv, BK2, CU_TENSOR_MAP_SWIZZLE_64B))) return rc;
   GemmShape shape;
   shape.M = n;

@@ -137,6 +137,17 @@ def test_cgemm_partial_coverage_and_empty_k(gpu):
     assert bytes(store.get("cg/Cz")) == bytes(96)
 
 
+@pytest.mark.parametrize("shape,cov", [((2100, 1300, 257), None), ((2100, 1300, 257), 2100 * 1300 - 98765),
+                                       ((2048, 2048, 40), None), ((4000, 2500, 33), None),
+                                       ((4100, 4000, 20), None)])
+def test_cgemm_pair_ragged(gpu, shape, cov):
+    """Shapes with >= 74 M256 x N256 tiles take the CTA-pair kernel: ragged M
+    (an odd count of 128-row blocks, so the last pair's second CTA has no
+    rows), ragged N, partial coverage, K not a multiple of the k-block."""
+    ex, store = gpu
+    _cgemm_check(ex, store, *shape, cov=cov, seed=shape[0] + shape[2])
+
+
 def test_cgemm_config1_1024(gpu):
     """BASELINE configs[0]: cGEMM 1024^3 complex64 kaasReq."""
     ex, store = gpu
