@@ -387,6 +387,14 @@ static int jacobi_run_length(const kaas_launch_desc *d, const Plan *plans, int i
   return len < 1 ? 1 : len;
 }
 
+// invocation runs: the shortest run worth one persistent launch, and the dev
+// A/B switch (KAAS_RUN=0: every invocation launches on its own)
+constexpr int kRunMinLength = 2;
+static bool run_use_enabled() {
+  const char *e = KAAS_DEV_ENV("KAAS_RUN");
+  return !(e && e[0] == '0');
+}
+
 static int coop_serialise_begin(int dev, cudaStream_t s) {
   std::lock_guard<std::mutex> g(g_mu);
   auto it = g_coop_event.find(dev);
@@ -530,6 +538,7 @@ int kaas_stream_destroy(uint64_t stream) {
     if (sc->cg_buf) cudaFreeAsync(sc->cg_buf, s);
     free_jacobi_memo(sc);
     if (sc->mm_buf) cudaFreeAsync(sc->mm_buf, s);
+    if (sc->run_done) cudaFreeAsync(sc->run_done, s);
     cudaStreamSynchronize(s);
     if (sc->panel_done) cudaFree(sc->panel_done);
     if (sc->cg_ev_ready) cudaEventDestroy(sc->cg_ev_ready);
@@ -826,6 +835,35 @@ static int launch_batch_impl(int dev, uint64_t stream, const kaas_launch_desc *d
       if ((rc = coop_serialise_end(dev, s))) return rc;
       i += run;
       continue;
+    }
+    // a run of >= 2 builtin invocations: one persistent launch (runs.cu)
+    {
+      auto inv_of = [&](int j) {
+        RunInv r{};
+        const kaas_launch_desc &d = descs[j];
+        r.kernel = d.kernel;
+        r.flags = d.flags;
+        memcpy(r.ext, plans[j].ext, sizeof r.ext);
+        r.cov = plans[j].cov;
+        r.fval = plans[j].fval;
+        for (int q = 0; q < 4; ++q) {
+          r.ptr[q] = q < KAAS_MAX_ARGS ? d.ptrs[q] : 0;
+          r.size[q] = q < KAAS_MAX_ARGS ? d.sizes[q] : 0;
+        }
+        return r;
+      };
+      int len = 0;
+      while (i + len < n && run_use_enabled() && run_eligible(inv_of(i + len))) ++len;
+      if (len >= kRunMinLength) {
+        std::vector<RunInv> inv((size_t)len);
+        for (int t = 0; t < len; ++t) inv[t] = inv_of(i + t);
+        int rc;
+        if ((rc = coop_serialise_begin(dev, s))) return rc;
+        if ((rc = launch_builtin_run(s, dev, sc, inv.data(), len))) return rc;
+        if ((rc = coop_serialise_end(dev, s))) return rc;
+        i += len;
+        continue;
+      }
     }
     ProgressiveOut po;
     const ProgressiveOut *pop = nullptr;

@@ -6,6 +6,7 @@
 
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/kaas_b200.h"
 
@@ -58,6 +59,10 @@ struct StreamScratch {
   void *jac_memo = nullptr;  // owned; freed by free_jacobi_memo
   // cGEMM write-back ordering events, created on first use, reused per launch
   cudaEvent_t cg_ev_ready = nullptr, cg_ev_done = nullptr;
+  // invocation-run kernel (runs.cu): per-task arrival counters, monotonic
+  // across launches, and the host's running expectation of each
+  unsigned *run_done = nullptr;  // [kRunMaxTasks]
+  std::vector<uint32_t> run_expect;
 };
 constexpr int kJacTaggedMaxN = 4096;
 constexpr int kMaxPanels = 1024;
@@ -125,5 +130,19 @@ struct CgemmPrepared {
 int launch_cgemm(cudaStream_t s, int dev, int n, int m, int k, uint64_t cov,
                  const float *A, const float *B, float *C, StreamScratch *sc,
                  const ProgressiveOut *po = nullptr, const CgemmPrepared *prep = nullptr);
+
+// ---- invocation runs (runs.cu): consecutive builtin invocations of one
+// batch executed by one persistent cooperative launch
+struct RunInv {
+  int kernel;     // KAAS_K_*
+  int flags;      // kaas_launch_desc.flags
+  uint64_t ext[3];
+  uint64_t cov;
+  float fval;
+  uint64_t ptr[4];
+  uint64_t size[4];
+};
+bool run_eligible(const RunInv &v);
+int launch_builtin_run(cudaStream_t s, int dev, StreamScratch *sc, const RunInv *v, int n);
 
 }  // namespace kaas
