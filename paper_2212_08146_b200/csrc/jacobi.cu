@@ -914,29 +914,50 @@ k_jacobi_tmem(const __grid_constant__ ChainParams p, float *partials, unsigned *
     }
     return a;
   };
-  // fill the three tiers once per launch
+  // fill the three tiers once per launch (64 MiB of A at N = 4096): rows go
+  // in batches so each thread keeps 16 loads in flight -- one row at a time
+  // left the fill latency-bound (~20 us per request for 4 loads in flight)
+  constexpr int kFillB = 4;  // rows per batch
+  static_assert(kTmRT % kFillB == 0, "TMEM rows fill in whole batches");
 #pragma unroll 1
-  for (int r = 0; r < kTmRT; ++r) {
-    uint32_t v[16];
+  for (int rb = 0; rb < kTmRT; rb += kFillB) {
+    float4 t4[kFillB][kColC4];
 #pragma unroll
-    for (int u = 0; u < kColC4; ++u) {
-      const float4 a = lda(r, u);
-      v[4 * u + 0] = __float_as_uint(a.x);
-      v[4 * u + 1] = __float_as_uint(a.y);
-      v[4 * u + 2] = __float_as_uint(a.z);
-      v[4 * u + 3] = __float_as_uint(a.w);
+    for (int j = 0; j < kFillB; ++j)
+#pragma unroll
+      for (int u = 0; u < kColC4; ++u) t4[j][u] = lda(rb + j, u);
+#pragma unroll
+    for (int j = 0; j < kFillB; ++j) {
+      uint32_t v[16];
+#pragma unroll
+      for (int u = 0; u < kColC4; ++u) {
+        v[4 * u + 0] = __float_as_uint(t4[j][u].x);
+        v[4 * u + 1] = __float_as_uint(t4[j][u].y);
+        v[4 * u + 2] = __float_as_uint(t4[j][u].z);
+        v[4 * u + 3] = __float_as_uint(t4[j][u].w);
+      }
+      KAAS_TMEM_ST16(taddr + 16u * (rb + j), v);
     }
-    KAAS_TMEM_ST16(taddr + 16u * r, v);
+  }
+#pragma unroll 1
+  for (int rb = 0; rb < kTmRS; rb += kFillB) {
+    float4 t4[kFillB][kColC4];
+#pragma unroll
+    for (int j = 0; j < kFillB; ++j)
+#pragma unroll
+      for (int u = 0; u < kColC4; ++u)
+        t4[j][u] = rb + j < kTmRS ? lda(kTmRT + kTmRR + rb + j, u) : zero4();
+#pragma unroll
+    for (int j = 0; j < kFillB; ++j)
+#pragma unroll
+      for (int u = 0; u < kColC4; ++u)
+        if (rb + j < kTmRS) acache[((rb + j) * kColC4 + u) * kColT + tid] = t4[j][u];
   }
   float4 areg[kTmRR][kColC4];
 #pragma unroll
   for (int r = 0; r < kTmRR; ++r)
 #pragma unroll
     for (int u = 0; u < kColC4; ++u) areg[r][u] = lda(kTmRT + r, u);
-#pragma unroll 1
-  for (int r = 0; r < kTmRS; ++r)
-#pragma unroll
-    for (int u = 0; u < kColC4; ++u) acache[(r * kColC4 + u) * kColT + tid] = lda(kTmRT + kTmRR + r, u);
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
