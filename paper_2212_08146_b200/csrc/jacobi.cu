@@ -252,6 +252,7 @@ struct ChainParams {
   int tagged;
   int poll_ns;  // back-off between unsuccessful polls
   unsigned zero;  // always 0: an opaque value ptxas cannot fold (k_jacobi_tmem)
+  unsigned sync_base;  // the grid-barrier counter's value when this launch starts
   unsigned *trace;  // dev: [32 sweeps][148 CTAs][3] globaltimer_lo stamps, or nullptr
 };
 
@@ -261,18 +262,20 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
   return v;
 }
 
-// Monotonic grid barrier: the counter is zeroed before each launch; barrier
-// number e completes when the counter reaches (e+1)*gridDim.x.  One
-// release-atomic per CTA, acquire-polling, no reset, no extra fences
-// (release is cumulative over the CTA's writes ordered by bar.sync).
-__device__ __forceinline__ void grid_sync_mono(unsigned *counter, unsigned epoch) {
+// Monotonic grid barrier: the counter only ever grows (the host tracks its
+// value across launches on the stream: no reset, no memset before a launch);
+// barrier number e of a launch completes when it reaches base + (e+1) *
+// gridDim.x (compared modulo 2^32).  One release-atomic per CTA,
+// acquire-polling, no extra fences (release is cumulative over the CTA's
+// writes ordered by bar.sync).
+__device__ __forceinline__ void grid_sync_mono(unsigned *counter, unsigned epoch, unsigned base) {
   __syncthreads();
   if (threadIdx.x == 0) {
     asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(counter) : "memory");
-    const unsigned target = (epoch + 1) * gridDim.x;
+    const unsigned target = base + (epoch + 1) * gridDim.x;
     // ld.acquire.gpu lowers to LDG.STRONG.GPU + CCTL.IVALL: the SM's L1 is
     // invalidated, so later plain loads of x see the other CTAs' writes
-    while (ld_acquire(counter) < target) {
+    while ((int)(ld_acquire(counter) - target) < 0) {
     }
   }
   __syncthreads();
@@ -436,7 +439,7 @@ k_jacobi_rows(const __grid_constant__ ChainParams p, float *partials, unsigned *
           slot[blockIdx.x] = cta;
         }
       }
-      grid_sync_mono(sync + 3, (unsigned)s);  // also: xs reads done before the next stage-in
+      grid_sync_mono(sync + 3, (unsigned)s, p.sync_base);  // also: xs reads done before the next stage-in
       if (want_resid && blockIdx.x == 0 && threadIdx.x < 32)
         finish_resid(slot, gridDim.x, p.ptrs[p.idx[s][2] & 0x7f]);
     } else {
@@ -785,7 +788,7 @@ k_jacobi_cols(const __grid_constant__ ChainParams p, float *partials, unsigned *
     }
     if (tr) trp[4] = gtimer_lo();  // rows published
     if (want_resid || !p.tagged) {
-      grid_sync_mono(sync + 3, epoch++);  // also orders red[] reuse
+      grid_sync_mono(sync + 3, epoch++, p.sync_base);  // also orders red[] reuse
       if (want_resid && blockIdx.x == 0 && threadIdx.x < 32)
         finish_resid(slot, gridDim.x, p.ptrs[p.idx[s][2] & 0x7f]);
     } else {
@@ -1193,7 +1196,7 @@ k_jacobi_tmem(const __grid_constant__ ChainParams p, float *partials, unsigned *
     if (tr) trp[4] = gtimer_lo();  // published
 #endif
     if (want_resid || !p.tagged) {
-      grid_sync_mono(sync + 3, epoch++);
+      grid_sync_mono(sync + 3, epoch++, p.sync_base);
       if (want_resid && blockIdx.x == 0 && threadIdx.x < 32)
         finish_resid(slot, gridDim.x, p.ptrs[p.idx[s][2] & 0x7f]);
     } else {
@@ -1530,7 +1533,7 @@ k_jacobi_split(const __grid_constant__ ChainParams p, float *partials, unsigned 
       }
     }
     if (want_resid || !p.tagged) {
-      grid_sync_mono(sync + 3, epoch++);
+      grid_sync_mono(sync + 3, epoch++, p.sync_base);
       if (want_resid && blockIdx.x == 0 && threadIdx.x < 32)
         finish_resid(slot, gridDim.x, p.ptrs[p.idx[s][2] & 0x7f]);
     }
@@ -1701,8 +1704,24 @@ void free_jacobi_memo(StreamScratch *sc) {
   sc->jac_memo_key = 0;
 }
 
-// the per-launch part of a tagged on-chip chain launch: fresh tags, barrier
-// counter reset, cooperative launch
+// grid barriers a launch of p passes (the kernels' grid_sync_mono calls):
+// every sweep for the untagged kernels, sweeps with an observable residual
+// for the tagged ones
+static unsigned chain_barriers(const ChainParams &p) {
+  if (!p.tagged) return (unsigned)p.sweeps;
+  unsigned c = 0;
+  for (int t = 0; t < p.sweeps; ++t) c += (p.idx[t][2] & 0x80) ? 1u : 0u;
+  return c;
+}
+
+// claim this launch's range of the stream's monotonic barrier counter
+static void claim_barriers(StreamScratch *sc, ChainParams &p, int blocks) {
+  p.sync_base = sc->jac_sync_base;
+  sc->jac_sync_base += chain_barriers(p) * (unsigned)blocks;
+}
+
+// the per-launch part of a tagged on-chip chain launch: fresh tags, the
+// barrier counter range, cooperative launch
 static int launch_tagged_chain(cudaStream_t s, StreamScratch *sc, ChainParams &p, const void *fn,
                                int blocks, size_t smem) {
   if (sc->jac_tag > 0x7fffffffu - (unsigned)p.sweeps - 2u) {  // tag space wrap: start over
@@ -1713,7 +1732,7 @@ static int launch_tagged_chain(cudaStream_t s, StreamScratch *sc, ChainParams &p
   sc->jac_tag += (unsigned)p.sweeps + 1u;
   float *partials = sc->jac_partials;
   unsigned *sync = sc->jac_sync;
-  KAAS_CUDA(cudaMemsetAsync(sync + 3, 0, sizeof(unsigned), s));  // monotonic barrier counter
+  claim_barriers(sc, p, blocks);
   void *cargs[] = {(void *)&p, (void *)&partials, (void *)&sync};
   KAAS_CUDA(cudaLaunchCooperativeKernel(fn, dim3(blocks), dim3(kColT), cargs, smem, s));
   count_launch();
@@ -1838,12 +1857,12 @@ int launch_jacobi_chain(cudaStream_t s, int dev, const JacobiChain &c, StreamScr
         done += cnt;
         continue;
       }
-      KAAS_CUDA(cudaMemsetAsync(sync + 3, 0, sizeof(unsigned), s));  // monotonic barrier counter
+      claim_barriers(sc, p, blocks);
       void *cargs[] = {(void *)&p, (void *)&partials, (void *)&sync};
       KAAS_CUDA(cudaLaunchCooperativeKernel(cfn, dim3(blocks), dim3(kColT), cargs, csmem, s));
     } else if (use_rows) {
       KAAS_CUDA(cudaFuncSetAttribute(rfn, cudaFuncAttributeMaxDynamicSharedMemorySize, c.n * 4));
-      KAAS_CUDA(cudaMemsetAsync(sync + 3, 0, sizeof(unsigned), s));  // monotonic barrier counter
+      claim_barriers(sc, p, blocks);
       void *rargs[] = {(void *)&p, (void *)&partials, (void *)&sync};
       KAAS_CUDA(cudaLaunchCooperativeKernel(rfn, dim3(blocks),
                                             dim3(rows_threads(dev, c.cov)), rargs, (size_t)c.n * 4, s));

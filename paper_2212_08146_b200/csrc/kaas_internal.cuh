@@ -50,6 +50,7 @@ struct StreamScratch {
   // Jacobi column kernel: x published as (value, tag) words, ping-pong
   unsigned long long *jac_xt = nullptr;  // [2][kJacTaggedMaxN], zeroed at creation
   unsigned jac_tag = 1;                  // next launch's tag base (host side, stream-ordered)
+  unsigned jac_sync_base = 0;            // value of the monotonic barrier counter jac_sync[3]
   // bit-exact matmul: B transposed for one launch when no prepared copy exists
   void *mm_buf = nullptr;
   size_t mm_bytes = 0;
