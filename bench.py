@@ -301,7 +301,9 @@ def measure_cgemm(n, steps, device, cold_too):
         "warm_device_ms": statistics.median(dev),
         "kernel_ms": kms,
         "useful_tflops": useful / kms / 1e9,
-        "tf32_issued_tflops": 3 * useful / kms / 1e9,
+        # tensor work issued: three fp16 products (hi.lo, lo.hi, hi.hi) per
+        # useful flop -- csrc/cgemm.cu's scaled 3xFP16 split
+        "f16_issued_tflops": 3 * useful / kms / 1e9,
         "d2h_bytes_per_step": 8 * n * n, "h2d_bytes_per_step": 0,
     })
     return out
@@ -620,16 +622,16 @@ def ours(args, rank, world, local_rank, dist):
                 # requests) under the 1 kW cap -> the SUSTAINED peak is the
                 # denominator (B200_PROFILING.md); 1024^3 is a burst kernel
                 sustained = key == "cgemm8192" and "bf16_tflops_sustained" in peaks
-                peak = (peaks["bf16_tflops_sustained"] if sustained else peaks["bf16_tflops"]) / 2
+                peak = peaks["bf16_tflops_sustained"] if sustained else peaks["bf16_tflops"]
                 e["roofline"] = {
                     "bound": "tensor", "unit": "TFLOP/s",
-                    "achieved": e["tf32_issued_tflops"],
+                    "achieved": e["f16_issued_tflops"],
                     "peak": peak,
                     "peak_kind": peak_kind + (" sustained" if sustained else " burst"),
-                    "peak_note": "TF32 dense = 1/2 of the measured BF16 dense peak (MEASURED_PEAKS.json "
-                                 "when present, else the profiling recipe's fallback)",
-                    "frac": e["tf32_issued_tflops"] / peak,
-                    "frac_of_burst": e["tf32_issued_tflops"] / (peaks["bf16_tflops"] / 2),
+                    "peak_note": "dense FP16 = the measured BF16 dense peak (same kind::f16 rate; "
+                                 "MEASURED_PEAKS.json when present, else the profiling recipe's fallback)",
+                    "frac": e["f16_issued_tflops"] / peak,
+                    "frac_of_burst": e["f16_issued_tflops"] / peaks["bf16_tflops"],
                     "traffic": profile_traffic(key),  # dram bytes per launch (ncu, cold L2)
                     "useful_tflops": e["useful_tflops"],
                 }

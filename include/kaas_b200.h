@@ -42,13 +42,15 @@ extern "C" {
 #define KAAS_K_MATMUL 3      /* backend.py:174-189  (i32 n,m,k; A, B, OUT)      */
 #define KAAS_K_REDUCE_SUM 4  /* backend.py:192-202  (i32 n; X, OUT)             */
 #define KAAS_K_FILL 5        /* backend.py:205-211  (i32 n, f32 v; OUT)         */
-#define KAAS_K_CGEMM 6       /* new: (i32 n,m,k; A, B, C) complex64, 4M x 3xTF32 */
+#define KAAS_K_CGEMM 6       /* new: (i32 n,m,k; A, B, C) complex64, 4M x 3xFP16 */
 #define KAAS_K_JACOBI 7      /* new: (i32 n; A, b, x_in, x_out, resid)         */
 
 /* kaas_launch_desc.flags for KAAS_K_CGEMM: prepared-operand cache.  ptrs[3] /
  * ptrs[4] (sizes[3] / sizes[4]) then hold the executor-owned buffers for the
- * 3xTF32-split A ([A_hi; A_lo], 2*n*ldk f32) and 4M-expanded, transposed,
- * split B ([Bt_hi; Bt_lo], 4*m*ldk f32), ldk = 2k rounded up to 32.  USE:
+ * scaled 3xFP16-split A ([A_hi; A_lo] 2*n*ldk fp16, then n u32 row
+ * max-bits: 4*n*ldk + 4*n bytes) and 4M-expanded, transposed, split B
+ * ([Bt_hi; Bt_lo] 4*m*ldk fp16, then m u32 column max-bits: 8*m*ldk + 4*m
+ * bytes), ldk = 2k rounded up to 64.  USE:
  * the buffer already holds them; FILL: compute them into it (else the
  * per-stream scratch is used and nothing is kept). */
 #define KAAS_F_CG_A_USE 1

@@ -8,30 +8,42 @@
 //   B_exp[2p,2j] = Br, B_exp[2p+1,2j] = -Bi, B_exp[2p,2j+1] = Bi, B_exp[2p+1,2j+1] = Br
 // so A needs no de-interleave and C is written interleaved directly.
 //
-// 3xTF32 split for FP32 accuracy: x = hi + lo, hi = rna_tf32(x), lo = x - hi
-// (exact).  C = A_hi.B_lo + A_lo.B_hi + A_hi.B_hi, small terms first.  (1xTF32
-// measures 2.9e-4 rel. Frobenius on 1024^3 -- over the 1e-4 budget.)  The
-// tensor core's accumulation is not round-to-nearest, so K is accumulated in
-// chunks of 512: each chunk in a fresh TMEM accumulator, the chunks summed in
-// FP32 round-to-nearest by the epilogue in fixed order (error flat in K).
+// 3xFP16 split with power-of-two scaling for FP32 accuracy.  Each row of A
+// (and each complex column of B) gets a scale 2^e that puts its largest
+// magnitude in [2^14, 2^15); then x*2^e = hi + lo with hi = rn_f16(x*2^e),
+// lo = rn_f16(x*2^e - hi): 22 significant bits, like a TF32 hi/lo pair, at
+// twice the tensor rate (kind::f16 runs K=16 per MMA where kind::tf32 runs
+// K=8, from the same 32 bytes of shared memory per row).  C =
+// A_hi.B_lo + A_lo.B_hi + A_hi.B_hi, small terms first, and the epilogue
+// multiplies by 2^-(e_row + e_col) (exact: powers of two).  (The round-1
+// kernel ran the same three products as 3xTF32: same accuracy, half the
+// rate; 1xTF32 measures 2.9e-4 rel. Frobenius at 1024^3 -- over the 1e-4
+// budget.)  The tensor core's accumulation is not round-to-nearest, so K is
+// accumulated in chunks of 512: each chunk in a fresh TMEM accumulator, the
+// chunks summed in FP32 round-to-nearest by the epilogue in fixed order
+// (error flat in K).
 //
 // Pipeline per launch:
-//   1. prep kernels (HBM-bound): A -> [A_hi; A_lo] (K-major, K padded to 32)
-//      and B -> [Bt_hi; Bt_lo] = B_exp^T (K-major), built with an smem
-//      transpose; skipped when the executor has them cached for a const input.
+//   1. prep kernels (HBM-bound): A -> [A_hi; A_lo] + row maxima (K-major
+//      fp16, K padded to 64) and B -> column maxima, then [Bt_hi; Bt_lo] =
+//      B_exp^T (K-major fp16), built with an smem transpose; skipped when the
+//      executor has them cached for a const input.  The GEMM kernel sees each
+//      fp16 row as 4-byte words (two k per word): TMA boxes and smem
+//      descriptors are the same bytes either way.
 //   2. persistent warp-specialised GEMM, one CTA per SM:
 //        warp 0  TMA producer (cp.async.bulk.tensor, SWIZZLE_64B, all four
 //                operand tiles per stage)
-//        warp 1  TMEM allocator + single-thread tcgen05.mma issuer (kind::tf32,
-//                M=128, N=BN, K=8), three products per k-step; commits release
+//        warp 1  TMEM allocator + single-thread tcgen05.mma issuer (kind::f16,
+//                M=128, N=BN, K=16), three products per k-step; commits release
 //                smem stages and publish finished K chunks
 //        warps 2-9 epilogue: tcgen05.ld 32x32b -> FP32 running sums in
-//                registers -> st.global (C interleaved complex, row-major),
-//                coverage-masked
+//                registers -> unscale -> st.global (C interleaved complex,
+//                row-major), coverage-masked
 //      TMEM holds two BN-column accumulators that alternate per K chunk, so
 //      draining chunk c overlaps the MMAs of chunk c+1 (and a tile's write-out
 //      overlaps the next tile's first chunk).
 #include <cuda.h>
+#include <cuda_fp16.h>
 
 #include <atomic>
 #include <cstdlib>
@@ -49,77 +61,135 @@ constexpr int GEMM_THREADS = 192;
 // ---------------------------------------------------------------------------
 // prep kernels
 
-__device__ __forceinline__ float tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
+// Operand scaling.  mx = the bits of max |x| over a row of A (or a complex
+// column of B); integer max on |x| bits, so a NaN beats Inf beats every
+// finite value.  e puts mx * 2^e in [2^14, 2^15) (fp16 max 65504); rows that
+// are all zero, or hold Inf / NaN, keep e = 0 (their results are Inf / NaN
+// as in FP32); e is clamped to +-125 so 2^e and 2^-e are normal floats.
+__host__ __device__ __forceinline__ int cg_exp(uint32_t mx) {
+  const int E = (int)((mx >> 23) & 0xffu);
+  if (E == 0xff) return 0;
+  if (E == 0) return mx == 0 ? 0 : 125;
+  const int e = 141 - E;  // 14 - (E - 127)
+  return e > 125 ? 125 : e;
+}
+__device__ __forceinline__ float cg_pow2(int e) { return __int_as_float((127 + e) << 23); }
+
+__device__ __forceinline__ uint32_t abs_bits(float x) { return __float_as_uint(x) & 0x7fffffffu; }
+
+// x (already scaled) -> (hi, lo) fp16 pair
+__device__ __forceinline__ void split16(float x, __half &hi, __half &lo) {
+  hi = __float2half_rn(x);
+  lo = __float2half_rn(x - __half2float(hi));
 }
 
-// A_il [n x k2] (k2 = 2k) -> Ahi/Alo [n x ldk], zero padded past k2.
-// One CTA per row band, 128-bit loads/stores when the row is 16B-aligned.
-__global__ void k_prep_a(int n, int k2, int ldk, const float *__restrict__ A, float *__restrict__ Ahi,
-                         float *__restrict__ Alo) {
+// A_il [n x k2] (k2 = 2k) -> Ahi/Alo [n x ldk] fp16 (zero padded past k2)
+// and amax[r] = max-bits of row r.  One CTA per row (grid-stride): the row is
+// read twice (max, then split), the second time from L1/L2.
+__global__ void k_prep_a(int n, int k2, int ldk, const float *__restrict__ A, __half *__restrict__ Ahi,
+                         __half *__restrict__ Alo, uint32_t *__restrict__ amax) {
+  __shared__ uint32_t wmax[32];
   const bool vec = (k2 & 3) == 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int r = blockIdx.x; r < n; r += gridDim.x) {
     const float *src = A + (size_t)r * k2;
-    float *hi = Ahi + (size_t)r * ldk, *lo = Alo + (size_t)r * ldk;
+    __half *hi = Ahi + (size_t)r * ldk, *lo = Alo + (size_t)r * ldk;
+    uint32_t mx = 0;
+    if (vec) {
+      for (int q4 = threadIdx.x; q4 < (k2 >> 2); q4 += blockDim.x) {
+        const float4 x = __ldg(reinterpret_cast<const float4 *>(src) + q4);
+        mx = max(max(mx, max(abs_bits(x.x), abs_bits(x.y))), max(abs_bits(x.z), abs_bits(x.w)));
+      }
+    } else {
+      for (int q = threadIdx.x; q < k2; q += blockDim.x) mx = max(mx, abs_bits(src[q]));
+    }
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if (lane == 0) wmax[warp] = mx;
+    __syncthreads();
+    mx = lane < nw ? wmax[lane] : 0u;
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    const float sc = cg_pow2(cg_exp(mx));
+    if (threadIdx.x == 0) amax[r] = mx;
     if (vec) {
       for (int q4 = threadIdx.x; q4 < (ldk >> 2); q4 += blockDim.x) {
         const int q = q4 << 2;
         const float4 x = q < k2 ? __ldg(reinterpret_cast<const float4 *>(src) + q4)
                                 : make_float4(0.f, 0.f, 0.f, 0.f);
-        const float4 h = make_float4(tf32_rna(x.x), tf32_rna(x.y), tf32_rna(x.z), tf32_rna(x.w));
-        reinterpret_cast<float4 *>(hi)[q4] = h;
-        reinterpret_cast<float4 *>(lo)[q4] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+        __align__(8) __half h[4], l[4];
+        split16(x.x * sc, h[0], l[0]);
+        split16(x.y * sc, h[1], l[1]);
+        split16(x.z * sc, h[2], l[2]);
+        split16(x.w * sc, h[3], l[3]);
+        reinterpret_cast<uint2 *>(hi)[q4] = *reinterpret_cast<const uint2 *>(h);
+        reinterpret_cast<uint2 *>(lo)[q4] = *reinterpret_cast<const uint2 *>(l);
       }
     } else {
       for (int q = threadIdx.x; q < ldk; q += blockDim.x) {
         const float x = q < k2 ? src[q] : 0.f;
-        const float h = tf32_rna(x);
-        hi[q] = h;
-        lo[q] = x - h;
+        split16(x * sc, hi[q], lo[q]);
       }
     }
+    __syncthreads();  // wmax is reused by the next row
   }
 }
 
-// B [k x m] complex -> Bt_hi/Bt_lo [2m x ldk]:
+// bmax[j] = max-bits over p of |Br[p][j]|, |Bi[p][j]| (bmax zeroed first).
+// 1-D grid over (64-row p strip, 256-column j strip) tiles: no grid.y limit.
+constexpr int kColMaxRows = 64;
+__global__ void k_colmax_b(int k, int m, const float2 *__restrict__ B, uint32_t *__restrict__ bmax) {
+  const uint64_t jt = ((uint64_t)m + 255) / 256, tiles = jt * (((uint64_t)k + kColMaxRows - 1) / kColMaxRows);
+  for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const int j = (int)(t % jt) * 256 + threadIdx.x;
+    const int p0 = (int)(t / jt) * kColMaxRows, p1 = min(k, p0 + kColMaxRows);
+    if (j >= m) continue;
+    uint32_t mx = 0;
+    for (int p = p0; p < p1; ++p) {
+      const float2 v = __ldg(B + (size_t)p * m + j);
+      mx = max(mx, max(abs_bits(v.x), abs_bits(v.y)));
+    }
+    atomicMax(bmax + j, mx);
+  }
+}
+
+// B [k x m] complex -> Bt_hi/Bt_lo [2m x ldk] fp16, column j scaled by 2^e_j:
 //   Bt[2j][2p] = Br[p][j]  Bt[2j][2p+1] = -Bi[p][j]
 //   Bt[2j+1][2p] = Bi[p][j]  Bt[2j+1][2p+1] = Br[p][j]
-// 32 (p) x 32 (j) complex tile through smem; block 32x8 threads.
-__global__ void k_prep_b(int k, int m, int ldk, const float2 *__restrict__ B, float *__restrict__ Bhi,
-                         float *__restrict__ Blo) {
+// 32 (p) x 32 (j) complex tile through smem; block 32x8 threads.  The tiles
+// cover p < ceil(k/32)*32 = ldk/2, so they also zero the K padding.
+__global__ void k_prep_b(int k, int m, int ldk, const float2 *__restrict__ B, const uint32_t *__restrict__ bmax,
+                         __half *__restrict__ Bhi, __half *__restrict__ Blo) {
   __shared__ float2 tile[32][33];
   const int tx = threadIdx.x, ty = threadIdx.y;
   // 1-D grid over the tiles (no 65535 grid.y limit on k)
   const uint64_t tiles_m = ((uint64_t)m + 31) / 32, tiles = tiles_m * (((uint64_t)k + 31) / 32);
   for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-  const int p0 = (int)(t / tiles_m) * 32, j0 = (int)(t % tiles_m) * 32;
-  for (int r = ty; r < 32; r += 8) {
-    const int p = p0 + r, j = j0 + tx;
-    tile[r][tx] = (p < k && j < m) ? B[(size_t)p * m + j] : make_float2(0.f, 0.f);
-  }
-  __syncthreads();
-  // write: for each j (row pair 2j, 2j+1), lanes cover p = p0 + tx
-  for (int c = ty; c < 32; c += 8) {
-    const int j = j0 + c;
-    if (j >= m) continue;
-    const int p = p0 + tx;
-    const int q = 2 * p;
-    if (q >= ldk) continue;
-    const float2 v = tile[tx][c];  // (Br, Bi) at [p][j]
-    const float e0 = v.x, e1 = -v.y, o0 = v.y, o1 = v.x;
-    const float he0 = tf32_rna(e0), he1 = tf32_rna(e1), ho0 = tf32_rna(o0), ho1 = tf32_rna(o1);
-    float2 *even_hi = reinterpret_cast<float2 *>(Bhi + (size_t)(2 * j) * ldk + q);
-    float2 *odd_hi = reinterpret_cast<float2 *>(Bhi + (size_t)(2 * j + 1) * ldk + q);
-    float2 *even_lo = reinterpret_cast<float2 *>(Blo + (size_t)(2 * j) * ldk + q);
-    float2 *odd_lo = reinterpret_cast<float2 *>(Blo + (size_t)(2 * j + 1) * ldk + q);
-    *even_hi = make_float2(he0, he1);
-    *odd_hi = make_float2(ho0, ho1);
-    *even_lo = make_float2(e0 - he0, e1 - he1);
-    *odd_lo = make_float2(o0 - ho0, o1 - ho1);
-  }
-  __syncthreads();
+    const int p0 = (int)(t / tiles_m) * 32, j0 = (int)(t % tiles_m) * 32;
+    for (int r = ty; r < 32; r += 8) {
+      const int p = p0 + r, j = j0 + tx;
+      tile[r][tx] = (p < k && j < m) ? B[(size_t)p * m + j] : make_float2(0.f, 0.f);
+    }
+    __syncthreads();
+    // write: for each j (row pair 2j, 2j+1), lanes cover p = p0 + tx
+    for (int c = ty; c < 32; c += 8) {
+      const int j = j0 + c;
+      if (j >= m) continue;
+      const int p = p0 + tx;
+      const int q = 2 * p;
+      if (q >= ldk) continue;
+      const float sc = cg_pow2(cg_exp(bmax[j]));
+      const float2 v = tile[tx][c];  // (Br, Bi) at [p][j]
+      __half2 eh, el, oh, ol;
+      split16(v.x * sc, eh.x, el.x);
+      split16(-v.y * sc, eh.y, el.y);
+      split16(v.y * sc, oh.x, ol.x);
+      oh.y = eh.x;
+      ol.y = el.x;
+      *reinterpret_cast<__half2 *>(Bhi + (size_t)(2 * j) * ldk + q) = eh;
+      *reinterpret_cast<__half2 *>(Bhi + (size_t)(2 * j + 1) * ldk + q) = oh;
+      *reinterpret_cast<__half2 *>(Blo + (size_t)(2 * j) * ldk + q) = el;
+      *reinterpret_cast<__half2 *>(Blo + (size_t)(2 * j + 1) * ldk + q) = ol;
+    }
+    __syncthreads();
   }
 }
 
@@ -181,12 +251,12 @@ __device__ __forceinline__ void tc_commit(uint64_t *bar) {
                : "memory");
 }
 
-__device__ __forceinline__ void tc_mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+__device__ __forceinline__ void tc_mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
                                             uint32_t idesc, uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
@@ -202,9 +272,10 @@ __device__ __forceinline__ uint64_t make_sw128_desc(uint32_t saddr) {
   return d;
 }
 
-// kind::tf32 instruction descriptor: D=F32, A=B=TF32, both K-major.
+// kind::f16 instruction descriptor: D=F32 (bits 4-5 = 1), A=B=F16 (bits
+// 7-9, 10-12 = 0), both K-major, N>>3 at bit 17, M>>4 at bit 24.
 __host__ __device__ constexpr uint32_t make_idesc(int mdim, int ndim) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(ndim >> 3) << 17) |
+  return (1u << 4) | (0u << 7) | (0u << 10) | ((uint32_t)(ndim >> 3) << 17) |
          ((uint32_t)(mdim >> 4) << 24);
 }
 
@@ -238,6 +309,8 @@ struct GemmShape {
                      // exactly, so the result is deterministic)
   int kb_chunk;      // k-blocks per fresh-accumulator chunk (see k_cgemm_fused4)
   int group_m;       // m-blocks per raster group
+  const uint32_t *amax;  // [M] max-bits of A's rows -> row scale 2^e (cg_exp)
+  const uint32_t *bmax;  // [N/2] max-bits of B's complex columns -> column scale
 };
 
 constexpr int kGroupM = 8;  // m-blocks per write-back panel (and the default raster group)
@@ -257,15 +330,15 @@ __device__ __forceinline__ void tile_coords(const GemmShape &s, int t, int &mb, 
 // ---------------------------------------------------------------------------
 // v2: all four operand tiles in every stage, three products per k-step.
 //
-// Stage = {A_hi, A_lo} [BM x 16] + {B_hi, B_lo} [BN x 16] fp32, 64-byte rows,
-// SWIZZLE_64B (48 KiB at BN = 256, 4 stages).  Per k-step of 8 the single MMA
-// thread issues A_hi.B_lo, A_lo.B_hi, A_hi.B_hi into the tile's TMEM
-// accumulator, so K is walked once instead of three times: 2/3 of v1's
-// L2->SMEM operand traffic for the same tensor work.
+// Stage = {A_hi, A_lo} [BM x 32] + {B_hi, B_lo} [BN x 32] fp16, 64-byte rows,
+// SWIZZLE_64B (48 KiB at BN = 256, 4 stages).  Per k-step of 16 the single
+// MMA thread issues A_hi.B_lo, A_lo.B_hi, A_hi.B_hi into the tile's TMEM
+// accumulator, so K is walked once instead of three times.  The smem arrays
+// and TMA coordinates count 4-byte words (two fp16 k each): BK2 words = 32 k.
 constexpr int BK2 = 16;
-// k-blocks (of BK2 interleaved k) per fresh-accumulator chunk: 512 of K
-constexpr int kCgemmChunkKb = 32;
-// ring depth: stages of (2 BM + 2 BN) x 16 fp32 -- 32 KiB at BN = 128, 48 KiB
+// k-blocks (of 2 * BK2 interleaved k) per fresh-accumulator chunk: 512 of K
+constexpr int kCgemmChunkKb = 16;
+// ring depth: stages of (2 BM + 2 BN) x 16 words -- 32 KiB at BN = 128, 48 KiB
 // at BN = 256 -- as many as fit next to the barriers (192 KiB either way); the
 // narrow-tile case needs the depth to cover L2 latency (each stage is only
 // 384 MMA cycles there)
@@ -309,6 +382,22 @@ __device__ __forceinline__ uint64_t make_sw64_desc(uint32_t saddr) {
 // share TMEM lane quarter w % 4 and split the tile's columns in halves, so a
 // thread holds BN / 2 running sums.
 constexpr int kEpiWarps = 8;
+
+// sums (in the scaled domain) of row `row`, real columns col0.. -> C's
+// values: times 2^-e_row, then 2^-e_col (each exact for normal results;
+// columns 2j and 2j+1 share complex column j's scale).  The warp's lanes
+// share the columns, so the scale loads are broadcasts.
+// Applied per 32-column block q right before its stores.
+template <int HALF>
+__device__ __forceinline__ void unscale(const GemmShape &s, float ra, int col, float (&sum)[HALF], int q) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int cj = (col >> 1) + j;
+    const float cb = 2 * cj < s.N ? cg_pow2(-cg_exp(__ldg(s.bmax + cj))) : 1.f;
+    sum[32 * q + 2 * j] = (sum[32 * q + 2 * j] * ra) * cb;
+    sum[32 * q + 2 * j + 1] = (sum[32 * q + 2 * j + 1] * ra) * cb;
+  }
+}
 constexpr int GEMM2_THREADS = 64 + 32 * kEpiWarps;
 
 template <int BN>
@@ -397,10 +486,10 @@ k_cgemm_fused4(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
               const uint32_t off = k * 32;
               // small terms first, then the main product; the chunk's first
               // MMA starts a fresh accumulator
-              tc_mma_tf32(tmem_d, make_sw64_desc(ah + off), make_sw64_desc(bl + off), idesc,
+              tc_mma_f16(tmem_d, make_sw64_desc(ah + off), make_sw64_desc(bl + off), idesc,
                           kb != c0 || k != 0);
-              tc_mma_tf32(tmem_d, make_sw64_desc(al + off), make_sw64_desc(bh + off), idesc, 1);
-              tc_mma_tf32(tmem_d, make_sw64_desc(ah + off), make_sw64_desc(bh + off), idesc, 1);
+              tc_mma_f16(tmem_d, make_sw64_desc(al + off), make_sw64_desc(bh + off), idesc, 1);
+              tc_mma_f16(tmem_d, make_sw64_desc(ah + off), make_sw64_desc(bh + off), idesc, 1);
             }
             tc_commit(&sm.empty[stage]);
             if (++stage == STAGES2) {
@@ -444,9 +533,11 @@ k_cgemm_fused4(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
       const int col0 = nb * BN + half * HALF;
       if (row < s.M) {
         float *dst = C + (size_t)row * s.N + col0;
+        const float ra = cg_pow2(-cg_exp(__ldg(s.amax + row)));
 #pragma unroll
         for (int q = 0; q < HALF / 32; ++q) {
           const int col = col0 + 32 * q;
+          unscale<HALF>(s, ra, col, sum, q);
           float *d = dst + 32 * q;
           const unsigned long long g0 = (unsigned long long)row * s.m_complex + (col >> 1);
           const bool full = (col + 32 <= s.N) && (g0 + 16 <= s.cov) &&
@@ -549,12 +640,12 @@ __device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap *map, uint64_
       "l"(map), "r"(smem_u32(bar) & kPeerBitMask), "r"(c0), "r"(c1)
       : "memory");
 }
-__device__ __forceinline__ void tc_mma_tf32_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+__device__ __forceinline__ void tc_mma_f16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                                  uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, {%5, %5, %5, %5, %5, %5, %5, %5}, p;\n\t}" ::"r"(
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, {%5, %5, %5, %5, %5, %5, %5, %5}, p;\n\t}" ::"r"(
           tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(0u)
       : "memory");
@@ -654,10 +745,10 @@ k_cgemm_pair(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ 
 #pragma unroll
             for (int k = 0; k < BK2 / 8; ++k) {
               const uint32_t off = k * 32;
-              tc_mma_tf32_pair(tmem_d, make_sw64_desc(ah + off), make_sw64_desc(bl + off), idesc,
+              tc_mma_f16_pair(tmem_d, make_sw64_desc(ah + off), make_sw64_desc(bl + off), idesc,
                                kb != c0 || k != 0);
-              tc_mma_tf32_pair(tmem_d, make_sw64_desc(al + off), make_sw64_desc(bh + off), idesc, 1);
-              tc_mma_tf32_pair(tmem_d, make_sw64_desc(ah + off), make_sw64_desc(bh + off), idesc, 1);
+              tc_mma_f16_pair(tmem_d, make_sw64_desc(al + off), make_sw64_desc(bh + off), idesc, 1);
+              tc_mma_f16_pair(tmem_d, make_sw64_desc(ah + off), make_sw64_desc(bh + off), idesc, 1);
             }
             tc_commit_pair(&sm.empty[stage]);
             if (++stage == kPairStages) {
@@ -699,9 +790,11 @@ k_cgemm_pair(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ 
       const int col0 = nb * BN + half * HALF;
       if (row < s.M) {
         float *dst = C + (size_t)row * s.N + col0;
+        const float ra = cg_pow2(-cg_exp(__ldg(s.amax + row)));
 #pragma unroll
         for (int q = 0; q < HALF / 32; ++q) {
           const int col = col0 + 32 * q;
+          unscale<HALF>(s, ra, col, sum, q);
           float *d = dst + 32 * q;
           const unsigned long long g0 = (unsigned long long)row * s.m_complex + (col >> 1);
           const bool full = (col + 32 <= s.N) && (g0 + 16 <= s.cov) &&
@@ -930,31 +1023,44 @@ int launch_cgemm(cudaStream_t s, int dev, int n, int m, int k, uint64_t cov, con
     KAAS_CUDA(cudaMemsetAsync(C, 0, cells * 8, s));
     return po ? plain_copy_after(s, po, C) : 0;
   }
+  // operand layout (cgemm_prepared_bytes): [hi plane | lo plane] fp16, rows
+  // of ldk halves (2k rounded up to 64: whole 128-byte rows), then the
+  // per-row (A) / per-complex-column (B) max-bits that fix the scales
   const int k2 = 2 * k;
-  const int ldk = (k2 + BK - 1) / BK * BK;
-  const size_t a_elems = (size_t)n * ldk, b_elems = (size_t)2 * m * ldk;
+  const int ldk = (int)cgemm_ldk16(k);
+  const int ldkw = ldk / 2;  // the same rows in 4-byte words (TMA / MMA view)
+  const size_t a_half = (size_t)n * ldk, b_half = (size_t)2 * m * ldk;
+  const size_t a_bytes = cgemm_prepared_bytes(0, n, m, k), b_bytes = cgemm_prepared_bytes(1, n, m, k);
   // operands come from the executor's prepared-operand cache when it has
   // them; otherwise from per-stream scratch (only the missing side)
   const bool a_ext = prep && prep->a, b_ext = prep && prep->b;
-  const size_t need = ((a_ext ? 0 : 2 * a_elems) + (b_ext ? 0 : 2 * b_elems)) * sizeof(float);
+  const size_t a_scr = a_ext ? 0 : (a_bytes + 255) / 256 * 256;
+  const size_t need = a_scr + (b_ext ? 0 : b_bytes);
   int rc = need ? ensure_cgemm_scratch(sc, s, need) : 0;
   if (rc) return rc;
-  float *scratch = (float *)sc->cg_buf;
-  float *Ahi = a_ext ? prep->a : scratch;
-  float *Alo = Ahi + a_elems;
-  float *Bhi = b_ext ? prep->b : scratch + (a_ext ? 0 : 2 * a_elems);
-  float *Blo = Bhi + b_elems;
+  char *scratch = (char *)sc->cg_buf;
+  __half *Ahi = a_ext ? (__half *)prep->a : (__half *)scratch;
+  __half *Alo = Ahi + a_half;
+  uint32_t *amax = reinterpret_cast<uint32_t *>(Ahi + 2 * a_half);
+  __half *Bhi = b_ext ? (__half *)prep->b : (__half *)(scratch + a_scr);
+  __half *Blo = Bhi + b_half;
+  uint32_t *bmax = reinterpret_cast<uint32_t *>(Bhi + 2 * b_half);
 
   const int sms = device_props(dev).sm_count;
   if (!(a_ext && prep->a_ready)) {
-    k_prep_a<<<n < sms * 16 ? n : sms * 16, 256, 0, s>>>(n, k2, ldk, A, Ahi, Alo);
+    k_prep_a<<<n < sms * 16 ? n : sms * 16, 256, 0, s>>>(n, k2, ldk, A, Ahi, Alo, amax);
     count_launch();
   }
   if (!(b_ext && prep->b_ready)) {
+    KAAS_CUDA(cudaMemsetAsync(bmax, 0, (size_t)m * 4, s));
+    const uint64_t ctiles = (((uint64_t)m + 255) / 256) * (((uint64_t)k + kColMaxRows - 1) / kColMaxRows);
+    k_colmax_b<<<(unsigned)(ctiles < (uint64_t)sms * 16 ? ctiles : (uint64_t)sms * 16), 256, 0, s>>>(
+        k, m, reinterpret_cast<const float2 *>(B), bmax);
+    count_launch();
     const uint64_t tiles = (uint64_t)((m + 31) / 32) * (uint64_t)((k + 31) / 32);
     dim3 gb((unsigned)(tiles < (uint64_t)sms * 16 ? tiles : (uint64_t)sms * 16));
     // also zero-fills the K padding columns [2k, ldk)
-    k_prep_b<<<gb, dim3(32, 8), 0, s>>>(k, m, ldk, reinterpret_cast<const float2 *>(B), Bhi, Blo);
+    k_prep_b<<<gb, dim3(32, 8), 0, s>>>(k, m, ldk, reinterpret_cast<const float2 *>(B), bmax, Bhi, Blo);
     count_launch();
   }
   KAAS_CUDA(cudaGetLastError());
@@ -966,7 +1072,7 @@ int launch_cgemm(cudaStream_t s, int dev, int n, int m, int k, uint64_t cov, con
   const bool full_cov = cov >= (uint64_t)n * m;
   const char *ke = KAAS_DEV_ENV("KAAS_CGEMM_KSPLIT");  // dev A/B: 0 = never split K
   const bool ksplit2 = !(ke && ke[0] == '0') && full_cov && tiles256 < sms && 2 * tiles256 <= sms &&
-                       ldk / BK2 >= 16;
+                       ldkw / BK2 >= 16;
   const bool narrow = tiles256 < sms && !ksplit2;
   const int BNv = narrow ? 128 : 256;
 
@@ -981,13 +1087,15 @@ int launch_cgemm(cudaStream_t s, int dev, int n, int m, int k, uint64_t cov, con
   const bool pair = !narrow && !ksplit2 && tiles_pair >= sms / 2 &&
                     (pe ? pe[0] == '1' : tiles_pair <= 8 * (sms / 2));
   CUtensorMap ma, mbm;
-  if ((rc = make_map(&ma, Ahi, (uint64_t)2 * n, ldk, BM, BK2, CU_TENSOR_MAP_SWIZZLE_64B))) return rc;
+  if ((rc = make_map(&ma, (const float *)Ahi, (uint64_t)2 * n, ldkw, BM, BK2, CU_TENSOR_MAP_SWIZZLE_64B))) return rc;
   if (pair) {
-    if ((rc = make_map(&mbm, Bhi, (uint64_t)2 * N, ldk, 128, BK2, CU_TENSOR_MAP_SWIZZLE_64B))) return rc;
+    if ((rc = make_map(&mbm, (const float *)Bhi, (uint64_t)2 * N, ldkw, 128, BK2, CU_TENSOR_MAP_SWIZZLE_64B))) return rc;
     GemmShape ps;
     ps.M = n;
     ps.N = N;
-    ps.kb_per_seg = ldk / BK2;
+    ps.kb_per_seg = ldkw / BK2;
+    ps.amax = amax;
+    ps.bmax = bmax;
     ps.a_lo_row = n;
     ps.b_lo_row = N;
     ps.num_m = (n + 255) / 256;
@@ -1001,11 +1109,13 @@ int launch_cgemm(cudaStream_t s, int dev, int n, int m, int k, uint64_t cov, con
     if (const char *ce = KAAS_DEV_ENV("KAAS_CGEMM_CHUNK")) ps.kb_chunk = atoi(ce) > 0 ? atoi(ce) : 1 << 30;
     return launch_pair(s, dev, ma, mbm, ps, C, sc, po);
   }
-  if ((rc = make_map(&mbm, Bhi, (uint64_t)2 * N, ldk, BNv, BK2, CU_TENSOR_MAP_SWIZZLE_64B))) return rc;
+  if ((rc = make_map(&mbm, (const float *)Bhi, (uint64_t)2 * N, ldkw, BNv, BK2, CU_TENSOR_MAP_SWIZZLE_64B))) return rc;
   GemmShape shape;
   shape.M = n;
   shape.N = N;
-  shape.kb_per_seg = ldk / BK2;
+  shape.kb_per_seg = ldkw / BK2;
+  shape.amax = amax;
+  shape.bmax = bmax;
   shape.a_lo_row = n;
   shape.b_lo_row = N;
   shape.num_m = (n + BM - 1) / BM;

@@ -300,14 +300,15 @@ static int run_plan(int dev, cudaStream_t s, const kaas_launch_desc *d, const Pl
       if (n > 0x7fffffff || p.ext[1] > 0x7fffffff || p.ext[2] > 0x7fffffff)
         return fail(KAAS_E_BOUNDS, "cgemm: extent exceeds i32");
       CgemmPrepared prep;
-      const uint64_t ldk = (2 * p.ext[2] + 31) / 32 * 32;
       if (d->flags & (KAAS_F_CG_A_USE | KAAS_F_CG_A_FILL)) {
-        if (d->sizes[3] < 2 * n * ldk * 4) return fail(KAAS_E_BOUNDS, "cgemm: prepared A buffer too small");
+        if (d->sizes[3] < cgemm_prepared_bytes(0, n, p.ext[1], p.ext[2]))
+          return fail(KAAS_E_BOUNDS, "cgemm: prepared A buffer too small");
         prep.a = (float *)d->ptrs[3];
         prep.a_ready = (d->flags & KAAS_F_CG_A_USE) != 0;
       }
       if (d->flags & (KAAS_F_CG_B_USE | KAAS_F_CG_B_FILL)) {
-        if (d->sizes[4] < 4 * p.ext[1] * ldk * 4) return fail(KAAS_E_BOUNDS, "cgemm: prepared B buffer too small");
+        if (d->sizes[4] < cgemm_prepared_bytes(1, n, p.ext[1], p.ext[2]))
+          return fail(KAAS_E_BOUNDS, "cgemm: prepared B buffer too small");
         prep.b = (float *)d->ptrs[4];
         prep.b_ready = (d->flags & KAAS_F_CG_B_USE) != 0;
       }

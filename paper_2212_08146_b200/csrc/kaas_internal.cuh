@@ -124,10 +124,19 @@ int launch_jacobi_memo(cudaStream_t s, int dev, StreamScratch *sc);
 void free_jacobi_memo(StreamScratch *sc);
 // Prepared-operand buffers for cGEMM (nullptr = use per-stream scratch).
 struct CgemmPrepared {
-  float *a = nullptr;  // [A_hi; A_lo]
-  float *b = nullptr;  // [Bt_hi; Bt_lo]
+  float *a = nullptr;  // [A_hi; A_lo] fp16 + row max-bits
+  float *b = nullptr;  // [Bt_hi; Bt_lo] fp16 + column max-bits
   bool a_ready = false, b_ready = false;
 };
+// fp16 elements per prepared operand row: 2k rounded up to 64 (128 bytes)
+inline uint64_t cgemm_ldk16(uint64_t k) { return (2 * k + 63) / 64 * 64; }
+// bytes of a prepared operand: side 0 = A (n rows), 1 = B (2m rows): hi and
+// lo planes of fp16 rows, then 4 bytes of max-bits per row of A / complex
+// column of B (gpu_executor.py computes the same sizes)
+inline uint64_t cgemm_prepared_bytes(int side, uint64_t n, uint64_t m, uint64_t k) {
+  const uint64_t ldk = cgemm_ldk16(k);
+  return side == 0 ? 2 * n * ldk * 2 + 4 * n : 2 * (2 * m) * ldk * 2 + 4 * m;
+}
 int launch_cgemm(cudaStream_t s, int dev, int n, int m, int k, uint64_t cov,
                  const float *A, const float *B, float *C, StreamScratch *sc,
                  const ProgressiveOut *po = nullptr, const CgemmPrepared *prep = nullptr);

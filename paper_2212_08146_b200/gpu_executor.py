@@ -752,9 +752,12 @@ class GpuExecutor:
                 n_, m_, k_ = (lit.value for lit in inv.literals)
                 if n_ * m_ * k_ == 0 or inv.dims.total_threads == 0:
                     continue  # nothing is computed, so nothing would be prepared
-                ldk = (2 * k_ + 31) // 32 * 32
+                # fp16 hi/lo planes (rows of 2k rounded up to 64) + 4 B of
+                # scale max-bits per row of A / complex column of B
+                # (cgemm_prepared_bytes, csrc/kaas_internal.cuh)
+                ldk = (2 * k_ + 63) // 64 * 64
                 sides = []
-                for j, nbytes in ((0, 8 * n_ * ldk), (1, 16 * m_ * ldk)):
+                for j, nbytes in ((0, 4 * n_ * ldk + 4 * n_), (1, 8 * m_ * ldk + 4 * m_)):
                     arg = by_name[inv.args[j]]
                     ok = arg.is_const and not arg.is_ephemeral and arg.name not in dirty
                     sides.append((arg.name, ("cg", j, n_, m_, k_), nbytes) if ok else None)

@@ -148,6 +148,36 @@ def test_cgemm_pair_ragged(gpu, shape, cov):
     _cgemm_check(ex, store, *shape, cov=cov, seed=shape[0] + shape[2])
 
 
+def test_cgemm_scaled_rows_and_columns(gpu):
+    """The fp16 split scales every row of A and complex column of B by its own
+    power of two: rows / columns spread over 2^-50 .. 2^50 (products over
+    2^-100 .. 2^100, and all-zero ones) each keep FP32-class accuracy, element
+    by element against the |A|.|B| bound (a matrix-wide rel. Frobenius would
+    hide the tiny rows)."""
+    ex, store = gpu
+    n, m, k = 200, 136, 150
+    rng = np.random.default_rng(77)
+    A = (rng.standard_normal((n, k)) + 1j * rng.standard_normal((n, k)))
+    B = (rng.standard_normal((k, m)) + 1j * rng.standard_normal((k, m)))
+    A *= np.exp2(rng.integers(-50, 51, n)).astype(np.float64)[:, None]
+    B *= np.exp2(rng.integers(-50, 51, m)).astype(np.float64)[None, :]
+    A[3] = 0
+    B[:, 5] = 0
+    A[7, :5] *= 2.0 ** 30   # one row with a wide internal range
+    A, B = A.astype("<c8"), B.astype("<c8")
+    store.put("cgs/A", A.tobytes())
+    store.put("cgs/B", B.tobytes())
+    _run(ex, W.cgemm_request("cgs", n, "cgs/A", "cgs/B", "cgs/C", m=m, k=k))
+    got = np.frombuffer(store.get("cgs/C"), "<c8").reshape(n, m).astype(np.complex128)
+    A64, B64 = A.astype(np.complex128), B.astype(np.complex128)
+    truth = A64 @ B64
+    bound = np.abs(A64) @ np.abs(B64)
+    rel = np.abs(got - truth) / np.where(bound > 0, bound, 1.0)
+    assert np.all(got[3] == 0) and np.all(got[:, 5] == 0)
+    print(f"cgemm scaled rows/columns: max |err| / (|A||B|) = {rel.max():.3e}")
+    assert rel.max() <= 1e-5, f"max elementwise error / (|A||B|) = {rel.max():.3e}"
+
+
 def test_cgemm_config1_1024(gpu):
     """BASELINE configs[0]: cGEMM 1024^3 complex64 kaasReq."""
     ex, store = gpu
@@ -156,7 +186,7 @@ def test_cgemm_config1_1024(gpu):
 
 
 def test_cgemm_prepared_operand_cache(cuda):
-    """Warm cGEMMs reuse the cached 3xTF32 operands: results are bit-identical
+    """Warm cGEMMs reuse the cached split operands: results are bit-identical
     to a run without the cache; a refill of the key through a non-const
     binding, and eviction, discard the prepared forms."""
     n, m, k = 192, 160, 96

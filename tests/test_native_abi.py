@@ -63,7 +63,7 @@ def test_sass_contains_blackwell_instructions():
                              text=True, timeout=120).stdout
     except (OSError, subprocess.TimeoutExpired):
         pytest.skip("cuobjdump unavailable")
-    assert "UTCHMMA" in out        # tcgen05.mma kind::tf32
+    assert "UTCHMMA" in out        # tcgen05.mma kind::f16
     assert "LDTM" in out           # tcgen05.ld
     assert "UTMALDG" in out        # cp.async.bulk.tensor (cGEMM operands)
     assert "STTM" in out           # tcgen05.st (Jacobi band of A into TMEM)

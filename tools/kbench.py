@@ -82,7 +82,7 @@ def cgemm(n=8192, reps=3):
     ms = timed(s, lambda: native.launch_batch(0, s, d), reps)
     useful = 8.0 * n ** 3
     print(f"cgemm n={n}: {ms:.3f} ms/launch  useful {useful / ms / 1e9:.1f} TFLOP/s  "
-          f"tf32-issued {3 * useful / ms / 1e9:.1f} TFLOP/s")
+          f"f16-issued (3 products) {3 * useful / ms / 1e9:.1f} TFLOP/s")
 
 
 def matmul(M, N, K, reps=5):
