@@ -309,18 +309,19 @@ def measure_cgemm(n, steps, device, cold_too):
     return out
 
 
-def measure_mixed(device, clients=16, count=160, policy="affinity:8", capacity=512 << 20, devices=None):
-    """BASELINE configs[3]: multi-tenant mixed cGEMM (2048^3) + Jacobi (N=4096,
-    100 sweeps), Zipf(1.0) over 8+8 const objects, 16 client threads, LRU
-    pressure (768 MiB universe vs 512 MiB ledger per GPU).  One executor per
-    GPU in ``devices`` (default: this rank's GPU) behind the affinity router."""
+def measure_mixed(device, clients=16, count=160, policy="affinity:8", capacity=2 << 30, devices=None):
+    """BASELINE configs[3] at SURVEY.md 8(d)'s sizes: multi-tenant mixed cGEMM
+    (4096^3, A_i . B_j over 16 const 128 MiB matrices) + Jacobi (N=4096, 500
+    sweeps, 16 const 64 MiB systems), Zipf(1.0), 16 client threads, LRU
+    pressure (3 GiB universe vs a 2 GiB ledger per GPU).  One executor per GPU
+    in ``devices`` (default: this rank's GPU) behind the affinity router."""
     from paper_2212_08146_b200 import workloads as W
     from paper_2212_08146_b200.benchlib import run_stream
     from paper_2212_08146_b200.hoststore import PinnedStore
     from paper_2212_08146_b200.pool import KaasService
     store = PinnedStore()
-    uni = W.mixed_universe(store)
-    reqs = W.mixed_requests(uni, count)
+    uni = W.mixed_universe(store, n_cgemm=16, cg_n=4096, n_jacobi=16, jac_n=4096)
+    reqs = W.mixed_requests(uni, count, sweeps=500, out_slots=8)
     devices = devices or [device]
     with KaasService(store, n_executors=len(devices), capacity=capacity, policy=policy,
                      devices=devices) as svc:
@@ -344,8 +345,8 @@ def measure_mixed(device, clients=16, count=160, policy="affinity:8", capacity=5
         evictions = sum(e.cache.evictions for e in exs)
         per_gpu = [e.dev_stats.requests - s0 for e, s0 in zip(exs, served0)]
         ex_dev_ms = sum(e.dev_stats.device_ms for e in exs) - dev0
-    return {"workload": "mixed cgemm 2048^3 + jacobi N=4096x100 sweeps, zipf(1.0) over 8+8 const "
-                        f"objects, {clients} clients, {policy}, ledger {capacity >> 20} MiB/GPU; "
+    return {"workload": "mixed cgemm 4096^3 + jacobi N=4096x500 sweeps, zipf(1.0) over 16+16 const "
+                        f"objects (3 GiB), {clients} clients, {policy}, ledger {capacity >> 20} MiB/GPU; "
                         "measured pass after one warm-up pass of the same stream",
             "requests": len(reqs), "errors": sum(0 if r.status.ok else 1 for r in resps),
             "req_per_s": len(reqs) / wall, "p50_ms": percentile(lat, 0.5) * 1e3,

@@ -310,7 +310,7 @@ def mixed_universe(store, n_cgemm: int = 8, cg_n: int = 2048, n_jacobi: int = 8,
 
 
 def mixed_requests(universe: dict, count: int, sweeps: int = 100, zipf_s: float = 1.0,
-                   seed: int = 1) -> list[KaasRequest]:
+                   seed: int = 1, out_slots: int = 32) -> list[KaasRequest]:
     """Multi-tenant stream: half cGEMM (A_i . B_j, both const, Zipf-drawn),
     half Jacobi solves (system k const, Zipf-drawn); request ids carry a
     tenant prefix (``t<c>/``) for the exclusive policy."""
@@ -324,9 +324,9 @@ def mixed_requests(universe: dict, count: int, sweeps: int = 100, zipf_s: float 
         if rng.random() < 0.5:
             a, b = zc.draw(), zc.draw()
             out.append(cgemm_request(f"{tenant}/cg{i}", n, f"mix/cg/{a}", f"mix/cg/{b}",
-                                     f"mix/out/cg{i % 32}"))
+                                     f"mix/out/cg{i % out_slots}"))
         else:
             k = zj.draw()
             out.append(jacobi_request(f"{tenant}/jac{i}", jn, sweeps, f"mix/jA/{k}", f"mix/jb/{k}",
-                                      "mix/x0", f"mix/out/x{i % 32}", f"mix/out/r{i % 32}"))
+                                      "mix/x0", f"mix/out/x{i % out_slots}", f"mix/out/r{i % out_slots}"))
     return out
