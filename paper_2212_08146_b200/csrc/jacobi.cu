@@ -236,6 +236,7 @@ k_jacobi_sweep(int n, int cov, const float *__restrict__ A, const float *__restr
 
 constexpr int kChainMaxPtrs = 16;
 constexpr int kTraceStamps = 5;  // dev trace: per sweep and CTA (tools/jtrace.py)
+constexpr int kTracePro = 8;     // dev trace: per-CTA launch-phase stamps after the sweep stamps
 constexpr int kChainMaxSweeps = 2048;
 
 struct ChainParams {
@@ -875,6 +876,18 @@ __device__ __forceinline__ float sum2(unsigned long long v) {
 template <int RR, int MODE, int DEP>
 __global__ void __launch_bounds__(kColT, 1)
 k_jacobi_tmem(const __grid_constant__ ChainParams p, float *partials, unsigned *sync) {
+#ifdef KAAS_DEV
+  // launch-phase stamps (thread 0 of each CTA): entry, TMEM allocated, band
+  // filled, sweep 0 published, sweep 1 published, before teardown
+  unsigned *pro = p.trace != nullptr && threadIdx.x == 0
+                      ? p.trace + 32 * 148 * kTraceStamps + (blockIdx.x < 148 ? blockIdx.x : 147) * kTracePro
+                      : nullptr;
+  if (pro) pro[0] = gtimer_lo();
+#define KAAS_PRO(i) \
+  if (pro) pro[i] = gtimer_lo();
+#else
+#define KAAS_PRO(i)
+#endif
   constexpr int kTmRR = RR, kTmRS = kTmOther - RR, kTmDep = DEP, kTmBatch = 1;
   static_assert(kTmRS >= 0 && kTmRR + kTmRS <= 16, "one 16-slot reduction set for the non-TMEM rows");
   extern __shared__ __align__(16) float4 acache[];  // [kTmRS][kColC4][kColT]
@@ -898,15 +911,23 @@ k_jacobi_tmem(const __grid_constant__ ChainParams p, float *partials, unsigned *
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  KAAS_PRO(1)
   const uint32_t taddr = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(warp >> 2) * 256u;
 
-  // A[r0 + rl][cbase + 32u] with the diagonal zeroed; rows past the band and
-  // columns past n are 0 (their partials are discarded / contribute nothing)
+  // A[r0 + rl][cbase + 32u]; rows past the band and columns past n are 0
+  // (their partials are discarded / contribute nothing).  The diagonal is
+  // zeroed by zdiag AFTER a whole batch of loads is in flight: touching a
+  // loaded value right after its load makes the one warp holding the row's
+  // diagonal wait for that load before issuing the next, which serialised
+  // the fill into one HBM round trip per row (44 us per request; 4x the
+  // 64 MiB / HBM-bandwidth floor).
   auto lda = [&](int rl, int u) -> float4 {
     float4 a = zero4();
-    if (rl >= R) return a;
     const float4 *rp = reinterpret_cast<const float4 *>(p.A) + (size_t)(r0 + rl) * n4 + cbase;
-    if (full || cbase + 32 * u < n4) a = ld_a(reinterpret_cast<const float *>(rp + 32 * u), pol);
+    if (rl < R && (full || cbase + 32 * u < n4)) a = ld_a(reinterpret_cast<const float *>(rp + 32 * u), pol);
+    return a;
+  };
+  auto zdiag = [&](float4 &a, int rl, int u) {
     const int c4 = cbase + 32 * u, i = r0 + rl;
     if (c4 == (i >> 2)) {
       const int d = i & 3;
@@ -915,12 +936,14 @@ k_jacobi_tmem(const __grid_constant__ ChainParams p, float *partials, unsigned *
       a.z = d == 2 ? 0.f : a.z;
       a.w = d == 3 ? 0.f : a.w;
     }
-    return a;
   };
   // fill the three tiers once per launch (64 MiB of A at N = 4096): rows go
-  // in batches so each thread keeps 16 loads in flight -- one row at a time
-  // left the fill latency-bound (~20 us per request for 4 loads in flight)
-  constexpr int kFillB = 4;  // rows per batch
+  // in batches of 4 (16 loads per thread in flight), the diagonal patched
+  // after each batch's loads are issued.  (Issuing the shared-memory rows as
+  // cp.async up front, or the register rows first, fills 8 us faster but
+  // measured 8-17 us slower per 500-sweep request: the sweeps that follow
+  // run slower -- tools/jfill_ab2.sh.)
+  constexpr int kFillB = 4;  // TMEM rows per batch
   static_assert(kTmRT % kFillB == 0, "TMEM rows fill in whole batches");
 #pragma unroll 1
   for (int rb = 0; rb < kTmRT; rb += kFillB) {
@@ -931,6 +954,8 @@ k_jacobi_tmem(const __grid_constant__ ChainParams p, float *partials, unsigned *
       for (int u = 0; u < kColC4; ++u) t4[j][u] = lda(rb + j, u);
 #pragma unroll
     for (int j = 0; j < kFillB; ++j) {
+#pragma unroll
+      for (int u = 0; u < kColC4; ++u) zdiag(t4[j][u], rb + j, u);
       uint32_t v[16];
 #pragma unroll
       for (int u = 0; u < kColC4; ++u) {
@@ -954,18 +979,26 @@ k_jacobi_tmem(const __grid_constant__ ChainParams p, float *partials, unsigned *
     for (int j = 0; j < kFillB; ++j)
 #pragma unroll
       for (int u = 0; u < kColC4; ++u)
-        if (rb + j < kTmRS) acache[((rb + j) * kColC4 + u) * kColT + tid] = t4[j][u];
+        if (rb + j < kTmRS) {
+          zdiag(t4[j][u], kTmRT + kTmRR + rb + j, u);
+          acache[((rb + j) * kColC4 + u) * kColT + tid] = t4[j][u];
+        }
   }
   float4 areg[kTmRR][kColC4];
 #pragma unroll
   for (int r = 0; r < kTmRR; ++r)
 #pragma unroll
     for (int u = 0; u < kColC4; ++u) areg[r][u] = lda(kTmRT + r, u);
+#pragma unroll
+  for (int r = 0; r < kTmRR; ++r)
+#pragma unroll
+    for (int u = 0; u < kColC4; ++u) zdiag(areg[r][u], kTmRT + r, u);
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
+  KAAS_PRO(2)
   // reduction slot l holds band row l (slots 28..31 empty)
   const int my_rl = lane;
   float bi = 0.f, di = 1.f;
@@ -1195,6 +1228,9 @@ k_jacobi_tmem(const __grid_constant__ ChainParams p, float *partials, unsigned *
 #ifdef KAAS_DEV
     if (tr) trp[4] = gtimer_lo();  // published
 #endif
+    if (s < 2) {
+      KAAS_PRO(3 + s)
+    }
     if (want_resid || !p.tagged) {
       grid_sync_mono(sync + 3, epoch++, p.sync_base);
       if (want_resid && blockIdx.x == 0 && threadIdx.x < 32)
@@ -1204,6 +1240,8 @@ k_jacobi_tmem(const __grid_constant__ ChainParams p, float *partials, unsigned *
     }
   }
 
+  KAAS_PRO(5)
+#undef KAAS_PRO
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -1824,7 +1862,7 @@ int launch_jacobi_chain(cudaStream_t s, int dev, const JacobiChain &c, StreamScr
         if (KAAS_DEV_ENV("KAAS_JACOBI_NOWAIT")) p.tagged = 3;  // dev: compute-only timing
 #endif
         static unsigned *trace_buf = nullptr;  // dev: KAAS_JACOBI_TRACE=1 (tools/jtrace.py)
-        if (KAAS_DEV_ENV("KAAS_JACOBI_TRACE") && !trace_buf) cudaMalloc((void **)&trace_buf, 32 * 148 * kTraceStamps * 4);
+        if (KAAS_DEV_ENV("KAAS_JACOBI_TRACE") && !trace_buf) cudaMalloc((void **)&trace_buf, (32 * 148 * kTraceStamps + 148 * kTracePro) * 4);
         p.trace = KAAS_DEV_ENV("KAAS_JACOBI_TRACE") ? trace_buf : nullptr;
         jacobi_trace_buffer() = p.trace;
         const char *pe = KAAS_DEV_ENV("KAAS_JACOBI_POLL_NS");  // dev A/B
@@ -1884,7 +1922,8 @@ int launch_jacobi_chain(cudaStream_t s, int dev, const JacobiChain &c, StreamScr
 extern "C" int kaas_dev_jacobi_trace(void *host, unsigned long bytes) {
   unsigned *buf = kaas::jacobi_trace_buffer();
   if (!buf) return 1;
-  if (bytes > 32ul * 148 * kaas::kTraceStamps * 4) bytes = 32ul * 148 * kaas::kTraceStamps * 4;
+  const unsigned long cap = (32ul * 148 * kaas::kTraceStamps + 148ul * kaas::kTracePro) * 4;
+  if (bytes > cap) bytes = cap;
   return cudaMemcpy(host, buf, bytes, cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 2;
 }
 #endif

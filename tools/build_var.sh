@@ -10,7 +10,7 @@ cp "$root"/paper_2212_08146_b200/csrc/*.cu "$root"/paper_2212_08146_b200/csrc/*.
 sed -i "$expr" $T/p/c/$file
 cd $T/p/c
 F="-DKAAS_DEV -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo -Xcompiler -fPIC --expt-relaxed-constexpr"
-for f in kaas_abi builtins jacobi cgemm; do nvcc $F -c $f.cu -o $f.o 2>/dev/null & done; wait
+for f in kaas_abi builtins jacobi cgemm runs; do nvcc $F -c $f.cu -o $f.o 2>/dev/null & done; wait
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o "$root/build/var/$name.so" *.o -lcudart
 rm -rf $T
 echo "built build/var/$name.so"
