@@ -891,7 +891,12 @@ k_jacobi_tmem(const __grid_constant__ ChainParams p, float *partials, unsigned *
   constexpr int kTmRR = RR, kTmRS = kTmOther - RR, kTmDep = DEP, kTmBatch = 1;
   static_assert(kTmRS >= 0 && kTmRR + kTmRS <= 16, "one 16-slot reduction set for the non-TMEM rows");
   extern __shared__ __align__(16) float4 acache[];  // [kTmRS][kColC4][kColT]
-  __shared__ float red[kColW][32];
+  // per-warp row partials, double-buffered by sweep parity: a warp may run
+  // into sweep s+1 while warp 0 still reads sweep s's partials (no CTA
+  // barrier at the end of a sweep), and it cannot reach sweep s+2 -- the next
+  // write to this parity -- before every CTA, this one included, has
+  // published sweep s+1, which warp 0 does only after reading them
+  __shared__ float red[2][kColW][32];
   __shared__ uint32_t tmem_base;
   const int n = p.n, n4 = n >> 2;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1198,7 +1203,7 @@ k_jacobi_tmem(const __grid_constant__ ChainParams p, float *partials, unsigned *
       m0 = reduce16(v);
     }
     const float mine = lane < 16 ? m0 : m1;
-    red[warp][lane] = mine;
+    red[s & 1][warp][lane] = mine;
 #ifdef KAAS_DEV
     if (tr) trp[3] = gtimer_lo();  // TMEM rows + reductions done
 #endif
@@ -1207,7 +1212,7 @@ k_jacobi_tmem(const __grid_constant__ ChainParams p, float *partials, unsigned *
     if (warp == 0) {
       float tot = 0.f;
 #pragma unroll
-      for (int w8 = 0; w8 < kColW; ++w8) tot += red[w8][lane];
+      for (int w8 = 0; w8 < kColW; ++w8) tot += red[s & 1][w8][lane];
       float res = 0.f;
       if (my_rl < R) {
         const float xn = (bi - tot) * rdi;
@@ -1235,9 +1240,10 @@ k_jacobi_tmem(const __grid_constant__ ChainParams p, float *partials, unsigned *
       grid_sync_mono(sync + 3, epoch++, p.sync_base);
       if (want_resid && blockIdx.x == 0 && threadIdx.x < 32)
         finish_resid(slot, gridDim.x, p.ptrs[p.idx[s][2] & 0x7f]);
-    } else {
-      __syncthreads();
     }
+    // tagged sweeps end without a CTA barrier: the other warps go straight
+    // to polling the next x while warp 0 reduces and publishes (red is
+    // double-buffered, see above)
   }
 
   KAAS_PRO(5)
