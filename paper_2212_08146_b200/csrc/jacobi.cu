@@ -237,6 +237,7 @@ k_jacobi_sweep(int n, int cov, const float *__restrict__ A, const float *__restr
 constexpr int kChainMaxPtrs = 16;
 constexpr int kTraceStamps = 5;  // dev trace: per sweep and CTA (tools/jtrace.py)
 constexpr int kTracePro = 8;     // dev trace: per-CTA launch-phase stamps after the sweep stamps
+constexpr int kTraceWarpOff = 32 * 148 * kTraceStamps + 148 * kTracePro;  // then [32][148][8] per-warp x arrival
 constexpr int kChainMaxSweeps = 2048;
 
 struct ChainParams {
@@ -1074,6 +1075,8 @@ k_jacobi_tmem(const __grid_constant__ ChainParams p, float *partials, unsigned *
     }
 #ifdef KAAS_DEV
     if (tr) trp[1] = gtimer_lo();  // x arrived
+    if (p.trace != nullptr && s >= 100 && s < 132 && lane == 0)  // every warp's x arrival
+      p.trace[kTraceWarpOff + ((s - 100) * 148 + (blockIdx.x < 148 ? blockIdx.x : 147)) * 8 + warp] = gtimer_lo();
 #endif
     // packed FP32 (FFMA2, fma.rn.f32x2): even and odd columns accumulate in
     // the two halves of one 64-bit register pair, added at the end -- half
@@ -1868,7 +1871,7 @@ int launch_jacobi_chain(cudaStream_t s, int dev, const JacobiChain &c, StreamScr
         if (KAAS_DEV_ENV("KAAS_JACOBI_NOWAIT")) p.tagged = 3;  // dev: compute-only timing
 #endif
         static unsigned *trace_buf = nullptr;  // dev: KAAS_JACOBI_TRACE=1 (tools/jtrace.py)
-        if (KAAS_DEV_ENV("KAAS_JACOBI_TRACE") && !trace_buf) cudaMalloc((void **)&trace_buf, (32 * 148 * kTraceStamps + 148 * kTracePro) * 4);
+        if (KAAS_DEV_ENV("KAAS_JACOBI_TRACE") && !trace_buf) cudaMalloc((void **)&trace_buf, (kTraceWarpOff + 32 * 148 * 8) * 4);
         p.trace = KAAS_DEV_ENV("KAAS_JACOBI_TRACE") ? trace_buf : nullptr;
         jacobi_trace_buffer() = p.trace;
         const char *pe = KAAS_DEV_ENV("KAAS_JACOBI_POLL_NS");  // dev A/B
@@ -1928,7 +1931,7 @@ int launch_jacobi_chain(cudaStream_t s, int dev, const JacobiChain &c, StreamScr
 extern "C" int kaas_dev_jacobi_trace(void *host, unsigned long bytes) {
   unsigned *buf = kaas::jacobi_trace_buffer();
   if (!buf) return 1;
-  const unsigned long cap = (32ul * 148 * kaas::kTraceStamps + 148ul * kaas::kTracePro) * 4;
+  const unsigned long cap = (kaas::kTraceWarpOff + 32ul * 148 * 8) * 4;
   if (bytes > cap) bytes = cap;
   return cudaMemcpy(host, buf, bytes, cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 2;
 }
