@@ -870,6 +870,21 @@ __device__ __forceinline__ float sum2(unsigned long long v) {
   return lo + hi;
 }
 
+// MODE 3 schedule: what step i of the 16 TMEM steps computes besides TMEM
+// row i -- 100 + k = shared-memory row k (rows at steps k * 16 / RS), 1 + r
+// = register row r (the remaining steps in order), 0 = nothing
+__host__ __device__ constexpr int tm_spread(int i, int RR, int RS) {
+  for (int k = 0; k < RS; ++k)
+    if (k * 16 / RS == i) return 100 + k;
+  int r = 0;
+  for (int j = 0; j < i; ++j) {
+    bool sm = false;
+    for (int k = 0; k < RS; ++k) sm = sm || (k * 16 / RS == j);
+    if (!sm) ++r;
+  }
+  return r < RR ? 1 + r : 0;
+}
+
 // RR register rows, kTmOther - RR shared-memory rows.  MODE 0: the register
 // and smem rows first, then the TMEM rows (DEP tcgen05.ld in flight).  MODE 1:
 // interleaved -- step i loads TMEM row i while it computes register/smem row
@@ -1180,12 +1195,31 @@ k_jacobi_tmem(const __grid_constant__ ChainParams p, float *partials, unsigned *
       // interleaved: TMEM row i is in flight while register / smem row i is
       // computed (its LDS issued after the tcgen05.ld, before the wait)
       float v[16], w[16];
+      if (MODE == 3) {
+#pragma unroll
+        for (int k = kTmRR + kTmRS; k < 16; ++k) w[k] = 0.f;
+      }
 #pragma unroll
       for (int i = 0; i < kTmRT; ++i) {
         uint32_t t[16];
         const uint32_t dep = i < kTmDep ? 0u : (__float_as_uint(v[i - kTmDep]) & p.zero);
         KAAS_TMEM_LD16(taddr + dep + 16u * i, t);
-        if (i < kTmRR) {
+        // MODE 3: the shared-memory rows spread evenly over the 16 steps
+        // (one every 16 / RS), the register rows in the steps between, so
+        // the LDS stream (128 B/clk) overlaps the TMEM stream all sweep
+        // long instead of bunching in steps RR .. RR + RS - 1
+        const int sc = MODE == 3 ? tm_spread(i, kTmRR, kTmRS) : 0;
+        if (MODE == 3) {
+          if (sc >= 100) {
+            const int r = sc - 100;
+            float4 a[kColC4];
+#pragma unroll
+            for (int u = 0; u < kColC4; ++u) a[u] = lds4(&acache[(r * kColC4 + u) * kColT + tid]);
+            w[kTmRR + r] = dot(a);
+          } else if (sc > 0) {
+            w[sc - 1] = dot(areg[sc - 1]);
+          }
+        } else if (i < kTmRR) {
           w[i] = MODE == 2 ? dot2(areg[i < kTmRR ? i : 0]) : dot(areg[i < kTmRR ? i : 0]);
         } else if (i < kTmRR + kTmRS) {
           const int r = i - kTmRR;
@@ -1627,14 +1661,16 @@ struct TmVariant {
 };
 #define KAAS_TMV(RR, MODE, DEP) \
   TmVariant { RR, MODE, DEP, (const void *)k_jacobi_tmem<RR, MODE, DEP>, tm_smem<kTmOther - RR>() }
-constexpr int kTmDefRR = 6, kTmDefMode = 1, kTmDefDep = 4;
+constexpr int kTmDefRR = 6, kTmDefMode = 3, kTmDefDep = 5;
 const TmVariant &tm_variant() {
   static const TmVariant def = KAAS_TMV(kTmDefRR, kTmDefMode, kTmDefDep);
 #ifdef KAAS_DEV
   static const TmVariant split = TmVariant{0, 9, 0, (const void *)k_jacobi_split, kSpSmem};
   if (const char *e = KAAS_DEV_ENV("KAAS_JACOBI_TMV"))
     if (e[0] == 's') return split;
-  static const TmVariant vars[] = {KAAS_TMV(6, 0, 4), KAAS_TMV(6, 1, 2), KAAS_TMV(6, 1, 3),
+  static const TmVariant vars[] = {KAAS_TMV(6, 1, 4), KAAS_TMV(6, 3, 4), KAAS_TMV(6, 3, 6),
+                                   KAAS_TMV(5, 3, 5), KAAS_TMV(5, 3, 6), KAAS_TMV(7, 3, 5),
+                                   KAAS_TMV(6, 0, 4), KAAS_TMV(6, 1, 2), KAAS_TMV(6, 1, 3),
                                    KAAS_TMV(6, 2, 3), KAAS_TMV(6, 2, 4), KAAS_TMV(6, 2, 5),
                                    KAAS_TMV(7, 2, 4), KAAS_TMV(8, 2, 4)};
   if (const char *e = KAAS_DEV_ENV("KAAS_JACOBI_TMV")) {
