@@ -12,7 +12,8 @@ import sys
 import numpy as np
 
 os.environ.setdefault("KAAS_B200_LIB", "paper_2212_08146_b200/libkaas_b200_dev.so")
-os.environ.setdefault("KAAS_JACOBI_TRACE", "1")
+if not os.environ.get("JPRO_NOSTAMPS"):
+    os.environ.setdefault("KAAS_JACOBI_TRACE", "1")
 sys.path.insert(0, ".")
 sys.path.insert(0, "tools")
 from kbench import LaunchDims, default_registry, dev_buf, fill_desc, i32, native  # noqa: E402
