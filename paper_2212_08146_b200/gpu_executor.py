@@ -448,7 +448,7 @@ class GpuExecutor:
             self._dfree(ptr, nbytes, self.s_in if stream is None else stream)
 
     # -- prepared operands ------------------------------------------------------
-    # cGEMM's 3xTF32 split of A and split + 4M expansion + transpose of B are
+    # cGEMM's scaled 3xFP16 split of A and split + 4M expansion + transpose of B are
     # pure functions of a const input's bytes: they are kept beside the cache
     # entry, so a warm request skips the preparation pass.  They die with the
     # entry's contents (fill, kernel write, eviction); decisions are unaffected.
