@@ -396,24 +396,44 @@ static bool run_use_enabled() {
   return !(e && e[0] == '0');
 }
 
-static int coop_serialise_begin(int dev, cudaStream_t s) {
-  std::lock_guard<std::mutex> g(g_mu);
-  auto it = g_coop_event.find(dev);
-  if (it == g_coop_event.end()) return 0;
-  KAAS_CUDA(cudaStreamWaitEvent(s, it->second, 0));
-  return 0;
-}
+// Cooperative grids on one device must not overlap (two persistent grids
+// that each need every SM could wait on each other forever).  Launches on
+// one stream are ordered already; when the next cooperative launch comes
+// from a different stream than the last one, it first waits for everything
+// enqueued so far on that stream.  The per-device mutex is held from
+// coop_serialise_begin to coop_serialise_end, so check, launch and hand-over
+// are one step even with several executor threads on a device.
+static std::mutex g_coop_mu;
+static std::unordered_map<int, cudaStream_t> g_coop_last;  // last stream with a cooperative grid, per device
 
-static int coop_serialise_end(int dev, cudaStream_t s) {
-  std::lock_guard<std::mutex> g(g_mu);
+static int coop_serialise_begin(int dev, cudaStream_t s) {
+  g_coop_mu.lock();
+  auto last = g_coop_last.find(dev);
+  if (last == g_coop_last.end() || last->second == s) return 0;
   auto it = g_coop_event.find(dev);
   if (it == g_coop_event.end()) {
     cudaEvent_t ev;
-    KAAS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+      g_coop_mu.unlock();
+      return cuda_fail(e, "cudaEventCreateWithFlags");
+    }
     it = g_coop_event.emplace(dev, ev).first;
   }
-  KAAS_CUDA(cudaEventRecord(it->second, s));
+  cudaError_t e = cudaEventRecord(it->second, last->second);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(s, it->second, 0);
+  if (e != cudaSuccess) {
+    g_coop_mu.unlock();
+    return cuda_fail(e, "cooperative hand-over");
+  }
   return 0;
+}
+
+// rc: the launch's result; always releases the mutex taken by _begin
+static int coop_serialise_end(int dev, cudaStream_t s, int rc = 0) {
+  if (rc == 0) g_coop_last[dev] = s;
+  g_coop_mu.unlock();
+  return rc;
 }
 
 }  // namespace kaas
@@ -541,6 +561,13 @@ int kaas_stream_destroy(uint64_t stream) {
     if (sc->mm_buf) cudaFreeAsync(sc->mm_buf, s);
     if (sc->run_done) cudaFreeAsync(sc->run_done, s);
     cudaStreamSynchronize(s);
+    {
+      // its grids are finished: a later cooperative launch from another
+      // stream must not hand over from this one once it is destroyed
+      std::lock_guard<std::mutex> g(g_coop_mu);
+      for (auto it = g_coop_last.begin(); it != g_coop_last.end();)
+        it = it->second == s ? g_coop_last.erase(it) : std::next(it);
+    }
     if (sc->panel_done) cudaFree(sc->panel_done);
     if (sc->cg_ev_ready) cudaEventDestroy(sc->cg_ev_ready);
     if (sc->cg_ev_done) cudaEventDestroy(sc->cg_ev_done);
@@ -763,8 +790,8 @@ int kaas_launch_batch_memo(int dev, uint64_t stream, const kaas_launch_desc *des
       cudaStream_t s = (cudaStream_t)stream;
       int rc;
       if ((rc = coop_serialise_begin(dev, s))) return rc;
-      rc = launch_jacobi_memo(s, dev, sc);
-      if (rc == 0) return coop_serialise_end(dev, s);
+      rc = coop_serialise_end(dev, s, launch_jacobi_memo(s, dev, sc));
+      if (rc == 0) return 0;
       if (rc != 1) return rc;  // 1: nothing memoised after all -- take the full path
     }
   }
@@ -832,8 +859,8 @@ static int launch_batch_impl(int dev, uint64_t stream, const kaas_launch_desc *d
       int rc;
       if ((rc = coop_serialise_begin(dev, s))) return rc;
       // the whole batch is this one run: the caller's memo key may name it
-      if ((rc = launch_jacobi_chain(s, dev, c, sc, (i == 0 && run == n) ? memo_key : 0))) return rc;
-      if ((rc = coop_serialise_end(dev, s))) return rc;
+      if ((rc = coop_serialise_end(dev, s, launch_jacobi_chain(s, dev, c, sc, (i == 0 && run == n) ? memo_key : 0))))
+        return rc;
       i += run;
       continue;
     }
@@ -860,8 +887,7 @@ static int launch_batch_impl(int dev, uint64_t stream, const kaas_launch_desc *d
         for (int t = 0; t < len; ++t) inv[t] = inv_of(i + t);
         int rc;
         if ((rc = coop_serialise_begin(dev, s))) return rc;
-        if ((rc = launch_builtin_run(s, dev, sc, inv.data(), len))) return rc;
-        if ((rc = coop_serialise_end(dev, s))) return rc;
+        if ((rc = coop_serialise_end(dev, s, launch_builtin_run(s, dev, sc, inv.data(), len)))) return rc;
         i += len;
         continue;
       }

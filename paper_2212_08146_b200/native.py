@@ -11,6 +11,8 @@ import ctypes as C
 import os
 import threading
 
+import numpy as np
+
 from .faults import (
     ArityMismatchError,
     BackendFaultError,
@@ -131,9 +133,10 @@ EXPORTS = {
     "kaas_can_access_peer": [C.c_int, C.c_int, C.POINTER(C.c_int)],
     "kaas_memcpy_p2p_async": [_u64, C.c_int, _u64, C.c_int, _u64, _u64],
     "kaas_launch": [C.c_int, _u64, C.POINTER(LaunchDesc)],
-    "kaas_launch_batch": [C.c_int, _u64, C.POINTER(LaunchDesc), C.c_int],
-    "kaas_launch_batch_memo": [C.c_int, _u64, C.POINTER(LaunchDesc), C.c_int, _u64],
-    "kaas_launch_batch_ex": [C.c_int, _u64, C.POINTER(LaunchDesc), C.c_int,
+    # descriptor tables go in as void*: a ctypes array or a numpy buffer's address
+    "kaas_launch_batch": [C.c_int, _u64, C.c_void_p, C.c_int],
+    "kaas_launch_batch_memo": [C.c_int, _u64, C.c_void_p, C.c_int, _u64],
+    "kaas_launch_batch_ex": [C.c_int, _u64, C.c_void_p, C.c_int,
                              C.POINTER(StreamOut), C.c_int],
 }
 
@@ -369,8 +372,8 @@ def launch_batch(dev: int, stream: Stream, descs, outs=None, memo_key: int = 0) 
     n = len(descs)
     if n == 0:
         return
-    if hasattr(descs, "ctypes") and hasattr(descs, "dtype"):
-        ptr = descs.ctypes.data_as(C.POINTER(LaunchDesc))
+    if isinstance(descs, np.ndarray):
+        ptr = descs.__array_interface__["data"][0]
     else:
         ptr = descs
     if not outs:

@@ -83,6 +83,10 @@ class KaasService:
         # idle (nothing queued, nothing in flight), inline by a synchronous
         # submit() -- saving two thread hand-offs (~40 us) per request; this
         # lock says who owns it
+        self._dispatch = threading.Lock()  # route + enqueue / inline claim, atomically
+        # requests routed to an executor and not yet claimed by its worker
+        # (a dequeued item counts until the worker owns the executor)
+        self._pending = {e.executor_id: 0 for e in self.executors}
         self._owners = {e.executor_id: threading.Lock() for e in self.executors
                         if hasattr(e, "begin")}
         self._threads = [threading.Thread(target=self._worker, args=(e,), daemon=True,
@@ -109,6 +113,8 @@ class KaasService:
             item = q.get()
             if item is None:
                 return
+            with self._dispatch:
+                self._pending[executor.executor_id] -= 1
             req, fut = item
             try:
                 resp = executor.execute(req)
@@ -157,6 +163,9 @@ class KaasService:
                 item = q.get()
                 owner.acquire()
                 held = True
+            if item is not None:
+                with self._dispatch:
+                    self._pending[eid] -= 1
             if item is None:
                 executor.complete()
                 owner.release()
@@ -185,39 +194,51 @@ class KaasService:
     def submit_async(self, req: KaasRequest) -> Future:
         if self._closed:
             raise RuntimeError("service is closed")
-        eid = self.router.route(req)
         fut: Future = Future()
-        fut.executor_id = eid  # placement, for benches and tests
-        self._queues[eid].put((req, fut))
+        with self._dispatch:  # routing order = queue order per executor
+            eid = self.router.route(req)
+            fut.executor_id = eid  # placement, for benches and tests
+            self._pending[eid] += 1
+            self._queues[eid].put((req, fut))
         return fut
 
     def submit(self, req: KaasRequest) -> KaasResponse:
         if self._closed:
             raise RuntimeError("service is closed")
-        eid = self.router.route(req)
-        owner = self._owners.get(eid)
-        q = self._queues[eid]
-        if owner is not None and q.empty() and owner.acquire(blocking=False):
-            try:
+        # Route and claim under one lock, so every executor runs its requests
+        # in routing order (the decision log replays against a FIFO
+        # executor): a request routed later can neither be queued ahead of
+        # this one nor run inline before it.
+        with self._dispatch:
+            eid = self.router.route(req)
+            owner = self._owners.get(eid)
+            q = self._queues[eid]
+            inline = owner is not None and not self._pending[eid] and owner.acquire(blocking=False)
+            if inline:
                 ex = self._by_id[eid]
-                # idle and nobody queued ahead: this request is next in
-                # arrival order either way, so run it on this thread
-                if not ex.inflight and q.empty():
-                    try:
-                        resp = ex.execute(req)
-                    except BaseException as exc:
-                        failed = KaasResponse(req.request_id, Status.make_error("Internal", str(exc)))
-                        self.router.update_digest(eid, failed, req)
-                        raise
-                    self.router.update_digest(eid, resp, req)
-                    self._after(ex)
-                    return resp
-            finally:
-                owner.release()
-        fut: Future = Future()
-        fut.executor_id = eid
-        q.put((req, fut))
-        return fut.result()
+                if ex.inflight:
+                    owner.release()
+                    inline = False
+            if not inline:
+                fut: Future = Future()
+                fut.executor_id = eid
+                self._pending[eid] += 1
+                q.put((req, fut))
+        if not inline:
+            return fut.result()
+        # idle and nobody queued ahead: run it on this thread
+        try:
+            try:
+                resp = ex.execute(req)
+            except BaseException as exc:
+                failed = KaasResponse(req.request_id, Status.make_error("Internal", str(exc)))
+                self.router.update_digest(eid, failed, req)
+                raise
+            self.router.update_digest(eid, resp, req)
+            self._after(ex)
+            return resp
+        finally:
+            owner.release()
 
     def stats(self) -> dict:
         out = {"executors": [e.stats() for e in self.executors],
