@@ -1124,8 +1124,10 @@ int launch_cgemm(cudaStream_t s, int dev, int n, int m, int k, uint64_t cov, con
   shape.cov = cov;
   shape.ksplit = ksplit2 ? 2 : 1;
   shape.kb_chunk = kCgemmChunkKb;
-  shape.group_m = kGroupM;
-  if (const char *ge = KAAS_DEV_ENV("KAAS_CGEMM_GROUPM")) shape.group_m = atoi(ge) > 0 ? atoi(ge) : kGroupM;
+  // raster groups of 16 m-blocks: 8192^3 reads 8.8 GB of DRAM per launch
+  // instead of 11.3 GB at 8 (same time; tools/cg8192_group.sh)
+  shape.group_m = 2 * kGroupM;
+  if (const char *ge = KAAS_DEV_ENV("KAAS_CGEMM_GROUPM")) shape.group_m = atoi(ge) > 0 ? atoi(ge) : 2 * kGroupM;
   if (const char *ce = KAAS_DEV_ENV("KAAS_CGEMM_CHUNK")) shape.kb_chunk = atoi(ce) > 0 ? atoi(ce) : 1 << 30;
   if (ksplit2) KAAS_CUDA(cudaMemsetAsync(C, 0, (size_t)n * m * 8, s));
   return narrow ? launch_gemm2<128>(s, dev, ma, mbm, shape, C, sc, po)
