@@ -68,7 +68,8 @@ constexpr int mm_smem_bytes() {
 template <int TY, int TX, int TM, int TN, int S, int BK, bool AV, bool BT, bool kPdl>
 __device__ __forceinline__ void mm_tile(int n, int m, int k, uint64_t cov, const float *__restrict__ a,
                                         const float *__restrict__ b, float *__restrict__ out, int bm, int bn,
-                                        float *mm_smem, int tid = threadIdx.x, int bar = 0) {
+                                        float *mm_smem, int tid = threadIdx.x, int bar = 0,
+                                        const float *__restrict__ res = nullptr, uint64_t res_cov = 0) {
   constexpr int T = TY * TX, BM = TY * TM, BN = TX * TN, LD = BK + 4;
   constexpr int A_ST = BM * LD, B_ST = BN * LD;
   constexpr int NA4 = (BM * (BK / 4) + T - 1) / T;  // 16-byte A copies per thread
@@ -262,6 +263,34 @@ __device__ __forceinline__ void mm_tile(int n, int m, int k, uint64_t cov, const
   }
   cp_async_wait<0>();
   if (kPdl) mm_pdl_release();
+  if (res != nullptr) {
+    // a following vector_add(out, res -> out) fused into the store:
+    // fl(acc + res[g]), the add's own arithmetic on the value the matmul
+    // would have stored (runs.cu).  All of the tile's residual loads go out
+    // before any is used (one memory round trip, not one per cell).
+    float rv[TM][TN];
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const int r = bm + ty + TY * i, c = bn + tx + TX * j;
+        const uint64_t g = (uint64_t)r * m + c;
+        rv[i][j] = (r < n && c < m && g < res_cov) ? __ldg(res + g) : 0.0f;
+      }
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+      const int r = bm + ty + TY * i;
+      if (r >= n) continue;
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const int c = bn + tx + TX * j;
+        if (c >= m) continue;
+        const uint64_t g = (uint64_t)r * m + c;
+        if (g < cov) out[g] = g < res_cov ? __fadd_rn(acc[i][j], rv[i][j]) : acc[i][j];
+      }
+    }
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < TM; ++i) {
     const int r = bm + ty + TY * i;

@@ -37,7 +37,9 @@ constexpr int kRunMaxTasks = 128;       // per launch (kernel parameter space)
 constexpr uint64_t kEltItem = 2048;    // elements per elementwise work item (2 float4 per thread)
 constexpr uint64_t kCopyItem = 32768;  // bytes per copy work item (8 x 16 bytes per thread)
 
-enum : uint8_t { R_MM = 0, R_ADD, R_SAXPY, R_FILL, R_REDUCE, R_TRANSPOSE, R_COPY };
+// R_ADDC: a fill(v) of a buffer followed by vector_add(x, that buffer -> that
+// buffer) over the same elements, as one pass: out = fl(x + v)
+enum : uint8_t { R_MM = 0, R_ADD, R_SAXPY, R_FILL, R_REDUCE, R_TRANSPOSE, R_COPY, R_ADDC };
 
 struct RunTask {
   uint8_t op, cfg, arrive, vec;  // vec: 16-byte aligned operands (elementwise, copy)
@@ -50,6 +52,8 @@ struct RunTask {
   uint64_t cov;      // elements (elementwise, reduce), cells (matmul), bytes (copy)
   const float *x, *y;
   float *out;
+  const float *res;  // matmul: fused residual add (out = fl(acc + res)) for cells < res_cov, or null
+  uint64_t res_cov;
 };
 
 struct RunParams {
@@ -126,7 +130,7 @@ __device__ __forceinline__ void run_mm(const RunTask &T, unsigned i, float *smem
   float *sm = smem + g * (cfg_smem(c) / 4);
   const int bar = NT == kRunThreads ? 0 : (int)(1 + g);
   mm_tile<c.ty, c.tx, c.tm, c.tn, c.s, c.bk, true, true, false>((int)T.n, (int)T.m, (int)T.k, T.cov, T.x, T.y, T.out,
-                                                                bm, bn, sm, (int)(tid % NT), bar);
+                                                                bm, bn, sm, (int)(tid % NT), bar, T.res, T.res_cov);
 }
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
@@ -136,7 +140,7 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
 }
 
 __device__ __forceinline__ float elt(uint8_t op, float a, float x, float y) {
-  return op == R_ADD ? __fadd_rn(x, y) : op == R_SAXPY ? __fadd_rn(__fmul_rn(a, x), y) : a;
+  return op == R_ADD ? __fadd_rn(x, y) : op == R_SAXPY ? __fadd_rn(__fmul_rn(a, x), y) : op == R_ADDC ? __fadd_rn(x, a) : a;
 }
 
 __global__ void __launch_bounds__(kRunThreads, 1) k_run(const __grid_constant__ RunParams p) {
@@ -183,6 +187,7 @@ __global__ void __launch_bounds__(kRunThreads, 1) k_run(const __grid_constant__ 
           break;
         case R_ADD:
         case R_SAXPY:
+        case R_ADDC:
         case R_FILL: {
           // exact aliasing (out == x or y) is safe: each element is read and
           // then written by the same thread.  All of a thread's loads are
@@ -198,7 +203,7 @@ __global__ void __launch_bounds__(kRunThreads, 1) k_run(const __grid_constant__ 
               const uint64_t q = e0 / 4 + tid + (uint64_t)u * kRunThreads;
               if (q < q1 && T.op != R_FILL) {
                 xv[u] = reinterpret_cast<const float4 *>(T.x)[q];
-                yv[u] = reinterpret_cast<const float4 *>(T.y)[q];
+                yv[u] = T.op == R_ADDC ? xv[u] : reinterpret_cast<const float4 *>(T.y)[q];
               }
             }
 #pragma unroll
@@ -216,7 +221,7 @@ __global__ void __launch_bounds__(kRunThreads, 1) k_run(const __grid_constant__ 
             e = q1 * 4;
           }
           for (e += tid; e < e1; e += kRunThreads)
-            T.out[e] = T.op == R_FILL ? T.a : elt(T.op, T.a, T.x[e], T.y[e]);
+            T.out[e] = T.op == R_FILL ? T.a : elt(T.op, T.a, T.x[e], T.op == R_ADDC ? 0.f : T.y[e]);
           break;
         }
         case R_REDUCE:
@@ -390,17 +395,31 @@ int launch_builtin_run(cudaStream_t s, int dev, StreamScratch *sc, const RunInv 
 
   // ---- pass 2: tasks with their buffer footprints
   struct Foot {
-    uint64_t r[2], w;  // base pointers read / written (0: none)
+    uint64_t r[3], w;  // base pointers read / written (0: none)
   };
   std::vector<RunTask> tasks;
   std::vector<Foot> feet;
   tasks.reserve((size_t)n_inv * 2);
   feet.reserve((size_t)n_inv * 2);
-  auto add = [&](RunTask t, uint64_t r0, uint64_t r1, uint64_t w) {
+  auto add = [&](RunTask t, uint64_t r0, uint64_t r1, uint64_t w, uint64_t r2 = 0) {
     tasks.push_back(t);
-    feet.push_back(Foot{{r0, r1}, w});
+    feet.push_back(Foot{{r0, r1, r2}, w});
   };
   auto aligned = [](uint64_t p) { return (p & 15) == 0; };
+  // Peephole fusions (results bit-identical: the fused task performs the
+  // second invocation's own rounding on exactly the values it would read):
+  //  * fill(F, v) then vector_add(X, F -> F) over the same elements, X != F:
+  //    one pass F = fl(X + v) (R_ADDC)
+  //  * matmul(A, B -> D) then vector_add(D, S -> D) (either operand order)
+  //    over elements the matmul covers, S != D: fl(acc + S) in the matmul's
+  //    store (a ResNet block's residual add)
+  auto fused_add = [&](int i, uint64_t dst) -> const RunInv * {
+    if (i + 1 >= n_inv) return nullptr;
+    const RunInv &a = v[i + 1];
+    if (a.kernel != KAAS_K_VECTOR_ADD || a.cov == 0 || a.ptr[2] != dst) return nullptr;
+    if ((a.ptr[0] == dst) == (a.ptr[1] == dst)) return nullptr;  // exactly one operand is dst
+    return &a;
+  };
   for (int i = 0; i < n_inv; ++i) {
     const RunInv &q = v[i];
     RunTask t{};
@@ -410,6 +429,23 @@ int launch_builtin_run(cudaStream_t s, int dev, StreamScratch *sc, const RunInv 
       case KAAS_K_SAXPY:
       case KAAS_K_FILL: {
         if (q.cov == 0) break;
+        if (q.kernel == KAAS_K_FILL) {
+          const RunInv *a = fused_add(i, q.ptr[0]);
+          if (a != nullptr && a->cov == q.cov) {
+            const uint64_t x = a->ptr[0] == q.ptr[0] ? a->ptr[1] : a->ptr[0];
+            t.op = R_ADDC;
+            t.cov = q.cov;
+            t.a = q.fval;
+            t.out = (float *)q.ptr[0];
+            t.x = (const float *)x;
+            t.y = nullptr;
+            t.vec = aligned((uint64_t)t.out) && aligned(x);
+            t.items = (uint32_t)((q.cov + kEltItem - 1) / kEltItem);
+            add(t, x, 0, (uint64_t)t.out);
+            ++i;  // the add is done
+            break;
+          }
+        }
         const bool fill = q.kernel == KAAS_K_FILL;
         t.op = q.kernel == KAAS_K_VECTOR_ADD ? R_ADD : q.kernel == KAAS_K_SAXPY ? R_SAXPY : R_FILL;
         t.cov = q.cov;
@@ -489,7 +525,15 @@ int launch_builtin_run(cudaStream_t s, int dev, StreamScratch *sc, const RunInv 
           t.per = (uint32_t)pk.per;
           t.items = (uint32_t)((tiles + pk.per - 1) / pk.per);
         }
-        add(t, q.ptr[0], (uint64_t)t.y, (uint64_t)t.out);
+        if (!tmp) {
+          const RunInv *a = fused_add(i, out);
+          if (a != nullptr && a->cov <= q.cov) {
+            t.res = (const float *)(a->ptr[0] == out ? a->ptr[1] : a->ptr[0]);
+            t.res_cov = a->cov;
+          }
+        }
+        add(t, q.ptr[0], (uint64_t)t.y, (uint64_t)t.out, (uint64_t)t.res);
+        if (t.res) ++i;  // the residual add is done
         if (tmp) {
           RunTask c{};
           c.wait = -1;

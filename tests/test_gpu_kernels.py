@@ -335,6 +335,55 @@ def test_resnet_chain_bit_exact(gpu, depth):
     assert canon(store.get(f"{pfx}/out")) == canon(ostore.get(f"{pfx}/out"))
 
 
+def test_run_fusions_edge_cases(gpu):
+    """The invocation-run kernel fuses fill(F, v) + vector_add(X, F -> F) and
+    matmul(.. -> D) + vector_add(D, S -> D); bit-exact against the oracle on
+    the fusable and the look-alike non-fusable patterns: swapped add
+    operands, a residual shorter than the matmul, a residual that is the
+    matmul's own input, an add over more elements than the fill / matmul
+    covered, NaN / -0.0 / Inf operands, and an add writing elsewhere."""
+    ex, store = gpu
+    rng = np.random.default_rng(31)
+    n, m, k = 40, 24, 36
+    a = rng.standard_normal(n * k).astype("<f4")
+    w = rng.standard_normal(k * m).astype("<f4")
+    s_ = rng.standard_normal(n * m).astype("<f4")
+    s_[:5] = [np.nan, -0.0, np.inf, -np.inf, 0.0]
+    a[:3] = [-0.0, np.nan, np.inf]
+    data = {"fu/a": a, "fu/w": w, "fu/s": s_}
+    for key, arr in data.items():
+        store.put(key, arr.tobytes())
+    nm = n * m
+    bufs = (BufferArg("a", 4 * n * k, "input", key="fu/a"),
+            BufferArg("w", 4 * k * m, "input", key="fu/w", is_const=True),
+            BufferArg("s", 4 * nm, "input", key="fu/s"),
+            BufferArg("d", 4 * nm, "output", key="fu/d"),
+            BufferArg("e", 4 * nm, "output", key="fu/e"),
+            BufferArg("f", 4 * nm, "output", key="fu/f"),
+            BufferArg("g", 4 * nm, "output", key="fu/g"),
+            BufferArg("h", 4 * n * k, "output", key="fu/h"))
+    mm = lambda x, out, cov=nm: KernelInvocation("matmul", LaunchDims(grid_x=cov),  # noqa: E731
+                                                 (i32(n), i32(m), i32(k)), (x, "w", out))
+    add = lambda c, x, y, out: KernelInvocation("vector_add", LaunchDims(grid_x=c), (i32(c),), (x, y, out))  # noqa
+    fill = lambda c, v, out: KernelInvocation("fill", LaunchDims(grid_x=c), (i32(c), f32(v)), (out,))  # noqa
+    invs = (
+        mm("a", "d"), add(nm, "d", "s", "d"),            # residual, operand order (D, S)
+        mm("a", "e"), add(nm - 77, "s", "e", "e"),       # swapped, shorter than the matmul
+        mm("a", "f", nm - 50), add(nm, "f", "s", "f"),   # add longer than the matmul's cover: not fused
+        fill(nm, -0.0, "g"), add(nm, "s", "g", "g"),     # fill + add fused (x + -0.0)
+        fill(n * k, 2.5, "h"), add(n * k - 9, "a", "h", "h"),  # different lengths: not fused
+        mm("a", "g"), add(nm, "g", "a", "e"),            # add writes elsewhere: not fused
+        mm("a", "d"), add(nm, "d", "d", "d"),            # add of D with itself: not fused
+    )
+    req = KaasRequest("fu", bufs, invs)
+    _run(ex, req)
+    ostore = DictStore({key: arr.tobytes() for key, arr in data.items()})
+    o = OracleExecutor(1 << 30, ostore).execute(req)
+    assert o.status.ok
+    for key in ("d", "e", "f", "g", "h"):
+        assert canon(store.get(f"fu/{key}")) == canon(ostore.get(f"fu/{key}")), key
+
+
 @pytest.mark.parametrize("n", [2048, 4096])
 def test_jacobi_every_residual_observable(gpu, n):
     """Each sweep writes its own keyed residual (every sweep is a last writer,

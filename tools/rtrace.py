@@ -23,7 +23,7 @@ from paper_2212_08146_b200 import workloads as W  # noqa: E402
 from paper_2212_08146_b200.gpu_executor import ExecutorConfig, GpuExecutor  # noqa: E402
 from paper_2212_08146_b200.hoststore import PinnedStore  # noqa: E402
 
-OPS = ["mm", "add", "saxpy", "fill", "reduce", "transpose", "copy"]
+OPS = ["mm", "add", "saxpy", "fill", "reduce", "transpose", "copy", "addc"]
 
 native.init_device(0)
 store = PinnedStore()
