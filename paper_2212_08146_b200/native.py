@@ -189,6 +189,17 @@ def call(name: str, *args) -> None:
     check(getattr(load(), name)(*args), name)
 
 
+_FAST: dict = {}
+
+
+def _fn(name: str):
+    """The bound C function (hot paths: skip call()'s per-call lookup)."""
+    f = _FAST.get(name)
+    if f is None:
+        f = _FAST[name] = getattr(load(), name)
+    return f
+
+
 def device_count() -> int:
     n = C.c_int(0)
     call("kaas_device_count", C.byref(n))
@@ -253,7 +264,9 @@ class Stream:
         call("kaas_stream_sync", self.handle)
 
     def wait(self, event: "Event") -> None:
-        call("kaas_stream_wait_event", self.handle, event.handle)
+        rc = _fn("kaas_stream_wait_event")(self.handle, event.handle)
+        if rc:
+            check(rc, "kaas_stream_wait_event")
 
     def destroy(self) -> None:
         if self.handle:
@@ -271,7 +284,9 @@ class Event:
         self.handle = h.value
 
     def record(self, stream: Stream) -> "Event":
-        call("kaas_event_record", self.handle, stream.handle)
+        rc = _fn("kaas_event_record")(self.handle, stream.handle)
+        if rc:
+            check(rc, "kaas_event_record")
         return self
 
     def sync(self) -> None:
@@ -327,11 +342,15 @@ def memset_async(ptr: int, value: int, nbytes: int, stream: Stream) -> None:
 
 
 def h2d_async(dst: int, src_addr: int, nbytes: int, stream: Stream) -> None:
-    call("kaas_memcpy_h2d_async", dst, src_addr, nbytes, stream.handle)
+    rc = _fn("kaas_memcpy_h2d_async")(dst, src_addr, nbytes, stream.handle)
+    if rc:
+        check(rc, "kaas_memcpy_h2d_async")
 
 
 def d2h_async(dst_addr: int, src: int, nbytes: int, stream: Stream) -> None:
-    call("kaas_memcpy_d2h_async", dst_addr, src, nbytes, stream.handle)
+    rc = _fn("kaas_memcpy_d2h_async")(dst_addr, src, nbytes, stream.handle)
+    if rc:
+        check(rc, "kaas_memcpy_d2h_async")
 
 
 def d2d_async(dst: int, src: int, nbytes: int, stream: Stream) -> None:
@@ -378,8 +397,9 @@ def launch_batch(dev: int, stream: Stream, descs, outs=None, memo_key: int = 0) 
         ptr = descs
     if not outs:
         if memo_key:
-            check(load().kaas_launch_batch_memo(dev, stream.handle, ptr, n, memo_key),
-                  "kaas_launch_batch_memo")
+            rc = _fn("kaas_launch_batch_memo")(dev, stream.handle, ptr, n, memo_key)
+            if rc:
+                check(rc, "kaas_launch_batch_memo")
         else:
             check(load().kaas_launch_batch(dev, stream.handle, ptr, n), "kaas_launch_batch")
         return

@@ -71,6 +71,16 @@ class _Timed:
 
 
 native.load = lambda: _Timed(_orig_lib)
+if ex.peers is not None:
+    wrap(ex.peers, "borrow", key=lambda a: "peers.borrow")
+    wrap(ex.peers, "publish", key=lambda a: "peers.publish")
+wrap(ex.store, "get_versioned", key=lambda a: "store.get_versioned")
+wrap(GE.native, "h2d_async", key=lambda a: "native.h2d_async")
+wrap(native.Event, "record", key=lambda a: "Event.record")
+wrap(native.Stream, "wait", key=lambda a: "Stream.wait")
+for nm in ("_wait_for_user", "_fence_lends", "_clear_derived", "_alloc", "_derived_slot", "_attach_prepared"):
+    if hasattr(ex, nm):
+        wrap(ex, nm)
 N = 50
 for i in range(N):
     svc.submit(mk(100 + i))
