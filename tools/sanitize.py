@@ -35,6 +35,18 @@ reqs.append(KaasRequest("mm", (
     KernelInvocation("saxpy", LaunchDims(grid_x=96 * 72), (i32(96 * 72), f32(0.5)), ("t", "t", "o")),
     KernelInvocation("vector_add", LaunchDims(grid_x=96 * 72), (i32(96 * 72),), ("o", "t", "t")),
     KernelInvocation("reduce_sum", LaunchDims(), (i32(96 * 72),), ("t", "r")))))
+# invocation-run fusions: fill + add -> one pass, matmul + residual add -> fused store
+store.put("fx", rng.standard_normal(96 * 72, dtype=np.float32).tobytes())
+reqs.append(KaasRequest("fu", (
+    BufferArg("a", 4 * 96 * 200, "input", key="ma", is_const=True),
+    BufferArg("b", 4 * 200 * 72, "input", key="mb", is_const=True),
+    BufferArg("x", 4 * 96 * 72, "input", key="fx"),
+    BufferArg("s", 4 * 96 * 72, "inout", is_ephemeral=True),
+    BufferArg("d", 4 * 96 * 72, "output", key="fd")), (
+    KernelInvocation("fill", LaunchDims(grid_x=96 * 72), (i32(96 * 72), f32(0.0)), ("s",)),
+    KernelInvocation("vector_add", LaunchDims(grid_x=96 * 72), (i32(96 * 72),), ("x", "s", "s")),
+    KernelInvocation("matmul", LaunchDims(grid_x=96 * 72), (i32(96), i32(72), i32(200)), ("a", "b", "d")),
+    KernelInvocation("vector_add", LaunchDims(grid_x=96 * 72), (i32(96 * 72),), ("d", "s", "d")))))
 for rep in range(2):  # second pass: const hits, prepared operands, memoised chain
     for r in reqs:
         resp = ex.execute(r)
