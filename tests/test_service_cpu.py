@@ -134,3 +134,95 @@ def test_bench_cli_validates_like_the_reference(capsys):
     from paper_2212_08146_b200.benchlib import bench_main
     assert bench_main(["run", "--workload", "mixed", "--requests", "0"]) == 2
     assert "invalid workload" in capsys.readouterr().err
+
+
+class _FakePipelined:
+    """GPU-executor-shaped stand-in (begin / complete / inflight / execute):
+    records the order in which requests reach it, and sleeps a little so the
+    pool's inline and worker paths interleave."""
+
+    def __init__(self, eid):
+        import threading
+        self.executor_id = eid
+        self.order = []
+        self._inflight = {}
+        self._seq = 0
+        self._lock = threading.Lock()
+        self.on_complete = None
+        self.poisoned = None
+
+    @property
+    def inflight(self):
+        return len(self._inflight)
+
+    def _resp(self, req):
+        from paper_2212_08146_b200.api import KaasResponse, Status
+        return KaasResponse(req.request_id, Status.make_ok())
+
+    def execute(self, req):
+        import time
+        with self._lock:
+            self.order.append(req.request_id)
+        time.sleep(0.0003)
+        return self._resp(req)
+
+    def begin(self, req):
+        from types import SimpleNamespace
+        with self._lock:
+            self.order.append(req.request_id)
+        self._seq += 1
+        rec = SimpleNamespace(seq=self._seq, response=self._resp(req))
+        self._inflight[self._seq] = rec
+        return rec
+
+    def complete(self, through=None, block=True):
+        import time
+        done = 0
+        for seq in sorted(self._inflight):
+            if through is not None and seq > through:
+                break
+            time.sleep(0.0002)
+            rec = self._inflight.pop(seq)
+            if self.on_complete is not None:
+                self.on_complete(rec, rec.response)
+            done += 1
+        return done
+
+
+@pytest.mark.parametrize("policy", ["rr", "affinity:8", "random:7", "exclusive"])
+def test_each_executor_runs_requests_in_routing_order(policy):
+    """Many client threads through submit(): every executor sees its requests
+    in the order the router placed them (the inline fast path may not
+    overtake a request routed earlier), so a decision log replays against a
+    FIFO executor (tests/test_gpu_service.py)."""
+    import threading
+    from paper_2212_08146_b200 import workloads as W
+
+    reqs = [W.cgemm_request(f"t{i % 16}/r{i}", 8, f"k/A{i % 5}", f"k/B{i % 3}", f"k/C{i % 7}")
+            for i in range(600)]
+    svc = KaasService(None, n_executors=4, policy=policy, executor_factory=_FakePipelined,
+                      log_decisions=True)
+    try:
+        it = iter(range(len(reqs)))
+        lock = threading.Lock()
+
+        def client():
+            while True:
+                with lock:
+                    i = next(it, None)
+                if i is None:
+                    return
+                assert svc.submit(reqs[i]).status.ok
+
+        threads = [threading.Thread(target=client) for _ in range(16)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        decisions = list(svc.router.decisions)
+    finally:
+        svc.close()
+    assert len(decisions) == len(reqs)
+    for e in svc.executors:
+        routed = [rid for rid, chosen, _ in decisions if chosen == e.executor_id]
+        assert e.order == routed
