@@ -309,11 +309,17 @@ struct GemmShape {
                      // exactly, so the result is deterministic)
   int kb_chunk;      // k-blocks per fresh-accumulator chunk (see k_cgemm_fused4)
   int group_m;       // m-blocks per raster group
+  int panel_m;       // m-blocks (of 128 rows) per progressive write-back panel
   const uint32_t *amax;  // [M] max-bits of A's rows -> row scale 2^e (cg_exp)
   const uint32_t *bmax;  // [N/2] max-bits of B's complex columns -> column scale
 };
 
-constexpr int kGroupM = 8;  // m-blocks per write-back panel (and the default raster group)
+constexpr int kGroupM = 8;  // default raster group, in m-blocks
+// m-blocks per progressive write-back panel: a warm 8192^3 request is bound by
+// its 512 MiB PCIe write-back, which starts when the first panel is done --
+// 2-block panels start it sooner than 8 (11.85 vs 12.0 ms per request,
+// tools/cgwarm_ab.sh; raster groups of 16 were 13.8-14.1 ms)
+constexpr int kPanelM = 2;
 
 __device__ __forceinline__ void tile_coords(const GemmShape &s, int t, int &mb, int &nb) {
   // group m-blocks together so concurrently running CTAs share B tiles in L2
@@ -579,7 +585,7 @@ k_cgemm_fused4(const __grid_constant__ CUtensorMap map_a, const __grid_constant_
         asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
         if (warp == 2 && lane == 0) {
           __threadfence_system();
-          atomicAdd(&panel_done[mb / kGroupM], 1u);
+          atomicAdd(&panel_done[mb / s.panel_m], 1u);
         }
       }
     }
@@ -820,7 +826,7 @@ k_cgemm_pair(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ 
         const int mb128 = mb * 2 + (int)rank;
         if (warp == 2 && lane == 0 && mb128 * BM < s.M) {
           __threadfence_system();
-          atomicAdd(&panel_done[mb128 / kGroupM], 1u);
+          atomicAdd(&panel_done[mb128 / s.panel_m], 1u);
         }
       }
     }
@@ -899,7 +905,8 @@ int launch_gemm2(cudaStream_t s, int dev, const CUtensorMap &ma, const CUtensorM
   const int units = shape.num_m * shape.num_n * shape.ksplit;
   int grid = device_props(dev).sm_count;
   if (grid > units) grid = units;
-  const int npanels = (shape.num_m + kGroupM - 1) / kGroupM;
+  const int PM = shape.panel_m;
+  const int npanels = (shape.num_m + PM - 1) / PM;
   WaitValue32Fn waitv = get_wait_value();
   const bool progressive = po != nullptr && waitv != nullptr && npanels > 1 &&
                            npanels <= kMaxPanels && sc->panel_done != nullptr;
@@ -922,7 +929,7 @@ int launch_gemm2(cudaStream_t s, int dev, const CUtensorMap &ma, const CUtensorM
   uint64_t copied = 0;
   if (progressive) {
     for (int p = 0; p < npanels; ++p) {
-      const int mb0 = p * kGroupM, mbs = min(kGroupM, shape.num_m - mb0);
+      const int mb0 = p * PM, mbs = min(PM, shape.num_m - mb0);
       const int row0 = mb0 * BM, row1 = min(shape.M, (mb0 + mbs) * BM);
       const unsigned want = (unsigned)(mbs * shape.num_n * shape.ksplit);
       CUresult r = waitv((CUstream)po->out_stream, (CUdeviceptr)(sc->panel_done + p), want,
@@ -958,7 +965,8 @@ int launch_pair(cudaStream_t s, int dev, const CUtensorMap &ma, const CUtensorMa
   int pairs = device_props(dev).sm_count / 2;
   if (pairs > tiles) pairs = tiles;
   const int num_m128 = (shape.M + BM - 1) / BM;
-  const int npanels = (num_m128 + kGroupM - 1) / kGroupM;
+  const int PM = shape.panel_m;
+  const int npanels = (num_m128 + PM - 1) / PM;
   WaitValue32Fn waitv = get_wait_value();
   const bool progressive = po != nullptr && waitv != nullptr && npanels > 1 && npanels <= kMaxPanels &&
                            sc->panel_done != nullptr;
@@ -980,7 +988,7 @@ int launch_pair(cudaStream_t s, int dev, const CUtensorMap &ma, const CUtensorMa
   uint64_t copied = 0;
   if (progressive) {
     for (int p = 0; p < npanels; ++p) {
-      const int mb0 = p * kGroupM, mbs = min(kGroupM, num_m128 - mb0);
+      const int mb0 = p * PM, mbs = min(PM, num_m128 - mb0);
       const int row0 = mb0 * BM, row1 = min(shape.M, (mb0 + mbs) * BM);
       const unsigned want = (unsigned)(mbs * shape.num_n);
       CUresult r = waitv((CUstream)po->out_stream, (CUdeviceptr)(sc->panel_done + p), want,
@@ -1105,6 +1113,8 @@ int launch_cgemm(cudaStream_t s, int dev, int n, int m, int k, uint64_t cov, con
     ps.ksplit = 1;
     ps.kb_chunk = kCgemmChunkKb;
     ps.group_m = kGroupM / 2;
+    ps.panel_m = kPanelM;
+    if (const char *pe2 = KAAS_DEV_ENV("KAAS_CGEMM_PANELM")) ps.panel_m = atoi(pe2) > 0 ? atoi(pe2) : kPanelM;
     if (const char *ge = KAAS_DEV_ENV("KAAS_CGEMM_GROUPM")) ps.group_m = atoi(ge) > 0 ? atoi(ge) : kGroupM / 2;
     if (const char *ce = KAAS_DEV_ENV("KAAS_CGEMM_CHUNK")) ps.kb_chunk = atoi(ce) > 0 ? atoi(ce) : 1 << 30;
     return launch_pair(s, dev, ma, mbm, ps, C, sc, po);
@@ -1124,10 +1134,10 @@ int launch_cgemm(cudaStream_t s, int dev, int n, int m, int k, uint64_t cov, con
   shape.cov = cov;
   shape.ksplit = ksplit2 ? 2 : 1;
   shape.kb_chunk = kCgemmChunkKb;
-  // raster groups of 16 m-blocks: 8192^3 reads 8.8 GB of DRAM per launch
-  // instead of 11.3 GB at 8 (same time; tools/cg8192_group.sh)
-  shape.group_m = 2 * kGroupM;
-  if (const char *ge = KAAS_DEV_ENV("KAAS_CGEMM_GROUPM")) shape.group_m = atoi(ge) > 0 ? atoi(ge) : 2 * kGroupM;
+  shape.group_m = kGroupM;
+  if (const char *ge = KAAS_DEV_ENV("KAAS_CGEMM_GROUPM")) shape.group_m = atoi(ge) > 0 ? atoi(ge) : kGroupM;
+  shape.panel_m = kPanelM;
+  if (const char *pe2 = KAAS_DEV_ENV("KAAS_CGEMM_PANELM")) shape.panel_m = atoi(pe2) > 0 ? atoi(pe2) : kPanelM;
   if (const char *ce = KAAS_DEV_ENV("KAAS_CGEMM_CHUNK")) shape.kb_chunk = atoi(ce) > 0 ? atoi(ce) : 1 << 30;
   if (ksplit2) KAAS_CUDA(cudaMemsetAsync(C, 0, (size_t)n * m * 8, s));
   return narrow ? launch_gemm2<128>(s, dev, ma, mbm, shape, C, sc, po)
