@@ -809,8 +809,11 @@ def init_dist():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         # the process group carries only a barrier and one float (max time):
         # NCCL on a B200 box, gloo when asked (e.g. several ranks on one GPU)
+        ndev = torch.cuda.device_count() if torch.cuda.is_available() else 0
+        # NCCL needs one GPU per rank; more ranks than GPUs (a 1-GPU dev box)
+        # share the devices and talk over gloo
         backend = os.environ.get("KAAS_DIST_BACKEND") or (
-            "nccl" if torch.cuda.is_available() else "gloo")
+            "nccl" if ndev >= int(os.environ.get("LOCAL_WORLD_SIZE", world)) else "gloo")
         if backend == "nccl":
             torch.cuda.set_device(local)
         td.init_process_group(backend=backend)
