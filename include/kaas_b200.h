@@ -193,6 +193,14 @@ int kaas_launch_batch_ex(int dev, uint64_t stream, const kaas_launch_desc *descs
  * parameters without re-parsing the descriptors (key 0 = no memo). */
 int kaas_launch_batch_memo(int dev, uint64_t stream, const kaas_launch_desc *descs, int n,
                            uint64_t memo_key);
+/* kaas_launch_batch_memo with the request's stream plumbing in the same
+ * crossing (the executor's launch step, executor.py:356-369): when
+ * join_event != 0 it is recorded on join_stream (the fills' copy stream) and
+ * `stream` waits for it; ev_start / ev_end (0 = none) are recorded on
+ * `stream` right before / after the launches (the request's kernel span). */
+int kaas_launch_batch_timed(int dev, uint64_t stream, const kaas_launch_desc *descs, int n,
+                            uint64_t memo_key, uint64_t join_stream, uint64_t join_event,
+                            uint64_t ev_start, uint64_t ev_end);
 
 #ifdef __cplusplus
 }

@@ -798,6 +798,20 @@ int kaas_launch_batch_memo(int dev, uint64_t stream, const kaas_launch_desc *des
   return launch_batch_impl(dev, stream, descs, n, nullptr, 0, memo_key);
 }
 
+int kaas_launch_batch_timed(int dev, uint64_t stream, const kaas_launch_desc *descs, int n,
+                            uint64_t memo_key, uint64_t join_stream, uint64_t join_event,
+                            uint64_t ev_start, uint64_t ev_end) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (join_event) {
+    KAAS_CUDA(cudaEventRecord((cudaEvent_t)join_event, (cudaStream_t)join_stream));
+    KAAS_CUDA(cudaStreamWaitEvent(s, (cudaEvent_t)join_event, 0));
+  }
+  if (ev_start) KAAS_CUDA(cudaEventRecord((cudaEvent_t)ev_start, s));
+  if (const int rc = kaas_launch_batch_memo(dev, stream, descs, n, memo_key)) return rc;
+  if (ev_end) KAAS_CUDA(cudaEventRecord((cudaEvent_t)ev_end, s));
+  return 0;
+}
+
 static int launch_batch_impl(int dev, uint64_t stream, const kaas_launch_desc *descs, int n,
                              const kaas_stream_out *outs, int n_outs, uint64_t memo_key) {
   if (n < 0 || (n > 0 && !descs)) return fail(KAAS_E_INVALID, "null launch descriptors");

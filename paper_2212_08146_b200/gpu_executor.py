@@ -973,7 +973,11 @@ class GpuExecutor:
         if plan.fail_at is not None:
             raise plan.fail_exc
         ev = rec.events
-        if self.time_requests and rec.has_fills:
+        timed = self.time_requests
+        # the usual launch (no stream-outs): the fills' join, the kernel span
+        # and the launch in one C crossing (kaas_launch_batch_timed)
+        one_call = bool(plan.n) and not plan.stream_outs
+        if timed and rec.has_fills and not one_call:
             ev[5].record(self.s_in)
         if plan.n:
             ptrs = tuple(resolved[nm].ptr for nm in plan.names)
@@ -994,6 +998,17 @@ class GpuExecutor:
                     plan.last_ptrs, plan.last_descs = ptrs, descs
                     plan.last_key = memo_key = next(_DESC_KEYS)
             filled = self._attach_prepared(plan, descs, resolved) if plan.prepared else ()
+            if one_call:
+                # s_exec waits for everything enqueued on s_in so far (the fills)
+                native.launch_batch_timed(self.device, self.s_exec, descs, memo_key, self.s_in,
+                                          ev[5] if timed and rec.has_fills else self._ev_fill,
+                                          ev[2] if timed else None, ev[3] if timed else None)
+                self.dev_stats.resolve()  # earlier requests' spans, while this one runs
+                for slot in filled:
+                    slot[2] = True  # later launches on s_exec are ordered after the fill
+                rec.has_kernels = True
+                self.dev_stats.kernel_launches += plan.n
+                return
             if self.time_requests and rec.has_fills:
                 self.s_exec.wait(ev[5])  # recorded on s_in just above: the fills' end
             else:

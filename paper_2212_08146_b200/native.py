@@ -136,6 +136,7 @@ EXPORTS = {
     # descriptor tables go in as void*: a ctypes array or a numpy buffer's address
     "kaas_launch_batch": [C.c_int, _u64, C.c_void_p, C.c_int],
     "kaas_launch_batch_memo": [C.c_int, _u64, C.c_void_p, C.c_int, _u64],
+    "kaas_launch_batch_timed": [C.c_int, _u64, C.c_void_p, C.c_int, _u64, _u64, _u64, _u64, _u64],
     "kaas_launch_batch_ex": [C.c_int, _u64, C.c_void_p, C.c_int,
                              C.POINTER(StreamOut), C.c_int],
 }
@@ -379,6 +380,22 @@ def host_alloc(nbytes: int) -> int:
 
 def host_free(addr: int) -> None:
     call("kaas_host_free", C.c_void_p(addr))
+
+
+def launch_batch_timed(dev: int, stream: Stream, descs, memo_key: int = 0, join_stream: Stream | None = None,
+                       join_event: Event | None = None, ev_start: Event | None = None,
+                       ev_end: Event | None = None) -> None:
+    """launch_batch (no stream-outs) with the join / kernel-span events in the
+    same crossing (kaas_launch_batch_timed)."""
+    n = len(descs)
+    ptr = descs.__array_interface__["data"][0] if isinstance(descs, np.ndarray) else descs
+    rc = _fn("kaas_launch_batch_timed")(dev, stream.handle, ptr, n, memo_key,
+                                        join_stream.handle if join_event is not None else 0,
+                                        join_event.handle if join_event is not None else 0,
+                                        ev_start.handle if ev_start is not None else 0,
+                                        ev_end.handle if ev_end is not None else 0)
+    if rc:
+        check(rc, "kaas_launch_batch_timed")
 
 
 def launch_batch(dev: int, stream: Stream, descs, outs=None, memo_key: int = 0) -> None:
