@@ -40,6 +40,8 @@ lib = native.load()
 times = []
 for rep in range(int(os.environ.get("JPRO_REPS", "4"))):
     native.memset_async(flush, rep, 256 << 20, s)
+    if os.environ.get("JPRO_IDLE"):  # the GPU idles before the launch (as in a request)
+        s.sync()
     e0, e1 = native.Event(0, True), native.Event(0, True)
     e0.record(s)
     native.launch_batch(0, s, descs)
