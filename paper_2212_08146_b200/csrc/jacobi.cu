@@ -1079,10 +1079,11 @@ k_jacobi_tmem(const __grid_constant__ ChainParams p, float *partials, unsigned *
           if (pending & (1u << u)) q[u] = ld_relaxed_u64x4(src + 4 * (cbase + 32 * u));
 #pragma unroll
         for (int u = 0; u < kColC4; ++u) {
-          if ((pending & (1u << u)) && (unsigned)(q[u].w[0] >> 32) == want &&
-              (unsigned)(q[u].w[1] >> 32) == want && (unsigned)(q[u].w[2] >> 32) == want &&
-              (unsigned)(q[u].w[3] >> 32) == want)
-            pending &= ~(1u << u);
+          // all four tags == want, as one OR of XORs (the check runs once
+          // more after the last word lands -- it is on the critical path)
+          const unsigned d = ((unsigned)(q[u].w[0] >> 32) ^ want) | ((unsigned)(q[u].w[1] >> 32) ^ want) |
+                             ((unsigned)(q[u].w[2] >> 32) ^ want) | ((unsigned)(q[u].w[3] >> 32) ^ want);
+          if ((pending & (1u << u)) && d == 0u) pending &= ~(1u << u);
         }
       }
 #pragma unroll
@@ -1253,7 +1254,13 @@ k_jacobi_tmem(const __grid_constant__ ChainParams p, float *partials, unsigned *
     if (warp == 0) {
       float tot = 0.f;
 #pragma unroll
-      for (int w8 = 0; w8 < kColW; ++w8) tot += red[s & 1][w8][lane];
+      {
+        // the 8 warps' partials as a tree (3 dependent adds, not 8; fixed
+        // order, so still deterministic)
+        static_assert(kColW == 8, "tree over 8 warps");
+        const float *rr = &red[s & 1][0][lane];
+        tot = ((rr[0] + rr[32]) + (rr[64] + rr[96])) + ((rr[128] + rr[160]) + (rr[192] + rr[224]));
+      }
       float res = 0.f;
       if (my_rl < R) {
         const float xn = (bi - tot) * rdi;
