@@ -1065,7 +1065,8 @@ k_jacobi_tmem(const __grid_constant__ ChainParams p, float *partials, unsigned *
         if (cbase + 32 * u < n4) pending |= 1u << u;
       unsigned spins = 0;
       while (pending) {
-        if (++spins > (1u << 22)) __trap();  // a lost producer: fail loudly, never hang
+        // a lost producer: fail loudly, never hang (checked every 256 polls)
+        if ((++spins & 0xffu) == 0u && spins > (1u << 22)) __trap();
 #ifdef KAAS_DEV
         if (p.tagged == 3 && spins > 1) break;  // dev: no waiting (compute-only timing; wrong results)
         if (spins > 1 && p.poll_ns) {  // dev A/B: busy back-off (cycles) between polls
@@ -1083,7 +1084,9 @@ k_jacobi_tmem(const __grid_constant__ ChainParams p, float *partials, unsigned *
           // more after the last word lands -- it is on the critical path)
           const unsigned d = ((unsigned)(q[u].w[0] >> 32) ^ want) | ((unsigned)(q[u].w[1] >> 32) ^ want) |
                              ((unsigned)(q[u].w[2] >> 32) ^ want) | ((unsigned)(q[u].w[3] >> 32) ^ want);
-          if ((pending & (1u << u)) && d == 0u) pending &= ~(1u << u);
+          // branch-free: a chunk done earlier (or out of range) only clears
+          // a bit that is already clear
+          pending &= d == 0u ? ~(1u << u) : ~0u;
         }
       }
 #pragma unroll
