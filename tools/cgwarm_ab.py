@@ -9,6 +9,7 @@ import bench  # noqa: E402
 from paper_2212_08146_b200 import native  # noqa: E402
 
 native.init_device(0)
-r = bench.measure_cgemm(8192, 12, 0, False)
-print(json.dumps({"group": os.environ.get("KAAS_CGEMM_GROUPM", "def"), "panel": os.environ.get("KAAS_CGEMM_PANELM", "def"),
+N = int(os.environ.get("CG_N", "8192"))
+r = bench.measure_cgemm(N, 12 if N >= 4096 else 200, 0, False)
+print(json.dumps({"n": N, "group": os.environ.get("KAAS_CGEMM_GROUPM", "def"), "panel": os.environ.get("KAAS_CGEMM_PANELM", "def"),
                   **{k: round(r[k], 3) for k in ("warm_req_per_s", "warm_p50_ms", "warm_device_ms", "kernel_ms")}}))
