@@ -845,9 +845,11 @@ class GpuExecutor:
         try:
             rec.events = ev = self._events()
             if self.time_requests:
+                # the request's first device op: its fills follow on s_in, its
+                # kernels wait on the fills' join (recorded on s_in later) and
+                # its flush waits on the kernels, so every span is ordered
+                # after this event without further cross-stream waits
                 ev[0].record(self.s_in)
-                self.s_exec.wait(ev[0])
-                self.s_out.wait(ev[0])
             by_name = req.by_name
             for nm in plan.names:
                 arg = by_name[nm]
