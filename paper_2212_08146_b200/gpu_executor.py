@@ -1067,7 +1067,23 @@ class GpuExecutor:
         (executor.py:371-380): the D2H copies are enqueued now, the puts
         happen in ``complete``; virtual time, IoStats and the clean marks are
         final now, as the next request's decisions depend on them."""
-        if self.time_requests and rec.has_kernels:
+        # Alone on the executor (nothing else in flight), the copies go on the
+        # exec stream right behind the kernels: no cross-stream hand-over
+        # between the last kernel and the write-back (a warm Jacobi request's
+        # kernel-end -> flush-done tail was 13 us).  With requests pipelined,
+        # they go on the copy-out stream so the next request's kernels
+        # overlap them.
+        alone = not rec.streamed and len(self._inflight) == 0
+        fs = self.s_exec if alone else self.s_out
+        if rec.has_fills and not rec.has_kernels:
+            # no kernel joined the fills: the request's end event must not
+            # come before them (complete() releases the fills' host sources)
+            join = rec.events[5] if self.time_requests else self._ev_fill
+            join.record(self.s_in)
+            fs.wait(join)
+        if alone:
+            pass
+        elif self.time_requests and rec.has_kernels:
             self.s_out.wait(rec.events[3])  # _launch recorded it on s_exec after the batch, just now
         else:
             self._ev_exec.record(self.s_exec)
@@ -1080,13 +1096,13 @@ class GpuExecutor:
                 blob = rec.streamed.get(nm)
                 if blob is None:
                     blob = PinnedBlob(buf.size)
-                    native.d2h_async(blob.addr, buf.ptr, buf.size, self.s_out)
+                    native.d2h_async(blob.addr, buf.ptr, buf.size, fs)
                 rec.pending.append((buf.key, blob, buf.size, buf))
                 self.clock.advance_ns(self.backend.timing.flush_time_ns(buf.size))
                 stats.store_puts += 1
                 stats.bytes_flushed += buf.size
                 buf.dirty = False
-        rec.events[1].record(self.s_out)
+        rec.events[1].record(fs)
 
     def _check_poison(self) -> None:
         if self.poisoned is None:
