@@ -197,10 +197,16 @@ int kaas_launch_batch_memo(int dev, uint64_t stream, const kaas_launch_desc *des
  * crossing (the executor's launch step, executor.py:356-369): when
  * join_event != 0 it is recorded on join_stream (the fills' copy stream) and
  * `stream` waits for it; ev_start / ev_end (0 = none) are recorded on
- * `stream` right before / after the launches (the request's kernel span). */
+ * `stream` right before / after the launches (the request's kernel span).
+ * `outs` (as kaas_launch_batch_ex): the final contents of those buffers are
+ * in host_dst once ev_end has completed -- a fused Jacobi chain writes its
+ * last sweep's x_out / resid there from the kernel, anything else is copied
+ * on the spec's out_stream after the batch (pass `stream` itself as the
+ * out_stream so that ev_end covers those copies). */
 int kaas_launch_batch_timed(int dev, uint64_t stream, const kaas_launch_desc *descs, int n,
                             uint64_t memo_key, uint64_t join_stream, uint64_t join_event,
-                            uint64_t ev_start, uint64_t ev_end);
+                            uint64_t ev_start, uint64_t ev_end, const kaas_stream_out *outs,
+                            int n_outs);
 
 #ifdef __cplusplus
 }

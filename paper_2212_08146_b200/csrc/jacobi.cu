@@ -200,13 +200,17 @@ __device__ __forceinline__ void band(int cov, int &r0, int &r1) {
 }
 
 // Final cross-CTA sum by one warp, fixed order -> deterministic.
-__device__ __forceinline__ void finish_resid(const float *partials, int nparts, float *resid) {
+__device__ __forceinline__ void finish_resid(const float *partials, int nparts, float *resid,
+                                             float *resid2 = nullptr) {
   const int lane = threadIdx.x & 31;
   double acc = 0.0;
   for (int p = lane; p < nparts; p += 32) acc += (double)__ldcg(partials + p);
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-  if (lane == 0) *resid = (float)acc;
+  if (lane == 0) {
+    *resid = (float)acc;
+    if (resid2 != nullptr) *resid2 = (float)acc;
+  }
 }
 
 template <int KC>
@@ -256,6 +260,9 @@ struct ChainParams {
   unsigned zero;  // always 0: an opaque value ptxas cannot fold (k_jacobi_tmem)
   unsigned sync_base;  // the grid-barrier counter's value when this launch starts
   unsigned *trace;  // dev: [32 sweeps][148 CTAs][3] globaltimer_lo stamps, or nullptr
+  // k_jacobi_tmem: the last sweep also writes x_out / resid here (pinned
+  // host memory; the request's write-back without a copy), or nullptr
+  float *wb_x, *wb_r;
 };
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
@@ -1272,6 +1279,7 @@ k_jacobi_tmem(const __grid_constant__ ChainParams p, float *partials, unsigned *
           st_relaxed_u64(p.xt + (size_t)((s + 1) & 1) * kJacTaggedMaxN + i,
                          tagged_word(xn, p.tag0 + (unsigned)s + 1));
         x_out[i] = xn;
+        if (p.wb_x != nullptr && s == p.sweeps - 1) p.wb_x[i] = xn;  // the request's write-back
         res = fabsf(xn - (from_tags ? xprev : __ldcg(x_in + i)));
         xprev = xn;
       }
@@ -1288,7 +1296,7 @@ k_jacobi_tmem(const __grid_constant__ ChainParams p, float *partials, unsigned *
     if (want_resid || !p.tagged) {
       grid_sync_mono(sync + 3, epoch++, p.sync_base);
       if (want_resid && blockIdx.x == 0 && threadIdx.x < 32)
-        finish_resid(slot, gridDim.x, p.ptrs[p.idx[s][2] & 0x7f]);
+        finish_resid(slot, gridDim.x, p.ptrs[p.idx[s][2] & 0x7f], s == p.sweeps - 1 ? p.wb_r : nullptr);
     }
     // tagged sweeps end without a CTA barrier: the other warps go straight
     // to polling the next x while warp 0 reduces and publishes (red is
@@ -1791,6 +1799,7 @@ struct JacobiMemo {
   const void *fn;
   int blocks;
   size_t smem;
+  bool wb_ok;  // the memoised kernel writes back the last sweep (k_jacobi_tmem)
 };
 
 void free_jacobi_memo(StreamScratch *sc) {
@@ -1834,10 +1843,13 @@ static int launch_tagged_chain(cudaStream_t s, StreamScratch *sc, ChainParams &p
   return 0;
 }
 
-int launch_jacobi_memo(cudaStream_t s, int dev, StreamScratch *sc) {
+int launch_jacobi_memo(cudaStream_t s, int dev, StreamScratch *sc, float *wb_x, float *wb_r) {
   (void)dev;
   auto *m = static_cast<JacobiMemo *>(sc->jac_memo);
   if (!m) return 1;
+  if ((wb_x || wb_r) && !m->wb_ok) return 1;  // its kernel cannot write back: the full path copies
+  m->p.wb_x = wb_x;
+  m->p.wb_r = wb_r;
   return launch_tagged_chain(s, sc, m->p, m->fn, m->blocks, m->smem);
 }
 
@@ -1904,6 +1916,7 @@ int launch_jacobi_chain(cudaStream_t s, int dev, const JacobiChain &c, StreamScr
     p.tagged = 0;
     p.zero = 0;
     p.trace = nullptr;
+    p.wb_x = p.wb_r = nullptr;
     if (use_rows && use_cols_kernel(dev, c.n, c.cov, blocks)) {
       // a pure ping-pong run (each sweep reads the previous one's output, no
       // in-place sweep) publishes x through tags instead of grid barriers
@@ -1938,8 +1951,13 @@ int launch_jacobi_chain(cudaStream_t s, int dev, const JacobiChain &c, StreamScr
         attr_done[tm].fetch_or(1ull << (dev & 63));
       }
       if (p.tagged) {
+        // only the TMEM kernel writes the last sweep back to host memory
+        const bool wb = tm && done + cnt == c.sweeps && (c.wb_x || c.wb_r);
+        p.wb_x = wb ? c.wb_x : nullptr;
+        p.wb_r = wb ? c.wb_r : nullptr;
         int rc = launch_tagged_chain(s, sc, p, cfn, blocks, csmem);
         if (rc) return rc;
+        if (wb && c.wb_done) *c.wb_done = true;
         if (memo_key && done == 0 && cnt == c.sweeps) {  // the whole run in one launch
           auto *m = static_cast<JacobiMemo *>(sc->jac_memo);
           if (!m) sc->jac_memo = m = new JacobiMemo();
@@ -1947,6 +1965,7 @@ int launch_jacobi_chain(cudaStream_t s, int dev, const JacobiChain &c, StreamScr
           m->fn = cfn;
           m->blocks = blocks;
           m->smem = csmem;
+          m->wb_ok = tm;
           sc->jac_memo_key = memo_key;
         }
         done += cnt;

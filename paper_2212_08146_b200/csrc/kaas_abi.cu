@@ -800,14 +800,37 @@ int kaas_launch_batch_memo(int dev, uint64_t stream, const kaas_launch_desc *des
 
 int kaas_launch_batch_timed(int dev, uint64_t stream, const kaas_launch_desc *descs, int n,
                             uint64_t memo_key, uint64_t join_stream, uint64_t join_event,
-                            uint64_t ev_start, uint64_t ev_end) {
+                            uint64_t ev_start, uint64_t ev_end, const kaas_stream_out *outs,
+                            int n_outs) {
   cudaStream_t s = (cudaStream_t)stream;
+  if (n_outs < 0 || (n_outs > 0 && !outs)) return fail(KAAS_E_INVALID, "null stream-out specs");
   if (join_event) {
     KAAS_CUDA(cudaEventRecord((cudaEvent_t)join_event, (cudaStream_t)join_stream));
     KAAS_CUDA(cudaStreamWaitEvent(s, (cudaEvent_t)join_event, 0));
   }
   if (ev_start) KAAS_CUDA(cudaEventRecord((cudaEvent_t)ev_start, s));
-  if (const int rc = kaas_launch_batch_memo(dev, stream, descs, n, memo_key)) return rc;
+  int rc = 1;
+  if (memo_key && n > 0 && descs) {
+    // a memoised Jacobi chain whose stream-outs are exactly its last sweep's
+    // x_out / resid: relaunch it with those as its write-back destinations
+    StreamScratch *sc = scratch_for(s);
+    float *wb_x = nullptr, *wb_r = nullptr;
+    bool ok = sc && sc->dev == dev && sc->jac_memo_key == memo_key && descs[n - 1].kernel == KAAS_K_JACOBI;
+    for (int o = 0; o < n_outs && ok; ++o) {
+      const kaas_stream_out &so = outs[o];
+      ok = so.desc_index == n - 1 && so.host_dst &&
+           so.bytes <= descs[n - 1].sizes[so.arg_index == 3 ? 3 : 4] &&
+           (so.arg_index == 3 || so.arg_index == 4);
+      if (ok) (so.arg_index == 3 ? wb_x : wb_r) = (float *)so.host_dst;
+    }
+    if (ok) {
+      KAAS_CUDA(cudaSetDevice(dev));
+      if ((rc = coop_serialise_begin(dev, s))) return rc;
+      rc = coop_serialise_end(dev, s, launch_jacobi_memo(s, dev, sc, wb_x, wb_r));
+      if (rc != 0 && rc != 1) return rc;
+    }
+  }
+  if (rc == 1 && (rc = launch_batch_impl(dev, stream, descs, n, outs, n_outs, memo_key))) return rc;
   if (ev_end) KAAS_CUDA(cudaEventRecord((cudaEvent_t)ev_end, s));
   return 0;
 }
@@ -870,11 +893,24 @@ static int launch_batch_impl(int dev, uint64_t stream, const kaas_launch_desc *d
       JacobiChain c{(int)plans[i].ext[0], plans[i].cov, (const float *)descs[i].ptrs[0],
                     (const float *)descs[i].ptrs[1], run, xin.data(),
                     (float *const *)xout.data(), (float *const *)res.data()};
+      // stream-outs of the run's last sweep's x_out / resid: written back by
+      // the kernel itself when it can (else copied below)
+      int wb_o[2] = {-1, -1};
+      for (int o = 0; o < n_outs; ++o)
+        if (!done_out[o] && outs[o].desc_index == i + run - 1 && (outs[o].arg_index == 3 || outs[o].arg_index == 4))
+          wb_o[outs[o].arg_index - 3] = o;
+      bool wb_done = false;
+      c.wb_x = wb_o[0] >= 0 ? (float *)outs[wb_o[0]].host_dst : nullptr;
+      c.wb_r = wb_o[1] >= 0 ? (float *)outs[wb_o[1]].host_dst : nullptr;
+      c.wb_done = &wb_done;
       int rc;
       if ((rc = coop_serialise_begin(dev, s))) return rc;
       // the whole batch is this one run: the caller's memo key may name it
       if ((rc = coop_serialise_end(dev, s, launch_jacobi_chain(s, dev, c, sc, (i == 0 && run == n) ? memo_key : 0))))
         return rc;
+      if (wb_done)
+        for (int q = 0; q < 2; ++q)
+          if (wb_o[q] >= 0) done_out[wb_o[q]] = 1;
       i += run;
       continue;
     }

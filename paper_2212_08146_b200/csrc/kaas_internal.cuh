@@ -116,11 +116,17 @@ struct JacobiChain {
   const float *const *x_in;  // [sweeps]
   float *const *x_out;       // [sweeps]
   float *const *resid;       // [sweeps]
+  // host (pinned, device-accessible) destinations the on-chip kernel writes
+  // the LAST sweep's x_out / resid to as well (nullptr: none); *wb_done is
+  // set when the chosen kernel did (otherwise the caller copies)
+  float *wb_x = nullptr, *wb_r = nullptr;
+  bool *wb_done = nullptr;
 };
 int launch_jacobi_chain(cudaStream_t s, int dev, const JacobiChain &c, StreamScratch *sc,
                         uint64_t memo_key = 0);
-// relaunch the memoised chain of sc (returns 1 when there is none to relaunch)
-int launch_jacobi_memo(cudaStream_t s, int dev, StreamScratch *sc);
+// relaunch the memoised chain of sc with these write-back destinations
+// (returns 1 when there is none to relaunch)
+int launch_jacobi_memo(cudaStream_t s, int dev, StreamScratch *sc, float *wb_x = nullptr, float *wb_r = nullptr);
 void free_jacobi_memo(StreamScratch *sc);
 // Prepared-operand buffers for cGEMM (nullptr = use per-stream scratch).
 struct CgemmPrepared {

@@ -36,6 +36,7 @@ from __future__ import annotations
 
 import itertools
 import threading
+import os
 import time
 
 from collections import OrderedDict, deque
@@ -206,6 +207,8 @@ class DeviceStats:
 
 
 # keys naming one immutable descriptor table (kaas_launch_batch_memo); never reused
+# dev A/B only: KAAS_DEV_NO_WB=1 turns the Jacobi in-kernel write-back off
+_NO_WB = os.environ.get("KAAS_DEV_NO_WB") == "1"
 _DESC_KEYS = itertools.count(1)
 
 
@@ -243,7 +246,8 @@ class _Plan:
     request costs a few numpy ops on the host instead of ~4 ms of Python."""
 
     __slots__ = ("error", "kernels", "fail_at", "fail_exc", "advance_ns", "per_inv",
-                 "template", "slots", "names", "dirty_names", "n", "stream_outs", "prepared",
+                 "template", "slots", "names", "dirty_names", "n", "stream_outs", "wb_outs", "wb_arr",
+                 "wb_next", "prepared",
                  "last_ptrs", "last_descs", "last_key", "skip_zero")
 
 
@@ -286,7 +290,7 @@ class _Req:
     and ``complete`` (device done, store puts, response)."""
 
     __slots__ = ("seq", "req", "response", "pending", "graveyard", "keepalive", "events",
-                 "has_kernels", "has_fills", "streamed")
+                 "has_kernels", "has_fills", "streamed", "wb")
 
     def __init__(self, seq, req):
         self.seq = seq
@@ -299,6 +303,7 @@ class _Req:
         self.has_kernels = False
         self.has_fills = False
         self.streamed = {}
+        self.wb = False        # streamed buffers written back on the exec stream (by the kernel)
 
 
 class GpuExecutor:
@@ -734,6 +739,21 @@ class GpuExecutor:
                 if not later and all(o[2] != nm for o in outs):
                     outs = [o for o in outs if o[2] != nm] + [(i, 2, nm)]
         p.stream_outs = tuple(outs)
+        # a request ending in a jacobi_sweep: its keyed x_out / resid are
+        # written back to their host blobs by the chain kernel itself (no D2H
+        # copy after it; kaas_launch_batch_timed copies when it cannot)
+        wb = []
+        if (p.fail_at is None and req.invocations and kernels[-1].kernel_id == "jacobi_sweep" and not outs
+                and not _NO_WB):
+            last = req.invocations[-1]
+            for ai in (3, 4):
+                nm = last.args[ai]
+                arg = by_name[nm]
+                if not arg.is_ephemeral and arg.key is not None and all(w[2] != nm for w in wb):
+                    wb.append((len(req.invocations) - 1, ai, nm))
+        p.wb_outs = tuple(wb)
+        p.wb_arr = None   # native.StreamOut array for wb_outs, built on first launch
+        p.wb_next = None  # host blobs for the next launch, allocated after this one
         # operands whose prepared forms may be cached: const inputs the request
         # does not rewrite -- cgemm's split A / expanded B, matmul's Bt
         prep = []
@@ -1001,10 +1021,30 @@ class GpuExecutor:
                     plan.last_key = memo_key = next(_DESC_KEYS)
             filled = self._attach_prepared(plan, descs, resolved) if plan.prepared else ()
             if one_call:
+                wb = None
+                if plan.wb_outs:
+                    # the write-back blobs were allocated after the previous
+                    # launch of this plan: nothing but two field stores here
+                    blobs = plan.wb_next or [PinnedBlob(resolved[nm].size) for _, _, nm in plan.wb_outs]
+                    plan.wb_next = None
+                    wb = plan.wb_arr
+                    if wb is None:
+                        wb = plan.wb_arr = (native.StreamOut * len(plan.wb_outs))()
+                        for o, (di, ai, nm) in enumerate(plan.wb_outs):
+                            wb[o].desc_index, wb[o].arg_index = di, ai
+                            wb[o].out_stream, wb[o].bytes = self.s_exec.handle, resolved[nm].size
+                    for o, (_, _, nm) in enumerate(plan.wb_outs):
+                        blob = blobs[o]
+                        rec.keepalive.append(blob)
+                        rec.streamed[nm] = blob
+                        wb[o].host_dst = blob.addr
+                    rec.wb = True
                 # s_exec waits for everything enqueued on s_in so far (the fills)
                 native.launch_batch_timed(self.device, self.s_exec, descs, memo_key, self.s_in,
                                           ev[5] if timed and rec.has_fills else self._ev_fill,
-                                          ev[2] if timed else None, ev[3] if timed else None)
+                                          ev[2] if timed else None, ev[3] if timed else None, wb)
+                if plan.wb_outs:  # the next launch's write-back blobs, off its critical path
+                    plan.wb_next = [PinnedBlob(resolved[nm].size) for _, _, nm in plan.wb_outs]
                 self.dev_stats.resolve()  # earlier requests' spans, while this one runs
                 for slot in filled:
                     slot[2] = True  # later launches on s_exec are ordered after the fill
@@ -1073,7 +1113,7 @@ class GpuExecutor:
         # kernel-end -> flush-done tail was 13 us).  With requests pipelined,
         # they go on the copy-out stream so the next request's kernels
         # overlap them.
-        alone = not rec.streamed and len(self._inflight) == 0
+        alone = rec.wb or (not rec.streamed and len(self._inflight) == 0)
         fs = self.s_exec if alone else self.s_out
         if rec.has_fills and not rec.has_kernels:
             # no kernel joined the fills: the request's end event must not

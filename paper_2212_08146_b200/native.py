@@ -136,7 +136,8 @@ EXPORTS = {
     # descriptor tables go in as void*: a ctypes array or a numpy buffer's address
     "kaas_launch_batch": [C.c_int, _u64, C.c_void_p, C.c_int],
     "kaas_launch_batch_memo": [C.c_int, _u64, C.c_void_p, C.c_int, _u64],
-    "kaas_launch_batch_timed": [C.c_int, _u64, C.c_void_p, C.c_int, _u64, _u64, _u64, _u64, _u64],
+    "kaas_launch_batch_timed": [C.c_int, _u64, C.c_void_p, C.c_int, _u64, _u64, _u64, _u64, _u64,
+                                C.c_void_p, C.c_int],
     "kaas_launch_batch_ex": [C.c_int, _u64, C.c_void_p, C.c_int,
                              C.POINTER(StreamOut), C.c_int],
 }
@@ -384,16 +385,28 @@ def host_free(addr: int) -> None:
 
 def launch_batch_timed(dev: int, stream: Stream, descs, memo_key: int = 0, join_stream: Stream | None = None,
                        join_event: Event | None = None, ev_start: Event | None = None,
-                       ev_end: Event | None = None) -> None:
-    """launch_batch (no stream-outs) with the join / kernel-span events in the
-    same crossing (kaas_launch_batch_timed)."""
+                       ev_end: Event | None = None, outs=None) -> None:
+    """launch_batch with the join / kernel-span events in the same crossing
+    (kaas_launch_batch_timed).  ``outs``: (desc_index, arg_index, host_addr,
+    nbytes) write-backs that are complete once ``ev_end`` is (a fused Jacobi
+    chain writes its last sweep there from the kernel; anything else is
+    copied on ``stream`` after the batch)."""
     n = len(descs)
     ptr = descs.__array_interface__["data"][0] if isinstance(descs, np.ndarray) else descs
+    arr, n_outs = None, 0
+    if isinstance(outs, C.Array):  # a prebuilt StreamOut array (the caller keeps it current)
+        arr, n_outs = outs, len(outs)
+    elif outs:
+        n_outs = len(outs)
+        arr = (StreamOut * n_outs)()
+        for i, (di, ai, addr, nb) in enumerate(outs):
+            arr[i].desc_index, arr[i].arg_index = di, ai
+            arr[i].out_stream, arr[i].host_dst, arr[i].bytes = stream.handle, addr, nb
     rc = _fn("kaas_launch_batch_timed")(dev, stream.handle, ptr, n, memo_key,
                                         join_stream.handle if join_event is not None else 0,
                                         join_event.handle if join_event is not None else 0,
                                         ev_start.handle if ev_start is not None else 0,
-                                        ev_end.handle if ev_end is not None else 0)
+                                        ev_end.handle if ev_end is not None else 0, arr, n_outs)
     if rc:
         check(rc, "kaas_launch_batch_timed")
 
