@@ -818,9 +818,11 @@ int kaas_launch_batch_timed(int dev, uint64_t stream, const kaas_launch_desc *de
     bool ok = sc && sc->dev == dev && sc->jac_memo_key == memo_key && descs[n - 1].kernel == KAAS_K_JACOBI;
     for (int o = 0; o < n_outs && ok; ++o) {
       const kaas_stream_out &so = outs[o];
+      // the kernel writes exactly x[0:n] (arg 3) / the one residual (arg 4)
+      const uint64_t nx = 4 * (uint64_t)descs[n - 1].lits[0].i;
       ok = so.desc_index == n - 1 && so.host_dst &&
-           so.bytes <= descs[n - 1].sizes[so.arg_index == 3 ? 3 : 4] &&
-           (so.arg_index == 3 || so.arg_index == 4);
+           ((so.arg_index == 3 && so.bytes == nx && descs[n - 1].sizes[3] == nx) ||
+            (so.arg_index == 4 && so.bytes == 4 && descs[n - 1].sizes[4] == 4));
       if (ok) (so.arg_index == 3 ? wb_x : wb_r) = (float *)so.host_dst;
     }
     if (ok) {
@@ -896,9 +898,16 @@ static int launch_batch_impl(int dev, uint64_t stream, const kaas_launch_desc *d
       // stream-outs of the run's last sweep's x_out / resid: written back by
       // the kernel itself when it can (else copied below)
       int wb_o[2] = {-1, -1};
-      for (int o = 0; o < n_outs; ++o)
-        if (!done_out[o] && outs[o].desc_index == i + run - 1 && (outs[o].arg_index == 3 || outs[o].arg_index == 4))
-          wb_o[outs[o].arg_index - 3] = o;
+      const uint64_t nx = 4 * (uint64_t)plans[i].ext[0];
+      for (int o = 0; o < n_outs; ++o) {
+        const kaas_stream_out &so = outs[o];
+        const int last = i + run - 1;
+        // the kernel writes exactly x[0:n] / the one residual
+        if (!done_out[o] && so.desc_index == last &&
+            ((so.arg_index == 3 && so.bytes == nx && descs[last].sizes[3] == nx) ||
+             (so.arg_index == 4 && so.bytes == 4 && descs[last].sizes[4] == 4)))
+          wb_o[so.arg_index - 3] = o;
+      }
       bool wb_done = false;
       c.wb_x = wb_o[0] >= 0 ? (float *)outs[wb_o[0]].host_dst : nullptr;
       c.wb_r = wb_o[1] >= 0 ? (float *)outs[wb_o[1]].host_dst : nullptr;

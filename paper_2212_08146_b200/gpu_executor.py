@@ -746,10 +746,14 @@ class GpuExecutor:
         if (p.fail_at is None and req.invocations and kernels[-1].kernel_id == "jacobi_sweep" and not outs
                 and not _NO_WB):
             last = req.invocations[-1]
-            for ai in (3, 4):
+            n_ = last.literals[0].value
+            for ai, nbytes in ((3, 4 * n_), (4, 4)):
                 nm = last.args[ai]
                 arg = by_name[nm]
-                if not arg.is_ephemeral and arg.key is not None and all(w[2] != nm for w in wb):
+                # the kernel writes exactly x[0:n] / the one residual: a
+                # larger buffer's tail must come from the device copy
+                if (not arg.is_ephemeral and arg.key is not None and arg.size == nbytes
+                        and all(w[2] != nm for w in wb)):
                     wb.append((len(req.invocations) - 1, ai, nm))
         p.wb_outs = tuple(wb)
         p.wb_arr = None   # native.StreamOut array for wb_outs, built on first launch

@@ -384,6 +384,36 @@ def test_run_fusions_edge_cases(gpu):
         assert canon(store.get(f"fu/{key}")) == canon(ostore.get(f"fu/{key}")), key
 
 
+@pytest.mark.parametrize("pad", [0, 64])
+def test_jacobi_kernel_write_back(gpu, pad):
+    """The fused chain writes its last sweep's x / resid straight into the
+    request's host blobs; an output buffer larger than the n values the
+    kernel writes takes the copy path instead (its zero tail must survive).
+    Both byte-identical to the flush of the same request on the oracle."""
+    ex, store = gpu
+    n, sweeps = 2048, 12
+    pfx = f"jw{pad}"
+    A, b = W.seed_jacobi(store, n, prefix=pfx)
+    req = W.jacobi_request(pfx, n, sweeps, f"{pfx}/A/{n}", f"{pfx}/b/{n}", f"{pfx}/x0/{n}", f"{pfx}/x", f"{pfx}/r")
+    if pad:
+        bufs = tuple(BufferArg(a.name, a.size + pad, a.direction, key=a.key) if a.name == "x" else a
+                     for a in req.buffers)
+        req = KaasRequest(req.request_id, bufs, req.invocations)
+    for _ in range(2):  # first launch builds the chain, the second relaunches the memo
+        _run(ex, req)
+    ostore = DictStore()
+    W.seed_jacobi(ostore, n, prefix=pfx)
+    OracleExecutor(1 << 30, ostore).execute(req)
+    got = np.frombuffer(store.get(f"{pfx}/x"), "<f4")
+    want = np.frombuffer(ostore.get(f"{pfx}/x"), "<f4")
+    assert got.size == want.size == n + pad // 4
+    assert np.all(got[n:] == 0) and np.all(want[n:] == 0)
+    assert np.abs(got[:n].astype(np.float64) - want[:n]).max() <= 1e-5
+    r_got = np.frombuffer(store.get(f"{pfx}/r"), "<f4")[0]
+    r_want = np.frombuffer(ostore.get(f"{pfx}/r"), "<f4")[0]
+    assert abs(float(r_got) - float(r_want)) <= 1e-3 * max(1.0, abs(float(r_want)))
+
+
 @pytest.mark.parametrize("n", [2048, 4096])
 def test_jacobi_every_residual_observable(gpu, n):
     """Each sweep writes its own keyed residual (every sweep is a last writer,
